@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark: FSR/SSR spike-stream reconstruction on B200 (arXiv 2412.11639).
+
+Metric (BASELINE.json): reconstructed frames/s at 400x250, with Gpixel-frames/s
+and the fraction of the HBM roofline.  One "step" = one pass of the hot path
+(bit-packed planes -> one uint8 frame per timestep, all pixels) over the
+BASELINE.json configs[1] workload: the moving scene, 400x250 px, 40,000
+timesteps (synthetic, seeded; the paper's datasets are not available).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--method fsr|ssr]
+    python bench.py --impl reference ...   # the reference CPU implementation
+
+N>1 (torchrun, one rank per GPU): every rank reconstructs its own independent
+stream (stream sharding, BASELINE configs[3] style): weak scaling, no
+data-path collective; time = max over ranks of device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "reconstructed frames/sec at 400x250 (and Gpixel-frames/s); % of HBM roofline"
+W, H, T = 400, 250, 40000
+FPGA_FPS = 20000.0  # FSR/SSR on the XCVU9P FPGA, 400x250
+BYTES_PER_PXF = 1.125  # 1 packed input bit + 1 uint8 output byte
+CPU_SAMPLE_FRAMES = 2000
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """NVML samples of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 -- clocks are reported as unavailable
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def report(self):
+        if not self.nv or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ CPU baseline --
+def cpu_reference_fps(planes_host: np.ndarray, pitch: int, w: int, h: int, t: int, method: int,
+                      repeats: int = 3):
+    """The reference's own bench() (proj/src/metrics.cpp:63-82) on the host."""
+    from oracle.oracle import Reference, ref_available
+
+    cores = os.cpu_count() or 1
+    if ref_available():
+        fps = Reference().bench_fps(planes_host, pitch, w, h, t, method, 32, repeats, cores)
+        return fps, cores, "reference"
+    from oracle.oracle import Oracle  # C restatement as the port baseline
+    o = Oracle()
+    t0 = time.perf_counter()
+    for _ in range(repeats):
+        o.reconstruct(planes_host, w, h, t, pitch, method, 32, dtype=np.float64, threads=cores)
+    return repeats * t / (time.perf_counter() - t0), cores, "port"
+
+
+def moving_scene_cpu(w: int, h: int, t: int, seed: int) -> np.ndarray:
+    """Host-only generator of the configs[1] moving scene for the reference arm
+    (same construction as the device generator: 16 seeded sinusoids in
+    [0.01, 0.6] translating at 0.05 px/step, an occluding bar at 0.2 px/step,
+    integrate-and-fire with threshold 1 and uniform initial residual).
+    Returns dense SPK1 planes [t, ceil(w*h/8)]."""
+    rng = np.random.default_rng(seed)
+    amp = 0.3 + rng.random(16)
+    fx = 0.004 + 0.06 * rng.random(16)
+    fy = 0.004 + 0.06 * rng.random(16)
+    ph = 2 * np.pi * rng.random(16)
+    bar_x0, bar_w, bar_i = 400 * rng.random(), 12 + 20 * rng.random(), 0.01 + 0.1 * rng.random()
+    # texture on the 0.05-px lattice: x - 0.05 n = 0.05 * (20 x - n)
+    k = np.arange(-(t - 1), 20 * (w - 1) + 1)
+    ys = np.arange(h)
+    arg = 2 * np.pi * (fx[None, None, :] * (0.05 * k)[None, :, None] +
+                       fy[None, None, :] * ys[:, None, None]) + ph
+    tex = (0.5 + 0.5 * (amp * np.sin(arg)).sum(-1) / amp.sum())
+    tex = np.clip(0.01 + 0.59 * tex, 0.01, 0.6).astype(np.float32)  # [h, len(k)]
+    xs = np.arange(w)
+    idx = (20 * xs)[None, :] + (t - 1)  # index of k = 20x - n at n = 0
+    residual = rng.random((h, w))
+    rate_sum = np.zeros((h, w))
+    fired = np.zeros((h, w))
+    fb = (w * h + 7) // 8
+    planes = np.zeros((t, fb), np.uint8)
+    for n in range(t):
+        q = tex[:, idx[0] - n].astype(np.float64)
+        bx = np.fmod(bar_x0 + 0.2 * n, w + bar_w) - bar_w
+        inbar = (xs >= bx) & (xs < bx + bar_w)
+        q[:, inbar] = np.float32(bar_i)
+        rate_sum += q
+        bit = residual + rate_sum - fired >= 1.0 - 1e-9
+        fired += bit
+        planes[n] = np.packbits(bit.reshape(-1), bitorder="little")[:fb]
+    return planes
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    method = {"fsr": 0, "ssr": 1}[args.method]
+    tcpu = CPU_SAMPLE_FRAMES
+    planes = moving_scene_cpu(W, H, tcpu, 0)
+    pitch = planes.shape[1]
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference_fps(planes, pitch, W, H, tcpu, method, repeats=3)
+    rates = []
+    for _ in range(args.steps):
+        fps_i, cores, kind = cpu_reference_fps(planes, pitch, W, H, tcpu, method, repeats=3)
+        rates.append(fps_i)
+    fps = float(np.median(rates))
+    total = args.steps * tcpu / fps
+    sample = (f"configs[1] moving scene, frames [0,{tcpu}) of 400x250 (host-generated); per step "
+              f"the reference bench() (median of 3 reconstruct() calls, {cores} workers)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": fps / FPGA_FPS, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "configs[1] moving 400x250x40000 (bounded CPU sample)",
+                   "method": args.method, "width": W, "height": H, "frames": tcpu},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- GPU arm --
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--method", default="fsr", choices=["fsr", "ssr"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--frames", type=int, default=T)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_11639_b200 as spk
+    from paper_2412_11639_b200 import _capi as capi
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    frames = args.frames
+    lib = capi.lib()
+
+    # each rank: its own seeded stream (stream sharding; weak scaling)
+    vol = spk.synth("moving", rank, W, H, frames, device=dev)
+    out = torch.empty((frames, W * H), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(method):
+        spk.reconstruct(vol, method, out=out)
+
+    def timed(method, steps, warmup):
+        for _ in range(warmup):
+            step(method)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        lib.spk_launch_count(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            step(method)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        launches = lib.spk_launch_count(1)
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms, launches
+
+    def kernel_times(method, steps):
+        """mean per-kernel device time (CUDA events on the launch stream)"""
+        import ctypes as C
+        fs, fe, ff = C.c_float(), C.c_float(), C.c_float()
+        seg, exp = [], []
+        lib.spk_set_timing(1)
+        for _ in range(steps):
+            step(method)
+            capi.check(lib.spk_last_timing(C.byref(fs), C.byref(fe), C.byref(ff)))
+            seg.append(fs.value)
+            exp.append(fe.value)
+        lib.spk_set_timing(0)
+        return float(np.mean(seg)), float(np.mean(exp))
+
+    sampler = ClockSampler(local)
+    with sampler:
+        ms, launches = timed(args.method, args.steps, args.warmup)
+    clocks = sampler.report()
+    seg_ms, exp_ms = kernel_times(args.method, max(3, min(20, args.steps)))
+    other = "ssr" if args.method == "fsr" else "fsr"
+    k2 = max(5, args.steps // 5)
+    ms2, _ = timed(other, k2, 3)
+    seg2, exp2 = kernel_times(other, max(3, min(20, k2)))
+
+    peak, peak_kind = peaks()
+    pxf = W * H * frames
+    ms_step = ms / args.steps
+    fps = world * frames / (ms_step * 1e-3)
+    gpxf = world * pxf / (ms_step * 1e-3) / 1e9
+
+    def roofline(seg, exp):
+        # dominant kernel: algorithmic bytes per launch / its mean duration
+        if exp >= seg:
+            kern, alg = "k_expand", pxf * 1.0
+            dur = exp
+        else:
+            kern, alg = "k_segment", pxf * 0.125
+            dur = seg
+        achieved = alg / (dur * 1e-3) / 1e9
+        traffic = None
+        tf = ROOT / "profiles" / f"traffic_{kern}_{args.method}.json"
+        if tf.exists():
+            traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+        return {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_kind": peak_kind, "kernel_ms": dur,
+                "step_frac": pxf * BYTES_PER_PXF / (ms_step * 1e-3) / 1e9 / peak,
+                "segment_ms": seg, "expand_ms": exp}
+
+    line = {
+        "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": fps / FPGA_FPS, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": f"configs[1] moving 400x250x{frames}", "method": args.method,
+                   "width": W, "height": H, "frames": frames,
+                   "parallelism": f"streams x{world} (one independent stream per GPU)",
+                   "l2": "no flush: 0.5 GB in + 4 GB out per step > 126 MB L2",
+                   "vs_baseline_ref": "FPGA 20,000 FPS (BASELINE.md, PAPER.md:199)"},
+        "gpx_frames_per_s": gpxf,
+        "roofline": roofline(seg_ms, exp_ms),
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        other: {"value": world * frames / (ms2 / k2 * 1e-3),
+                "ms_per_step": ms2 / k2,
+                "roofline": roofline(seg2, exp2)},
+    }
+
+    # end to end through the C-ABI host boundary (pinned host buffers)
+    if not args.no_e2e:
+        payload = torch.from_numpy(vol.payload()).pin_memory()
+        hout = torch.empty((frames, W * H), dtype=torch.uint8).pin_memory()
+        from paper_2412_11639_b200.recon import reconstruct_host_ptr
+        reconstruct_host_ptr(payload.data_ptr(), W, H, frames, args.method, capi.SPK_OUT_U8,
+                             hout.data_ptr(), W * H)  # warm
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            reconstruct_host_ptr(payload.data_ptr(), W, H, frames, args.method, capi.SPK_OUT_U8,
+                                 hout.data_ptr(), W * H)
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        check = hout[:, :].numpy()
+        assert np.array_equal(check[-1], out[-1].cpu().numpy()), "e2e result differs"
+        line["e2e"] = {"value": world * frames * args.e2e_steps / el, "unit": "frames/s",
+                       "h2d_bytes_per_step": int(payload.numel()),
+                       "d2h_bytes_per_step": int(hout.numel()),
+                       "path": "spk_reconstruct_host (C-ABI, pinned host in/out)"}
+
+    if rank == 0 and not args.no_cpu:
+        tcpu = min(CPU_SAMPLE_FRAMES, frames)
+        host = vol.planes[:tcpu].cpu().numpy()
+        fps_cpu, cores, kind = cpu_reference_fps(host, vol.pitch, W, H, tcpu,
+                                                 0 if args.method == "fsr" else 1)
+        line["cpu_baseline"] = {"value": fps_cpu, "unit": "frames/s", "cores": cores,
+                                "kind": kind,
+                                "sample": f"frames [0,{tcpu}) of the same stream, reference "
+                                          f"bench() median of 3, {cores} workers"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,143 @@
+/*
+ * spikecam_b200.h -- C-ABI of the B200-native spike-camera reconstruction path.
+ *
+ * Plain C, no torch or CUDA types in the signatures (streams are passed as
+ * `void*` holding a cudaStream_t, 0 = legacy default stream).  The library is
+ * libspikecam_b200.so, built in-tree by __graft_entry__.build().
+ *
+ * Each entry point replaces one reference interface (paths relative to the
+ * reference checkout, /root/reference):
+ *
+ *   spk_reconstruct_u8     reconstruct() (proj/src/reconstruct.cpp:441-471)
+ *                          followed by quantize() (proj/src/io.cpp:78-81) -- the
+ *                          uint8 frame the CLI writes per timestep
+ *                          (proj/tools/spikecam_main.cpp:174-179)
+ *   spk_reconstruct_f64    reconstruct() values, bit-exact doubles
+ *                          (proj/include/spikecam/reconstruct.hpp:73-79)
+ *   spk_reconstruct_f32    the same values rounded to float
+ *   spk_segment            segment_fsr / segment_ssr run lists
+ *                          (proj/src/reconstruct.cpp:107-130, 198-211)
+ *   spk_pack_bytes         pack_frame (proj/src/io.cpp:52-64): SpikeVolume bytes
+ *                          (proj/include/spikecam/core.hpp:32-33) -> SPK1 planes
+ *   spk_unpack_planes      unpack_frame (proj/src/io.cpp:66-76), incl. msb_first
+ *   spk_upload_planes      read_spk / read_raw payload ingest
+ *                          (proj/src/io.cpp:185-223) into the pitched device layout
+ *   spk_reconstruct_host   the host-buffer boundary of reconstruct(): host SPK1
+ *                          payload in, host frames out
+ *
+ * Error behaviour mirrors the reference's exceptions: SPK_EINVAL where the
+ * reference throws std::invalid_argument (bad method / window / geometry,
+ * proj/src/reconstruct.cpp:177-186, proj/src/core.cpp:11-13), SPK_ECUDA /
+ * SPK_ENOMEM for device failures (std::runtime_error in the C++ wrapper).
+ * spk_last_error() returns the calling thread's last message.
+ *
+ * Device data layout:
+ *   planes : T bit-planes, plane n at d_planes + n*plane_pitch; pixel
+ *            p = y*W + x is bit (p & 7) of byte (p >> 3), LSB-first (SPK1).
+ *            plane_pitch must be a multiple of 4 and >= 4*ceil(W*H/32).
+ *   output : T frame planes, frame n at d_out + n*out_pitch elements, pixel p
+ *            at element p (row-major W*H).  out_pitch >= W*H.
+ */
+#ifndef SPIKECAM_B200_H
+#define SPIKECAM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPK_OK 0
+#define SPK_EINVAL 1
+#define SPK_ECUDA 2
+#define SPK_ENOMEM 3
+
+/* ReconMethod::kind (proj/include/spikecam/reconstruct.hpp:10-18) */
+#define SPK_FSR 0
+#define SPK_SSR 1
+#define SPK_TFI 2
+#define SPK_TFP 3
+
+#define SPK_OUT_U8 0
+#define SPK_OUT_F32 1
+#define SPK_OUT_F64 2
+
+typedef struct spk_geom {
+    int32_t width;      /* W >= 1 */
+    int32_t height;     /* H >= 1 */
+    int64_t frames;     /* T >= 0, < 2^29 */
+    size_t plane_pitch; /* bytes between consecutive bit-planes */
+} spk_geom;
+
+/* One stable run of one pixel: frames [start, next run's start) -- or
+ * [start, last_spike) for the final run -- holding `intervals` intervals.
+ * Value = 255 * intervals / span (proj/src/reconstruct.cpp:124). */
+typedef struct spk_run {
+    uint32_t start;
+    uint32_t intervals;
+} spk_run;
+
+/* ---- device-resident path (asynchronous on `stream`) -------------------- */
+int spk_reconstruct_u8(const spk_geom* g, const void* d_planes, int method, int tfp_window,
+                       uint8_t* d_out, size_t out_pitch, void* stream);
+int spk_reconstruct_f32(const spk_geom* g, const void* d_planes, int method, int tfp_window,
+                        float* d_out, size_t out_pitch, void* stream);
+int spk_reconstruct_f64(const spk_geom* g, const void* d_planes, int method, int tfp_window,
+                        double* d_out, size_t out_pitch, void* stream);
+
+/* FSR / SSR runs of every pixel: pixel p's runs at d_runs[p*run_cap ...],
+ * its run count in d_counts[p] (a count > run_cap means the list was
+ * truncated), its last spike frame in d_last[p] (-1 if none). */
+int spk_segment(const spk_geom* g, const void* d_planes, int method, spk_run* d_runs,
+                int64_t run_cap, uint32_t* d_counts, int32_t* d_last, void* stream);
+
+/* one byte per bit (frame-major n*W*H + p, nonzero = spike) <-> planes */
+int spk_pack_bytes(const spk_geom* g, const uint8_t* d_bytes, void* d_planes, void* stream);
+int spk_unpack_planes(const spk_geom* g, const void* d_planes, uint8_t* d_bytes, void* stream);
+
+/* Host payload (planes `src_pitch` bytes apart; dense SPK1 payload:
+ * src_pitch = ceil(W*H/8)) -> pitched device planes; msb_first reverses the
+ * in-byte bit order of raw dumps (proj/src/io.cpp:72). */
+int spk_upload_planes(const spk_geom* g, const void* h_payload, size_t src_pitch,
+                      int msb_first, void* d_planes, void* stream);
+
+/* ---- host-buffer boundary (synchronous) ---------------------------------- */
+/* h_payload: dense SPK1 payload (T planes of ceil(W*H/8) bytes; g->plane_pitch
+ * is ignored).  out_type SPK_OUT_U8/F32/F64; h_out frame-major with
+ * out_pitch elements per frame.  Runs on the current CUDA device. */
+int spk_reconstruct_host(const spk_geom* g, const void* h_payload, int method, int tfp_window,
+                         int out_type, void* h_out, size_t out_pitch);
+
+/* ---- configuration / diagnostics ------------------------------------------ */
+/* run-list capacity per pixel used by spk_reconstruct_*: 0 = automatic
+ * (max(64, T/32)).  Pixels that overflow it are recomputed exactly by a
+ * slower direct-write pass, so results never depend on this value. */
+int spk_set_run_capacity(int64_t per_pixel);
+/* device bytes the pitched plane layout needs per frame for W*H pixels */
+size_t spk_plane_pitch(int32_t width, int32_t height);
+/* kernels launched by this thread since the last call (and reset) */
+int64_t spk_launch_count(int reset);
+/* Per-phase device timing of this thread's next spk_reconstruct_* calls:
+ * when enabled, CUDA events are recorded on the call's stream around the
+ * segment (K2), expand (K3) and fixup kernels (or the single TFI/TFP kernel,
+ * reported as `expand`).  spk_last_timing waits for the last call's events and
+ * returns milliseconds (negative if a phase did not run). */
+int spk_set_timing(int enable);
+int spk_last_timing(float* segment_ms, float* expand_ms, float* fixup_ms);
+const char* spk_last_error(void);
+int spk_version(void);
+
+/* ---- synthetic inputs (benchmark / test harness, not the hot path) -------- */
+/* Integrate-and-fire streams (threshold 1, subtractive reset, uniform initial
+ * residual; proj/src/simulator.cpp:41-68) of the BASELINE.json configs:
+ * scene 1 static gradient+texture, 2 moving texture + bar, 3 large sensor
+ * with slow illumination, 5 extreme dynamic range; 0 = uniform random bits
+ * with probability `param` (noise).  frame0 offsets time (time shards). */
+int spk_synth(int scene, uint64_t seed, const spk_geom* g, int64_t frame0, double param,
+              void* d_planes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

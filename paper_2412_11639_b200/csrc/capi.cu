@@ -1,0 +1,460 @@
+// capi.cu -- the C-ABI of libspikecam_b200.so (declared in include/spikecam_b200.h).
+//
+// Validation mirrors the reference's exceptions (SPK_EINVAL where it throws
+// std::invalid_argument), workspaces come from the device's stream-ordered
+// memory pool (cudaMallocAsync: no host synchronisation, thread-safe across
+// streams), and every kernel launch is counted for the benchmark's
+// `gpu_launches` claim.  There is no CPU fallback: every path launches the
+// sm_100a kernels or returns an error.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cstdio>
+#include <string>
+
+#include "spk_common.cuh"
+#include "spk_fsm.cuh"
+#include "spk_kernels.cuh"
+
+using namespace spk;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+thread_local bool g_timing = false;
+thread_local cudaEvent_t g_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+thread_local int g_ev_used = 0;  // events recorded by the last call
+
+// phase marker k (0..3) on stream s when timing is enabled
+int mark(int k, cudaStream_t s) {
+    if (!g_timing) return SPK_OK;
+    if (!g_ev[k]) {
+        cudaError_t e = cudaEventCreate(&g_ev[k]);
+        if (e != cudaSuccess) return SPK_ECUDA;
+    }
+    cudaEventRecord(g_ev[k], s);
+    g_ev_used = k + 1;
+    return SPK_OK;
+}
+std::atomic<int64_t> g_run_cap{0};
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    cudaGetLastError();  // clear sticky-free errors
+    return e == cudaErrorMemoryAllocation ? SPK_ENOMEM : SPK_ECUDA;
+}
+
+#define SPK_CK(call)                                         \
+    do {                                                     \
+        cudaError_t e_ = (call);                             \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+    } while (0)
+
+#define SPK_LAUNCHED(name)                                   \
+    do {                                                     \
+        ++g_launches;                                        \
+        cudaError_t e_ = cudaGetLastError();                 \
+        if (e_ != cudaSuccess) return cuda_fail(e_, name);   \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int64_t npix_of(const spk_geom* g) { return (int64_t)g->width * (int64_t)g->height; }
+size_t plane_bytes(const spk_geom* g) { return (size_t)((npix_of(g) + 7) / 8); }
+size_t min_pitch(int64_t npix) { return (size_t)((npix + 31) / 32) * 4; }
+
+// SpikeVolume / geometry rules (proj/src/core.cpp:11-13) + device layout rules
+int check_geom(const spk_geom* g, bool check_pitch) {
+    if (!g) return fail(SPK_EINVAL, "spk: null geometry");
+    if (g->width < 1 || g->height < 1 || g->frames < 0)
+        return fail(SPK_EINVAL, "SpikeVolume: width/height must be >= 1, frames >= 0");
+    if (g->frames >= (int64_t)1 << 29)
+        return fail(SPK_EINVAL, "spk: frames must be < 2^29");
+    if (npix_of(g) >= (int64_t)1 << 31) return fail(SPK_EINVAL, "spk: W*H must be < 2^31");
+    if (check_pitch && (g->plane_pitch % 4 != 0 || g->plane_pitch < min_pitch(npix_of(g))))
+        return fail(SPK_EINVAL, "spk: plane_pitch must be a multiple of 4 and >= 4*ceil(W*H/32)");
+    return SPK_OK;
+}
+
+// ReconMethod::parse rules (proj/src/reconstruct.cpp:177-186)
+int check_method(int method, int window) {
+    if (method < SPK_FSR || method > SPK_TFP)
+        return fail(SPK_EINVAL, "unknown reconstruction method: " + std::to_string(method));
+    if (method == SPK_TFP && window < 1) return fail(SPK_EINVAL, "tfp window must be >= 1");
+    return SPK_OK;
+}
+
+int run_capacity(int64_t frames) {
+    int64_t cap = g_run_cap.load();
+    if (cap <= 0) cap = std::max<int64_t>(64, frames / 32);
+    cap = std::min<int64_t>(cap, std::max<int64_t>(1, frames));
+    return (int)cap;
+}
+
+void ensure_pool(int dev) {
+    static std::atomic<uint64_t> done{0};
+    if (dev < 0 || dev >= 64) return;
+    const uint64_t bit = 1ull << dev;
+    if (done.load() & bit) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;  // keep freed workspaces cached in the pool
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done.fetch_or(bit);
+}
+
+// RAII stream-ordered scratch
+struct Scratch {
+    void* p = nullptr;
+    cudaStream_t s;
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s); }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+
+int launch_segment(int method, const SegArgs& a, cudaStream_t s) {
+    const int64_t nwords = (a.npix + 31) / 32;
+    const int64_t threads = nwords * 32;
+    const unsigned blocks = (unsigned)((threads + kSegThreads - 1) / kSegThreads);
+    if (method == SPK_FSR)
+        k_segment<kFSR><<<blocks, kSegThreads, 0, s>>>(a);
+    else
+        k_segment<kSSR><<<blocks, kSegThreads, 0, s>>>(a);
+    SPK_LAUNCHED("k_segment");
+    return SPK_OK;
+}
+
+template <typename OUT>
+int launch_expand(const SegArgs& sa, OUT* out, size_t out_pitch, cudaStream_t s) {
+    ExpArgs e;
+    e.runs = sa.runs;
+    e.tbl = sa.tbl;
+    e.counts = sa.counts;
+    e.last = sa.last;
+    e.npix = sa.npix;
+    e.frames = sa.frames;
+    e.cap = sa.cap;
+    e.out = out;
+    e.pitch = out_pitch;
+    e.vec_ok = ((reinterpret_cast<uintptr_t>(out) | (out_pitch * sizeof(OUT))) & 15) == 0;
+    const int64_t per_block = (int64_t)kExpThreads * kExpPix;
+    const unsigned bx = (unsigned)((sa.npix + per_block - 1) / per_block);
+    for (int c0 = 0; c0 < sa.nchunks; c0 += 65535) {
+        e.chunk0 = c0;
+        const unsigned by = (unsigned)std::min(65535, sa.nchunks - c0);
+        k_expand<OUT><<<dim3(bx, by), kExpThreads, 0, s>>>(e);
+        SPK_LAUNCHED("k_expand");
+    }
+    return SPK_OK;
+}
+
+template <typename OUT>
+int launch_fixup(int method, const SegArgs& sa, OUT* out, size_t out_pitch, cudaStream_t s) {
+    const unsigned blocks = (unsigned)((sa.npix + 127) / 128);
+    if (method == SPK_FSR)
+        k_fixup<kFSR, OUT><<<blocks, 128, 0, s>>>(sa, out, out_pitch);
+    else
+        k_fixup<kSSR, OUT><<<blocks, 128, 0, s>>>(sa, out, out_pitch);
+    SPK_LAUNCHED("k_fixup");
+    return SPK_OK;
+}
+
+template <typename OUT>
+int launch_causal(const spk_geom* g, const void* planes, int method, int window, OUT* out,
+                  size_t out_pitch, cudaStream_t s) {
+    CausalArgs c;
+    c.planes = planes;
+    c.pitch = g->plane_pitch;
+    c.npix = npix_of(g);
+    c.frames = (int)g->frames;
+    c.window = method == SPK_TFP ? window : 1;
+    c.out = out;
+    c.out_pitch = out_pitch;
+    const int lut_cap = (int)(32768 / sizeof(OUT));
+    if (method == SPK_TFI)
+        c.lut_n = sizeof(OUT) == 1 ? 512 : 1024;
+    else
+        c.lut_n = window + 1 <= lut_cap ? window + 1 : 0;
+    const size_t lut_bytes = ((size_t)c.lut_n * sizeof(OUT) + 15) & ~(size_t)15;
+    const size_t smem = lut_bytes + (size_t)kCausalWarps * 32 * (32 * sizeof(OUT) + 16);
+    const int64_t nwords = (c.npix + 31) / 32;
+    const unsigned blocks = (unsigned)((nwords + kCausalWarps - 1) / kCausalWarps);
+    auto go = [&](auto kern) -> int {
+        if (smem > 48 * 1024)
+            SPK_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<blocks, kCausalWarps * 32, smem, s>>>(c);
+        SPK_LAUNCHED("k_causal");
+        return SPK_OK;
+    };
+    return method == SPK_TFI ? go(k_causal<kTFI, OUT>) : go(k_causal<kTFP, OUT>);
+}
+
+template <typename OUT>
+int reconstruct_impl(const spk_geom* g, const void* planes, int method, int window, OUT* out,
+                     size_t out_pitch, void* stream) {
+    int rc = check_geom(g, true);
+    if (rc) return rc;
+    if ((rc = check_method(method, window))) return rc;
+    const int64_t npix = npix_of(g);
+    if (g->frames == 0) return SPK_OK;
+    if (!planes || !out) return fail(SPK_EINVAL, "spk: null device buffer");
+    if (out_pitch < (size_t)npix) return fail(SPK_EINVAL, "spk: out_pitch must be >= W*H");
+    cudaStream_t s = as_stream(stream);
+    g_ev_used = 0;
+    if (method == SPK_TFI || method == SPK_TFP) {
+        mark(0, s);
+        mark(1, s);
+        rc = launch_causal<OUT>(g, planes, method, window, out, out_pitch, s);
+        mark(2, s);
+        return rc;
+    }
+
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    SegArgs a;
+    a.planes = planes;
+    a.pitch = g->plane_pitch;
+    a.npix = npix;
+    a.frames = (int)g->frames;
+    a.cap = run_capacity(g->frames);
+    a.nchunks = (int)((g->frames + kChunk - 1) / kChunk);
+    Scratch runs(s), tbl(s), counts(s), last(s);
+    SPK_CK(runs.alloc((size_t)npix * a.cap * sizeof(spk_run_t)));
+    SPK_CK(tbl.alloc((size_t)npix * a.nchunks * sizeof(int32_t)));
+    SPK_CK(counts.alloc((size_t)npix * sizeof(uint32_t)));
+    SPK_CK(last.alloc((size_t)npix * sizeof(int32_t)));
+    a.runs = static_cast<spk_run_t*>(runs.p);
+    a.tbl = static_cast<int32_t*>(tbl.p);
+    a.counts = static_cast<uint32_t*>(counts.p);
+    a.last = static_cast<int32_t*>(last.p);
+    mark(0, s);
+    if ((rc = launch_segment(method, a, s))) return rc;
+    mark(1, s);
+    if ((rc = launch_expand<OUT>(a, out, out_pitch, s))) return rc;
+    mark(2, s);
+    rc = launch_fixup<OUT>(method, a, out, out_pitch, s);
+    mark(3, s);
+    return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spk_reconstruct_u8(const spk_geom* g, const void* d_planes, int method, int tfp_window,
+                       uint8_t* d_out, size_t out_pitch, void* stream) {
+    return reconstruct_impl<uint8_t>(g, d_planes, method, tfp_window, d_out, out_pitch, stream);
+}
+
+int spk_reconstruct_f32(const spk_geom* g, const void* d_planes, int method, int tfp_window,
+                        float* d_out, size_t out_pitch, void* stream) {
+    return reconstruct_impl<float>(g, d_planes, method, tfp_window, d_out, out_pitch, stream);
+}
+
+int spk_reconstruct_f64(const spk_geom* g, const void* d_planes, int method, int tfp_window,
+                        double* d_out, size_t out_pitch, void* stream) {
+    return reconstruct_impl<double>(g, d_planes, method, tfp_window, d_out, out_pitch, stream);
+}
+
+int spk_segment(const spk_geom* g, const void* d_planes, int method, spk_run* d_runs,
+                int64_t run_cap, uint32_t* d_counts, int32_t* d_last, void* stream) {
+    int rc = check_geom(g, true);
+    if (rc) return rc;
+    if (method != SPK_FSR && method != SPK_SSR)
+        return fail(SPK_EINVAL, "spk_segment: method must be fsr or ssr");
+    if (run_cap < 1 || run_cap > INT_MAX) return fail(SPK_EINVAL, "spk_segment: bad run_cap");
+    const int64_t npix = npix_of(g);
+    cudaStream_t s = as_stream(stream);
+    if (g->frames == 0) {
+        SPK_CK(cudaMemsetAsync(d_counts, 0, (size_t)npix * sizeof(uint32_t), s));
+        SPK_CK(cudaMemsetAsync(d_last, 0xff, (size_t)npix * sizeof(int32_t), s));
+        return SPK_OK;
+    }
+    if (!d_planes || !d_runs || !d_counts || !d_last)
+        return fail(SPK_EINVAL, "spk: null device buffer");
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    SegArgs a;
+    a.planes = d_planes;
+    a.pitch = g->plane_pitch;
+    a.npix = npix;
+    a.frames = (int)g->frames;
+    a.cap = (int)run_cap;
+    a.nchunks = (int)((g->frames + kChunk - 1) / kChunk);
+    Scratch tbl(s);
+    SPK_CK(tbl.alloc((size_t)npix * a.nchunks * sizeof(int32_t)));
+    a.runs = d_runs;
+    a.tbl = static_cast<int32_t*>(tbl.p);
+    a.counts = d_counts;
+    a.last = d_last;
+    return launch_segment(method, a, s);
+}
+
+int spk_pack_bytes(const spk_geom* g, const uint8_t* d_bytes, void* d_planes, void* stream) {
+    int rc = check_geom(g, true);
+    if (rc) return rc;
+    if (g->frames == 0) return SPK_OK;
+    if (!d_bytes || !d_planes) return fail(SPK_EINVAL, "spk: null device buffer");
+    const int64_t total = g->frames * (int64_t)g->plane_pitch;
+    const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 64);
+    k_pack<<<blocks, 256, 0, as_stream(stream)>>>(d_bytes, npix_of(g), g->frames,
+                                                  static_cast<uint8_t*>(d_planes), g->plane_pitch);
+    SPK_LAUNCHED("k_pack");
+    return SPK_OK;
+}
+
+int spk_unpack_planes(const spk_geom* g, const void* d_planes, uint8_t* d_bytes, void* stream) {
+    int rc = check_geom(g, true);
+    if (rc) return rc;
+    if (g->frames == 0) return SPK_OK;
+    if (!d_bytes || !d_planes) return fail(SPK_EINVAL, "spk: null device buffer");
+    const int64_t total = g->frames * (int64_t)plane_bytes(g);
+    const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 64);
+    k_unpack<<<blocks, 256, 0, as_stream(stream)>>>(static_cast<const uint8_t*>(d_planes),
+                                                    g->plane_pitch, npix_of(g), g->frames, d_bytes);
+    SPK_LAUNCHED("k_unpack");
+    return SPK_OK;
+}
+
+int spk_upload_planes(const spk_geom* g, const void* h_payload, size_t src_pitch, int msb_first,
+                      void* d_planes, void* stream) {
+    int rc = check_geom(g, true);
+    if (rc) return rc;
+    if (g->frames == 0) return SPK_OK;
+    const size_t row = plane_bytes(g);
+    if (!h_payload || !d_planes || src_pitch < row)
+        return fail(SPK_EINVAL, "spk_upload_planes: bad buffer or src_pitch");
+    cudaStream_t s = as_stream(stream);
+    if (g->plane_pitch > row)  // deterministic pad bytes
+        SPK_CK(cudaMemsetAsync(d_planes, 0, g->plane_pitch * (size_t)g->frames, s));
+    SPK_CK(cudaMemcpy2DAsync(d_planes, g->plane_pitch, h_payload, src_pitch, row,
+                             (size_t)g->frames, cudaMemcpyHostToDevice, s));
+    if (msb_first) {
+        const int64_t total = g->frames * (int64_t)row;
+        const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 64);
+        k_bitrev_bytes<<<blocks, 256, 0, s>>>(static_cast<uint8_t*>(d_planes), g->plane_pitch, row,
+                                              g->frames);
+        SPK_LAUNCHED("k_bitrev_bytes");
+    }
+    return SPK_OK;
+}
+
+size_t spk_plane_pitch(int32_t width, int32_t height) {
+    const int64_t npix = (int64_t)width * height;
+    return (min_pitch(npix) + 15) & ~(size_t)15;  // 16-B rows: vector/TMA friendly
+}
+
+int spk_reconstruct_host(const spk_geom* g, const void* h_payload, int method, int tfp_window,
+                         int out_type, void* h_out, size_t out_pitch) {
+    spk_geom dg = *g;
+    dg.plane_pitch = spk_plane_pitch(g->width, g->height);
+    int rc = check_geom(&dg, true);
+    if (rc) return rc;
+    if ((rc = check_method(method, tfp_window))) return rc;
+    if (out_type < SPK_OUT_U8 || out_type > SPK_OUT_F64)
+        return fail(SPK_EINVAL, "spk_reconstruct_host: bad out_type");
+    const int64_t npix = npix_of(g);
+    if (out_pitch < (size_t)npix) return fail(SPK_EINVAL, "spk: out_pitch must be >= W*H");
+    if (g->frames == 0) return SPK_OK;
+    if (!h_payload || !h_out) return fail(SPK_EINVAL, "spk: null host buffer");
+    const size_t esz = out_type == SPK_OUT_U8 ? 1 : out_type == SPK_OUT_F32 ? 4 : 8;
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    cudaStream_t s;
+    SPK_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    rc = [&]() -> int {
+        Scratch planes(s), out(s);
+        SPK_CK(planes.alloc(dg.plane_pitch * (size_t)g->frames));
+        SPK_CK(out.alloc(out_pitch * esz * (size_t)g->frames));
+        int r = spk_upload_planes(&dg, h_payload, plane_bytes(g), 0, planes.p, s);
+        if (r) return r;
+        if (out_type == SPK_OUT_U8)
+            r = spk_reconstruct_u8(&dg, planes.p, method, tfp_window, static_cast<uint8_t*>(out.p),
+                                   out_pitch, s);
+        else if (out_type == SPK_OUT_F32)
+            r = spk_reconstruct_f32(&dg, planes.p, method, tfp_window, static_cast<float*>(out.p),
+                                    out_pitch, s);
+        else
+            r = spk_reconstruct_f64(&dg, planes.p, method, tfp_window, static_cast<double*>(out.p),
+                                    out_pitch, s);
+        if (r) return r;
+        SPK_CK(cudaMemcpyAsync(h_out, out.p, out_pitch * esz * (size_t)g->frames,
+                               cudaMemcpyDeviceToHost, s));
+        return SPK_OK;
+    }();
+    cudaError_t se = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (rc) return rc;
+    if (se != cudaSuccess) return cuda_fail(se, "cudaStreamSynchronize");
+    return SPK_OK;
+}
+
+int spk_set_run_capacity(int64_t per_pixel) {
+    if (per_pixel < 0 || per_pixel > INT_MAX) return fail(SPK_EINVAL, "spk: bad run capacity");
+    g_run_cap.store(per_pixel);
+    return SPK_OK;
+}
+
+int64_t spk_launch_count(int reset) {
+    const int64_t n = g_launches;
+    if (reset) g_launches = 0;
+    return n;
+}
+
+int spk_set_timing(int enable) {
+    g_timing = enable != 0;
+    return SPK_OK;
+}
+
+int spk_last_timing(float* segment_ms, float* expand_ms, float* fixup_ms) {
+    float* outs[3] = {segment_ms, expand_ms, fixup_ms};
+    for (float* o : outs)
+        if (o) *o = -1.f;
+    if (g_ev_used < 2) return fail(SPK_EINVAL, "spk_last_timing: no timed call");
+    SPK_CK(cudaEventSynchronize(g_ev[g_ev_used - 1]));
+    for (int k = 0; k + 1 < g_ev_used; ++k) {
+        float ms = 0.f;
+        SPK_CK(cudaEventElapsedTime(&ms, g_ev[k], g_ev[k + 1]));
+        if (outs[k]) *outs[k] = ms;
+    }
+    return SPK_OK;
+}
+
+const char* spk_last_error(void) { return g_err.c_str(); }
+
+int spk_version(void) { return 100; }
+
+int spk_synth(int scene, uint64_t seed, const spk_geom* g, int64_t frame0, double param,
+              void* d_planes, void* stream) {
+    int rc = check_geom(g, true);
+    if (rc) return rc;
+    if (scene < 0 || scene > 5 || scene == 4) return fail(SPK_EINVAL, "spk_synth: bad scene");
+    if (frame0 < 0) return fail(SPK_EINVAL, "spk_synth: frame0 < 0");
+    if (g->frames == 0) return SPK_OK;
+    if (!d_planes) return fail(SPK_EINVAL, "spk: null device buffer");
+    cudaStream_t s = as_stream(stream);
+    SPK_CK(cudaMemsetAsync(d_planes, 0, g->plane_pitch * (size_t)g->frames, s));
+    const int64_t threads = (npix_of(g) + 31) / 32 * 32;
+    k_synth<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(
+        scene, seed, g->width, g->height, g->frames, frame0, param,
+        static_cast<uint8_t*>(d_planes), g->plane_pitch);
+    SPK_LAUNCHED("k_synth");
+    return SPK_OK;
+}
+
+}  // extern "C"

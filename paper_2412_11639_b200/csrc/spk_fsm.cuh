@@ -1,0 +1,200 @@
+// spk_fsm.cuh -- per-pixel streaming FSR / SSR stability state machine.
+//
+// One instance per pixel, fed the pixel's spike frames in increasing order.
+// It reproduces the reference's batch segmentation exactly:
+//   FSR  = fsr_runs_into            (proj/src/reconstruct.cpp:40-53)
+//   SSR  = fsr_runs_into followed by ssr_refine_into (reconstruct.cpp:64-99)
+// and emits every closed run as (start frame, interval count, end frame) to an
+// Emitter.  Runs tile [first spike, last spike) with no gap (a run closed at a
+// violating interval ends at that interval's opening spike, which starts the
+// next run -- reconstruct.cpp:366-371).
+//
+// The zero-order rule (PairScanner, reconstruct.cpp:17-36) is kept as
+// (lo, hw): accepted values are [lo, lo + hw] with hw in {0, 1}; "empty" is
+// lo = kNoPair.  The common case -- the interval is already in the pair --
+// is a single unsigned compare `(t - lo) <= hw`; everything else (first
+// spikes, pair completion, violations) goes to the general slow path.
+//
+// SSR keeps one second-level state per value of the current FSR pair, indexed
+// by value (slot A = lo, slot B = lo + 1) instead of first-occurrence order as
+// in ssr_refine_into's Level2[2]; the two are the same states relabelled, and
+// the relabelling is applied when the pair completes downwards (lo -> lo-1).
+// A second-level violation closes the sub-run, resets only the second-level
+// states (the FSR pair continues), and the violating interval reopens its
+// slot -- exactly ssr_refine_into's restart at `broke` (reconstruct.cpp:95-96).
+#pragma once
+
+#include "spk_common.cuh"
+
+// host+device so the state machine can also be unit-tested on the CPU
+// (tests/native/fsm_host.cu); the product only runs it on the GPU.
+#define SPK_HD __host__ __device__ __forceinline__
+
+namespace spk {
+
+enum { kFSR = 0, kSSR = 1, kTFI = 2, kTFP = 3 };
+
+template <int METHOD>
+struct Fsm {
+    int last;   // last spike frame (kNoSpike before the first spike)
+    int first;  // first spike frame
+    int rs;     // start frame of the open (sub-)run
+    int cnt;    // intervals in the open (sub-)run
+    int lo;     // FSR pair: accepted [lo, lo + hw]
+    uint32_t hw;
+    int nrun;   // runs emitted so far
+    // SSR second level (unused for FSR; the compiler drops them)
+    int ii;           // S1 index of the next interval
+    int lA, lB;       // S1 index of the value's last occurrence in the sub-run
+    int gAlo, gBlo;   // pair rule over that value's occurrence gaps
+    uint32_t gAhw, gBhw;
+
+    SPK_HD void init() {
+        last = kNoSpike;
+        first = 0;
+        rs = 0;
+        cnt = 0;
+        lo = kNoPair;
+        hw = 0;
+        nrun = 0;
+        ii = 0;
+        lA = lB = kNoIdx;
+        gAlo = gBlo = kNoPair;
+        gAhw = gBhw = 0;
+    }
+
+    SPK_HD void ssr_reset_to(int k) {
+        // fresh second-level states; the current interval (value lo + k) is
+        // the first occurrence of its value in the new sub-run
+        lA = k == 0 ? ii : kNoIdx;
+        lB = k == 1 ? ii : kNoIdx;
+        gAlo = gBlo = kNoPair;
+        gAhw = gBhw = 0;
+    }
+
+    // pair rule on one second-level slot; returns false on a violation
+    SPK_HD static bool gap_take(int& l, int& glo, uint32_t& ghw, int idx) {
+        if (l == kNoIdx) {
+            l = idx;
+            return true;
+        }
+        const int gap = idx - l;
+        if (glo == kNoPair) {
+            glo = gap;
+            ghw = 0;
+            l = idx;
+            return true;
+        }
+        const int gd = gap - glo;
+        if (gd == 0 || (ghw && gd == 1)) {
+            l = idx;
+            return true;
+        }
+        if (!ghw && (gd == 1 || gd == -1)) {
+            if (gd == -1) glo = gap;
+            ghw = 1;
+            l = idx;
+            return true;
+        }
+        return false;
+    }
+
+    template <class E>
+    SPK_HD void slow(int n, E& em) {
+        if (last == kNoSpike) {  // first spike: lead [0, n) stays 0
+            first = rs = last = n;
+            return;
+        }
+        const int t = n - last;
+        if (lo == kNoPair) {  // first interval fixes the pair's first value
+            lo = t;
+            hw = 0;
+            cnt = 1;
+            if (METHOD == kSSR) {
+                ssr_reset_to(0);
+                ++ii;
+            }
+            last = n;
+            return;
+        }
+        const int d = t - lo;
+        bool ok = d == 0 || (hw && d == 1);
+        if (!ok && !hw && (d == 1 || d == -1)) {  // pair completes
+            hw = 1;
+            if (d == -1) {
+                lo = t;
+                if (METHOD == kSSR) {  // old value lo is now slot B
+                    int tl = lA, tg = gAlo;
+                    uint32_t th = gAhw;
+                    lA = lB; gAlo = gBlo; gAhw = gBhw;
+                    lB = tl; gBlo = tg; gBhw = th;
+                }
+            }
+            ok = true;
+        }
+        if (!ok) {  // first-order violation: close the run at `last`
+            em.run(rs, cnt, last, nrun);
+            ++nrun;
+            rs = last;
+            lo = t;
+            hw = 0;
+            cnt = 1;
+            if (METHOD == kSSR) {
+                ssr_reset_to(0);
+                ++ii;
+            }
+            last = n;
+            return;
+        }
+        if (METHOD == kSSR) {
+            const int k = t - lo;
+            const bool gok = k == 0 ? gap_take(lA, gAlo, gAhw, ii) : gap_take(lB, gBlo, gBhw, ii);
+            if (!gok) {  // second-order violation: close the sub-run at `last`
+                em.run(rs, cnt, last, nrun);
+                ++nrun;
+                rs = last;
+                cnt = 0;
+                ssr_reset_to(k);
+            }
+            ++ii;
+        }
+        ++cnt;
+        last = n;
+    }
+
+    // one spike at frame n (frames strictly increasing)
+    template <class E>
+    SPK_HD void spike(int n, E& em) {
+        const int t = n - last;
+        const int d = t - lo;
+        if ((uint32_t)d > hw) {
+            slow(n, em);
+            return;
+        }
+        if (METHOD == kSSR) {
+            const int l = d ? lB : lA;
+            const int glo = d ? gBlo : gAlo;
+            const uint32_t ghw = d ? gBhw : gAhw;
+            if ((uint32_t)((ii - l) - glo) > ghw) {
+                slow(n, em);
+                return;
+            }
+            if (d) lB = ii; else lA = ii;
+            ++ii;
+        }
+        ++cnt;
+        last = n;
+    }
+
+    // end of stream: close the open run; the tail [last, T) carries its value
+    template <class E>
+    SPK_HD void finish(int frames, E& em) {
+        if (lo != kNoPair) {
+            em.run(rs, cnt, last, nrun);
+            ++nrun;
+        }
+        em.done(first, last == kNoSpike ? -1 : last, nrun, frames);
+    }
+};
+
+}  // namespace spk

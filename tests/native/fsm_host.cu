@@ -1,0 +1,45 @@
+// Host build of the product's streaming FSR/SSR state machine
+// (paper_2412_11639_b200/csrc/spk_fsm.cuh) for CPU unit tests: the exact
+// header the sm_100a kernels use, driven frame by frame on the CPU and
+// compared with the oracle in tests/test_fsm_host.py.  Test code only.
+#include <cstdint>
+
+#include "../../paper_2412_11639_b200/csrc/spk_fsm.cuh"
+
+namespace {
+struct Collect {
+    long* start;
+    long* end;
+    long* cnt;
+    long cap;
+    long n = 0;
+    void run(int rs, int c, int e, int) {
+        if (n < cap) {
+            start[n] = rs;
+            end[n] = e;
+            cnt[n] = c;
+        }
+        ++n;
+    }
+    void done(int, int, int, int) {}
+};
+}  // namespace
+
+extern "C" long fsm_runs(const uint8_t* bits, long frames, int method, long* start, long* end,
+                         long* cnt, long cap) {
+    Collect em{start, end, cnt, cap};
+    if (method == 0) {
+        spk::Fsm<spk::kFSR> f;
+        f.init();
+        for (long n = 0; n < frames; ++n)
+            if (bits[n]) f.spike((int)n, em);
+        f.finish((int)frames, em);
+    } else {
+        spk::Fsm<spk::kSSR> f;
+        f.init();
+        for (long n = 0; n < frames; ++n)
+            if (bits[n]) f.spike((int)n, em);
+        f.finish((int)frames, em);
+    }
+    return em.n;
+}

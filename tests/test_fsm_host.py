@@ -1,0 +1,77 @@
+"""The product's streaming FSR/SSR state machine (csrc/spk_fsm.cuh), compiled
+for the host by nvcc, reproduces the oracle's batch segmentation exactly.
+
+This is the header the sm_100a segment kernel runs; testing it on the CPU
+pins the state-machine logic independently of the GPU plumbing.
+"""
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+SRC = ROOT / "tests" / "native" / "fsm_host.cu"
+LIB = ROOT / "tests" / "native" / "libfsm_host.so"
+HDR = ROOT / "paper_2412_11639_b200" / "csrc" / "spk_fsm.cuh"
+
+
+@pytest.fixture(scope="module")
+def fsm():
+    if not LIB.exists() or LIB.stat().st_mtime < max(SRC.stat().st_mtime, HDR.stat().st_mtime):
+        subprocess.run(["nvcc", "-O2", "-std=c++17", "-arch=sm_100a", "-Xcompiler", "-fPIC",
+                        "-shared", "-diag-suppress", "20011", f"-I{ROOT / 'include'}", "-o",
+                        str(LIB), str(SRC)], check=True)
+    h = C.CDLL(str(LIB))
+    h.fsm_runs.restype = C.c_long
+    h.fsm_runs.argtypes = [C.c_void_p, C.c_long, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                           C.c_long]
+
+    def run(bits, m):
+        cap = bits.size + 1
+        s, e, c = (np.zeros(cap, np.int64) for _ in range(3))
+        n = h.fsm_runs(bits.ctypes.data, bits.size, m, s.ctypes.data, e.ctypes.data,
+                       c.ctypes.data, cap)
+        return s[:n], e[:n], c[:n]
+    return run
+
+
+def if_stream(rng, t, segs, flips):
+    b = np.zeros(t, np.uint8)
+    r = rng.random()
+    for k in range(segs):
+        q = rng.uniform(0.005, 1.0)
+        for n in range(k * t // segs, (k + 1) * t // segs):
+            r += q
+            if r >= 1 - 1e-9:
+                b[n] = 1
+                r -= 1
+    return b ^ (rng.random(t) < flips).astype(np.uint8)
+
+
+@pytest.mark.parametrize("family", ["noise", "if", "if_noisy", "if_rare_flips"])
+def test_fsm_matches_oracle(fsm, oracle, family):
+    rng = np.random.default_rng(hash(family) % 2**32)
+    for _ in range(2500):
+        t = int(rng.integers(0, 700))
+        if family == "noise":
+            b = (rng.random(t) < rng.uniform(0.01, 0.95)).astype(np.uint8)
+        else:
+            flips = {"if": 0.0, "if_noisy": 0.03, "if_rare_flips": 0.002}[family]
+            b = if_stream(rng, t, int(rng.integers(1, 5)), flips)
+        for m in (0, 1):
+            got, want = fsm(b, m), oracle.runs(b, m)
+            assert all(np.array_equal(x, y) for x, y in zip(got, want)), (family, m, t)
+
+
+def test_fsm_golden_rows(fsm, golden_dir):
+    z = np.load(golden_dir / "rows.npz")
+    for name in sorted({k.split("/")[0] for k in z.files}):
+        bits = z[f"{name}/bits"]
+        for m, tag in ((0, "fsr"), (1, "ssr")):
+            s, e, n = z[f"{name}/{tag}_seg"]
+            keep = n > 0
+            got = fsm(bits, m)
+            assert np.array_equal(got[0], s[keep]) and np.array_equal(got[1], e[keep]) \
+                and np.array_equal(got[2], n[keep]), (name, tag)

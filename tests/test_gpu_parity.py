@@ -1,0 +1,282 @@
+"""GPU parity: the sm_100a path (through the C-ABI) vs the reference's outputs.
+
+Bars (BASELINE.json north_star): bit-exact for uint8 frames, run/interval
+counts and f64 values; float32 within 1e-5 relative (F32_RTOL below).
+Expected values come from tests/golden (the reference library's own outputs)
+or from the oracle restatement (oracle/liboracle.so) on seeded inputs.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2412_11639_b200 as spk
+from paper_2412_11639_b200 import _capi as capi
+
+pytestmark = pytest.mark.gpu
+
+F32_RTOL = 1e-5
+FSR, SSR, TFI, TFP = 0, 1, 2, 3
+TAGS = {"fsr": (FSR, 32), "ssr": (SSR, 32), "tfi": (TFI, 32), "tfp32": (TFP, 32),
+        "tfp16": (TFP, 16), "tfp3": (TFP, 3)}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    yield
+    capi.lib().spk_set_run_capacity(0)
+
+
+def method_of(tag):
+    m, w = TAGS[tag]
+    return spk.ReconMethod(spk.Method(m), w)
+
+
+def run(vol, m, dtype=torch.uint8, out=None):
+    o = spk.reconstruct(vol, m, dtype=dtype, out=out)
+    torch.cuda.synchronize()
+    return o
+
+
+def host2d(t, npix):
+    return t.reshape(t.shape[0], -1)[:, :npix].cpu().numpy()
+
+
+def f32_close(got32, want64):
+    want = want64.astype(np.float64)
+    err = np.abs(got32.astype(np.float64) - want)
+    return bool(np.all(err <= F32_RTOL * np.maximum(np.abs(want), 1e-30)))
+
+
+# --------------------------------------------------------------- golden -----
+@pytest.mark.parametrize("vol", ["par12x9", "bar64x48", "noise40x25", "odd9x1", "odd13x7"])
+def test_golden_volumes_all_methods(golden_dir, vol):
+    z = np.load(golden_dir / f"vol_{vol}.npz")
+    w, h, t = (int(v) for v in z["geom"])
+    v = spk.PackedVolume.from_payload(z["planes"], w, h, t)
+    for tag in sorted({k.split("/")[0] for k in z.files if "/" in k}):
+        m = method_of(tag)
+        u8 = host2d(run(v, m), w * h)
+        assert np.array_equal(u8, z[f"{tag}/u8"]), (vol, tag)
+        f64 = host2d(run(v, m, torch.float64), w * h)
+        assert hashlib.sha256(f64.tobytes()).digest() == z[f"{tag}/f64_sha256"].tobytes(), (vol, tag)
+        f32 = host2d(run(v, m, torch.float32), w * h)
+        assert f32_close(f32, f64), (vol, tag)
+
+
+def test_golden_rows_as_single_pixels(golden_dir):
+    z = np.load(golden_dir / "rows.npz")
+    names = sorted({k.split("/")[0] for k in z.files})
+    for name in names:
+        bits = z[f"{name}/bits"]
+        t = bits.size
+        planes = bits.reshape(t, 1).astype(np.uint8)  # 1x1 volume: bit 0 of each plane
+        v = spk.PackedVolume.from_payload(planes, 1, 1, t)
+        for tag, (m, win) in (("fsr", (FSR, 32)), ("ssr", (SSR, 32)), ("tfi", (TFI, 32)),
+                              ("tfp32", (TFP, 32)), ("tfp7", (TFP, 7)), ("tfp1", (TFP, 1))):
+            want = z[f"{name}/{tag}_pix"]
+            meth = spk.ReconMethod(spk.Method(m), win)
+            f64 = run(v, meth, torch.float64).reshape(-1).cpu().numpy()
+            assert np.array_equal(f64.view(np.uint64), want.view(np.uint64)), (name, tag)
+            u8 = run(v, meth).reshape(-1).cpu().numpy()
+            q = np.floor(np.clip(want, 0, 255) + 0.5).astype(np.uint8)  # round-half-away, v >= 0
+            assert np.array_equal(u8, q), (name, tag)
+
+
+# -------------------------------------------------------- seeded vs oracle --
+SCENES = [("noise", 0.3), ("static", 0), ("moving", 0), ("sensor", 0), ("range", 0),
+          ("noise", 0.05)]
+
+
+@pytest.mark.parametrize("scene,param", SCENES)
+def test_synthetic_scenes_vs_oracle(oracle, scene, param):
+    w, h, t = 100, 24, 3000
+    v = spk.synth(scene, 11, w, h, t, param=param)
+    host = v.planes.cpu().numpy()
+    for tag in ("fsr", "ssr", "tfi", "tfp32", "tfp3"):
+        m, win = TAGS[tag]
+        want = oracle.reconstruct(host, w, h, t, v.pitch, m, win)
+        got = host2d(run(v, method_of(tag)), w * h)
+        assert np.array_equal(got, want), (scene, tag, int((got != want).sum()))
+    for tag in ("fsr", "ssr"):
+        m, win = TAGS[tag]
+        want = oracle.reconstruct(host, w, h, t, v.pitch, m, win, dtype=np.float64)
+        got = host2d(run(v, method_of(tag), torch.float64), w * h)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (scene, tag)
+
+
+@pytest.mark.parametrize("cap", [1, 2, 5])
+def test_run_capacity_overflow_is_exact(oracle, cap):
+    """Pixels whose run list overflows take the direct-write fixup path."""
+    w, h, t = 64, 5, 2500
+    v = spk.synth("noise", 5, w, h, t, param=0.4)
+    host = v.planes.cpu().numpy()
+    capi.check(capi.lib().spk_set_run_capacity(cap))
+    try:
+        for tag in ("fsr", "ssr"):
+            m, _ = TAGS[tag]
+            want = oracle.reconstruct(host, w, h, t, v.pitch, m)
+            assert np.array_equal(host2d(run(v, method_of(tag)), w * h), want), tag
+            want64 = oracle.reconstruct(host, w, h, t, v.pitch, m, dtype=np.float64)
+            got64 = host2d(run(v, method_of(tag), torch.float64), w * h)
+            assert np.array_equal(got64.view(np.uint64), want64.view(np.uint64)), tag
+    finally:
+        capi.lib().spk_set_run_capacity(0)
+
+
+@pytest.mark.parametrize("w,h,t", [(1, 1, 1), (1, 1, 2), (7, 5, 31), (33, 3, 33), (40, 1, 1023),
+                                   (17, 19, 1025), (500, 3, 2049), (31, 1, 4097), (3, 3, 0)])
+def test_edge_geometries(oracle, w, h, t):
+    v = spk.synth("noise", w * 1000 + t, w, h, t, param=0.35)
+    host = v.planes.cpu().numpy()
+    for tag in ("fsr", "ssr", "tfi", "tfp32", "tfp3"):
+        m, win = TAGS[tag]
+        want = oracle.reconstruct(host, w, h, t, v.pitch, m, win) if t else np.zeros((0, w * h))
+        got = host2d(run(v, method_of(tag)), w * h) if t else np.zeros((0, w * h))
+        assert np.array_equal(got, want), (w, h, t, tag)
+
+
+@pytest.mark.parametrize("extra", [0, 3, 16, 61])
+def test_out_pitch_and_alignment(oracle, extra):
+    """Caller-owned `out` with a row pitch > W*H (aligned and unaligned)."""
+    w, h, t = 48, 10, 1500
+    v = spk.synth("moving", 2, w, h, t)
+    host = v.planes.cpu().numpy()
+    for dtype, np_t in ((torch.uint8, np.uint8), (torch.float32, np.float32),
+                        (torch.float64, np.float64)):
+        out = torch.full((t, w * h + extra), 7, dtype=dtype, device="cuda")
+        for tag in ("fsr", "ssr", "tfi", "tfp16"):
+            m, win = TAGS[tag]
+            run(v, method_of(tag), out=out)
+            got = out.cpu().numpy()
+            want = oracle.reconstruct(host, w, h, t, v.pitch, m, win,
+                                      dtype=np.uint8 if np_t == np.uint8 else np.float64)
+            if np_t == np.float32:
+                assert f32_close(got[:, : w * h], want), (extra, tag)
+            else:
+                assert np.array_equal(got[:, : w * h], want), (extra, tag, dtype)
+            if extra:
+                assert np.all(got[:, w * h:] == 7), "wrote outside W*H"
+
+
+def test_segments_match_oracle_runs(oracle):
+    w, h, t = 37, 11, 5000
+    v = spk.synth("moving", 9, w, h, t)
+    bits = oracle.unpack(v.planes.cpu().numpy(), w, h, t, v.pitch)
+    for m in (FSR, SSR):
+        runs, counts, last = spk.segments(v, spk.ReconMethod(spk.Method(m)), run_cap=t)
+        runs, counts, last = runs.cpu().numpy(), counts.cpu().numpy(), last.cpu().numpy()
+        for p in range(w * h):
+            s, e, c = oracle.runs(bits[:, p], m)
+            n = counts[p]
+            assert n == len(s), (m, p)
+            assert np.array_equal(runs[p, :n, 0], s) and np.array_equal(runs[p, :n, 1], c)
+            nz = np.flatnonzero(bits[:, p])
+            assert last[p] == (nz[-1] if nz.size else -1)
+            if n:
+                assert np.array_equal(np.r_[s[1:], last[p]], e)
+
+
+def test_pack_unpack_and_msb_upload(oracle):
+    rng = np.random.default_rng(5)
+    w, h, t = 29, 13, 70
+    bits = (rng.random((t, w * h)) < 0.5).astype(np.uint8)
+    dev_bits = torch.from_numpy(bits).cuda()
+    v = spk.PackedVolume.from_bytes(dev_bits, w, h)
+    fb = spk.plane_bytes(w, h)
+    assert np.array_equal(v.planes.cpu().numpy()[:, :fb], oracle.pack(bits, w, h))
+    assert np.array_equal(v.to_bytes().reshape(t, -1).cpu().numpy(), bits)
+    payload = oracle.pack(bits, w, h)
+    msb = np.array([int(f"{b:08b}"[::-1], 2) for b in payload.reshape(-1)], np.uint8)
+    v2 = spk.PackedVolume.from_payload(msb, w, h, t, msb_first=True)
+    assert np.array_equal(v2.to_bytes().reshape(t, -1).cpu().numpy(), bits)
+    want = oracle.unpack(msb.reshape(t, fb), w, h, t, fb, msb_first=True)
+    assert np.array_equal(want, bits)
+
+
+def test_spk_files_roundtrip(tmp_path, golden_dir):
+    z = np.load(golden_dir / "formats.npz")
+    f = tmp_path / "g.spk"
+    f.write_bytes(z["spk_golden"].tobytes())
+    v, fps = spk.read_spk(f)
+    assert fps == 20000 and (v.width, v.height, v.frames) == (2, 1, 1)
+    assert v.to_bytes().reshape(-1).tolist() == [1, 0]
+    spk.write_spk(v, fps, tmp_path / "back.spk")
+    assert (tmp_path / "back.spk").read_bytes() == z["spk_golden"].tobytes()
+    big = spk.synth("noise", 1021, 400, 250, 32, param=0.5)
+    spk.write_spk(big, 20000, tmp_path / "big.spk")
+    back, _ = spk.read_spk(tmp_path / "big.spk")
+    assert torch.equal(back.to_bytes(), big.to_bytes())
+    raw = tmp_path / "big.raw"
+    raw.write_bytes((tmp_path / "big.spk").read_bytes()[16:])
+    assert torch.equal(spk.read_raw(raw, 400, 250).to_bytes(), big.to_bytes())
+
+
+def test_host_boundary_matches_device_path():
+    w, h, t = 400, 250, 1200
+    v = spk.synth("moving", 4, w, h, t)
+    payload = v.payload()
+    for m in ("fsr", "ssr", "tfi", "tfp"):
+        dev = host2d(run(v, m), w * h)
+        host = spk.reconstruct_host(payload, w, h, t, m)
+        assert np.array_equal(dev, host), m
+    f64 = spk.reconstruct_host(payload, w, h, t, "ssr", dtype=np.float64)
+    assert np.array_equal(f64, host2d(run(v, "ssr", torch.float64), w * h))
+
+
+def test_launch_count_and_determinism():
+    v = spk.synth("static", 1, 400, 250, 2000)
+    capi.lib().spk_launch_count(1)
+    a = run(v, "fsr")
+    assert capi.lib().spk_launch_count(1) == 3  # segment + expand + fixup
+    b = run(v, "fsr")
+    assert torch.equal(a, b)
+    run(v, "tfp")
+    assert capi.lib().spk_launch_count(1) == 1
+
+
+# ------------------------------------------------ BASELINE sizes (properties) --
+def full_size_check(oracle, scene, w, h, t, seed, tiles):
+    v = spk.synth(scene, seed, w, h, t)
+    host = v.planes.cpu().numpy()
+    npix = w * h
+    for tag in ("fsr", "ssr"):
+        m, _ = TAGS[tag]
+        u8 = run(v, method_of(tag))
+        f64 = run(v, method_of(tag), torch.float64)
+        # u8 == quantize(f64) everywhere (round half away from zero, values >= 0)
+        q = torch.floor(f64.clamp(0, 255) + 0.5).to(torch.uint8)
+        assert torch.equal(q, u8), tag
+        del f64, q
+        # exact parity with the oracle on spatial tiles
+        u8h = u8.reshape(t, npix)
+        for p0 in tiles:
+            p1 = min(npix, p0 + 800)
+            want = oracle.reconstruct(host, w, h, t, v.pitch, m, pix_begin=p0, pix_end=p1)
+            assert np.array_equal(u8h[:, p0:p1].cpu().numpy(), want), (scene, tag, p0)
+        # runs tile [first spike, last spike): total intervals == spikes - 1
+        runs, counts, last = spk.segments(v, method_of(tag), run_cap=max(64, t // 8))
+        spikes = v.to_bytes().reshape(t, npix).sum(0, dtype=torch.int64)
+        cap = runs.shape[1]
+        mask = torch.arange(cap, device="cuda")[None, :] < counts[:, None].clamp(max=cap)
+        tot = (runs[..., 1].to(torch.int64) * mask).sum(1)
+        ok = counts <= cap
+        assert torch.equal(tot[ok], (spikes - 1).clamp(min=0)[ok]), tag
+        del u8, u8h, runs
+    return v
+
+
+def test_c1_static_full_size(oracle):
+    """configs[0]: 400x250x20000 static -> one run per pixel (Theorem 1)."""
+    v = full_size_check(oracle, "static", 400, 250, 20000, 0, [0, 50000, 99200])
+    _, counts, _ = spk.segments(v, "fsr", run_cap=4)
+    assert int(counts.max()) == 1
+
+
+def test_c2_moving_full_size(oracle):
+    """configs[1]: 400x250x40000 moving texture + occluding bar."""
+    full_size_check(oracle, "moving", 400, 250, 40000, 0, [0, 37000, 99200])
