@@ -137,8 +137,28 @@ int launch_segment(int method, const SegArgs& a, cudaStream_t s) {
 }
 
 template <typename OUT>
-int launch_expand(const SegArgs& sa, OUT* out, size_t out_pitch, cudaStream_t s) {
+int launch_finalize(const SegArgs& sa, double* vals, cudaStream_t s) {
+    FinArgs f;
+    f.runs = sa.runs;
+    f.vals = vals;
+    f.tbl = sa.tbl;
+    f.counts = sa.counts;
+    f.last = sa.last;
+    f.npix = sa.npix;
+    f.frames = sa.frames;
+    f.cap = sa.cap;
+    f.nchunks = sa.nchunks;
+    const unsigned blocks = (unsigned)((sa.npix + kFinThreads - 1) / kFinThreads);
+    k_finalize<OUT><<<blocks, kFinThreads, 0, s>>>(f);
+    SPK_LAUNCHED("k_finalize");
+    return SPK_OK;
+}
+
+template <typename OUT>
+int launch_expand(const SegArgs& sa, const double* vals, OUT* out, size_t out_pitch,
+                  cudaStream_t s) {
     ExpArgs e;
+    e.vals = vals;
     e.runs = sa.runs;
     e.tbl = sa.tbl;
     e.counts = sa.counts;
@@ -241,9 +261,13 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
     a.counts = static_cast<uint32_t*>(counts.p);
     a.last = static_cast<int32_t*>(last.p);
     mark(0, s);
+    Scratch vals(s);
+    if (sizeof(OUT) == 8) SPK_CK(vals.alloc((size_t)npix * a.cap * sizeof(double)));
     if ((rc = launch_segment(method, a, s))) return rc;
+    if ((rc = launch_finalize<OUT>(a, static_cast<double*>(vals.p), s))) return rc;
     mark(1, s);
-    if ((rc = launch_expand<OUT>(a, out, out_pitch, s))) return rc;
+    if ((rc = launch_expand<OUT>(a, static_cast<const double*>(vals.p), out, out_pitch, s)))
+        return rc;
     mark(2, s);
     rc = launch_fixup<OUT>(method, a, out, out_pitch, s);
     mark(3, s);

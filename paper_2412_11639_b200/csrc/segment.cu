@@ -5,54 +5,20 @@
 //
 // Mapping: one thread per pixel, one warp per 32-bit plane word (32
 // consecutive pixels).  For every group of 32 frames lane i loads the warp's
-// word from plane (32g + i); a 5-stage shuffle transpose turns the 32x32 bit
-// block into one 32-frame word per pixel, and the lane walks its spikes with
-// ffs.  Loads are issued one batch (kBatch groups = 256 frames) ahead.
+// word from plane 32g + (31 - i); a 5-stage shuffle transpose turns the 32x32
+// bit block into one 32-frame word per pixel with the earliest frame in bit
+// 31, and the lane walks its spikes with clz, one spike per warp iteration
+// through the branch-free Scan automaton (spk_fsm.cuh).  Plane loads run one
+// batch (kBatch groups = 256 frames) ahead of the scan.
 //
-// Output per pixel p: runs[p*cap + k] = {start, intervals} for k < cap,
-// counts[p], last[p], and the run table tbl[c*npix + p] = index of the run
-// covering frame c*kChunk (-1 before the first run).  The expand kernel (K3)
-// turns these into frames.  Pixels whose run count exceeds `cap` are
-// recomputed by k_fixup (direct column writes) after K3.
+// Output per pixel p: runs[p*cap + k] = {start frame, intervals} (k < cap),
+// counts[p] (may exceed cap: overflow) and last[p] (last spike, -1 if none).
+// k_finalize (K2b) turns them into run values + the run table for K3;
+// overflowed pixels are rewritten exactly by k_fixup after K3.
 #include "spk_fsm.cuh"
 #include "spk_kernels.cuh"
 
 namespace spk {
-
-namespace {
-
-struct RunEmitter {
-    spk_run_t* runs;  // this pixel's slice
-    int32_t* tbl;     // tbl + p
-    uint32_t* counts;
-    int32_t* lastv;
-    int64_t npix;
-    int cap;
-    int nchunks;
-    int64_t p;
-
-    __device__ __forceinline__ void table(int c0, int c1, int v) {
-        for (int c = c0; c <= c1; ++c) tbl[(int64_t)c * npix] = v;
-    }
-    // run [rs, end) with `cnt` intervals, index idx
-    __device__ void run(int rs, int cnt, int end, int idx) {
-        if (idx < cap) runs[idx] = spk_run_t{(uint32_t)rs, (uint32_t)cnt};
-        table((rs + kChunk - 1) >> kChunkLog2, (end - 1) >> kChunkLog2, idx);
-    }
-    __device__ void done(int first, int last, int nrun, int frames) {
-        if (nrun == 0) {
-            table(0, nchunks - 1, -1);
-        } else {
-            table(0, ((first + kChunk - 1) >> kChunkLog2) - 1, -1);  // lead [0, first)
-            table((last + kChunk - 1) >> kChunkLog2, nchunks - 1, nrun - 1);  // tail
-        }
-        counts[p] = (uint32_t)nrun;
-        lastv[p] = last;
-        (void)frames;
-    }
-};
-
-}  // namespace
 
 template <int METHOD>
 __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
@@ -63,18 +29,22 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     const bool valid = p < a.npix;
     const int frames = a.frames;
     const int ngroups = (frames + 31) >> 5;
+    // lane i loads frame 32g + (31 - i): after the transpose bit 31 is the
+    // group's first frame, so spikes come out in time order with clz
     const char* col = reinterpret_cast<const char*>(a.planes) + word * 4;
     const size_t pitch = a.pitch;
+    const int rev = 31 - lane;
+    spk_run_t* rp = a.runs + (valid ? p * a.cap : 0);
+    const int capm1 = a.cap - 1;
 
-    Fsm<METHOD> fsm;
-    fsm.init();
-    RunEmitter em{a.runs + (valid ? p * a.cap : 0), a.tbl + (valid ? p : 0), a.counts, a.last,
-                  a.npix, a.cap, a.nchunks, p};
+    Scan<METHOD> sc;
+    sc.init();
+    int nrun = 0;
 
     uint32_t nxt[kBatch];
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
-        const int f = j * 32 + lane;
+        const int f = j * 32 + rev;
         nxt[j] = f < frames ? __ldg(reinterpret_cast<const uint32_t*>(col + (size_t)f * pitch)) : 0u;
     }
     for (int g0 = 0; g0 < ngroups; g0 += kBatch) {
@@ -84,7 +54,7 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         if (g0 + kBatch < ngroups) {
 #pragma unroll
             for (int j = 0; j < kBatch; ++j) {
-                const int f = (g0 + kBatch + j) * 32 + lane;
+                const int f = (g0 + kBatch + j) * 32 + rev;
                 nxt[j] = f < frames
                              ? __ldg(reinterpret_cast<const uint32_t*>(col + (size_t)f * pitch))
                              : 0u;
@@ -97,14 +67,26 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
                 if (!valid) w = 0;
                 const int base = (g0 + j) * 32;
                 while (w) {
-                    const int b = __ffs(w) - 1;
-                    w &= w - 1;
-                    fsm.spike(base + b, em);
+                    const int c = __clz(w);
+                    w ^= 0x80000000u >> c;
+                    int rs, cnt;
+                    if (sc.step(base + c, rs, cnt)) {
+                        rp[min(nrun, capm1)] = spk_run_t{(uint32_t)rs, (uint32_t)cnt};
+                        ++nrun;
+                    }
                 }
             }
         }
     }
-    if (valid) fsm.finish(frames, em);
+    if (valid) {
+        int rs, cnt;
+        if (sc.tail(rs, cnt)) {
+            rp[min(nrun, capm1)] = spk_run_t{(uint32_t)rs, (uint32_t)cnt};
+            ++nrun;
+        }
+        a.counts[p] = (uint32_t)nrun;
+        a.last[p] = sc.last == kNoSpike ? -1 : sc.last;
+    }
 }
 
 template __global__ void k_segment<kFSR>(SegArgs);

@@ -197,4 +197,95 @@ struct Fsm {
     }
 };
 
+// ---------------------------------------------------------------------------
+// Scan<METHOD>: the same automaton as Fsm, written branch-free for the warp
+// scan of K2.  A warp advances all 32 pixels one spike per iteration; any
+// data-dependent branch (pair completion, violation, first occurrence...)
+// would serialise the lanes that take it, and with runs every few dozen
+// spikes some lane takes one in most iterations.  Every case is therefore a
+// select, and a closed run is a single predicated 8-byte store of
+// (start frame, intervals); its end is the next run's start (or the pixel's
+// last spike) and its value is computed later by k_finalize.
+//
+// Encodings (frames < 2^29):
+//   lo >= kLim          no interval yet (kNoPair initially; after the first
+//                        spike lo = t >= 2^29 because last = kNoSpike)
+//   SSR slots are indexed by value parity (the pair {lo, lo+1} has one odd
+//   and one even value), so a completing pair never relabels a slot; a slot
+//   whose last occurrence precedes the sub-run start `sub0` is empty, so a
+//   violation resets both slots by moving sub0 only; glo >= kLim = no gap yet.
+constexpr int kLim = 1 << 29;
+
+template <int METHOD>
+struct Scan {
+    int last, lo, rs, cnt, nrun;
+    uint32_t hw;
+    int ii, sub0;         // SSR: S1 index of the next interval, sub-run start
+    int l0, l1, g0, g1;   // SSR: per parity slot: last index, gap pair low
+    uint32_t h0, h1;      //      gap pair width (0/1)
+
+    SPK_HD void init() {
+        last = kNoSpike;
+        lo = kNoPair;
+        rs = cnt = nrun = 0;
+        hw = 0;
+        ii = sub0 = 0;
+        l0 = l1 = kNoIdx;
+        g0 = g1 = kNoPair;
+        h0 = h1 = 0;
+    }
+
+    // returns true when the run (rs, cnt) closed before this spike
+    SPK_HD bool step(int n, int& out_rs, int& out_cnt) {
+        const int t = n - last;
+        const int d = t - lo;
+        const bool in = (uint32_t)d <= hw;
+        const bool ext = !in && hw == 0 && (uint32_t)(d + 1) <= 2u;
+        const bool fbrk = !in && !ext;
+        bool brk = fbrk;
+        bool emit = fbrk && lo < kLim;
+        if (METHOD == kSSR) {
+            const bool k = (t & 1) != 0;
+            const int l = k ? l1 : l0;
+            const int glo = k ? g1 : g0;
+            const uint32_t ghw = k ? h1 : h0;
+            const bool stale = l < sub0;
+            const int gap = ii - l;
+            const int gd = gap - glo;
+            const bool gempty = stale || glo >= kLim;
+            const bool gin = !gempty && (uint32_t)gd <= ghw;
+            const bool gext = !gempty && !gin && ghw == 0 && (uint32_t)(gd + 1) <= 2u;
+            const bool sbrk = !fbrk && !gempty && !gin && !gext;
+            brk = fbrk || sbrk;
+            emit = emit || sbrk;
+            const bool fresh = stale || brk;
+            const int nglo = fresh ? kNoPair : (glo >= kLim ? gap : (gext ? min(glo, gap) : glo));
+            const uint32_t nghw = (fresh || glo >= kLim) ? 0u : (ghw | (uint32_t)gext);
+            l0 = k ? l0 : ii;
+            l1 = k ? ii : l1;
+            g0 = k ? g0 : nglo;
+            g1 = k ? nglo : g1;
+            h0 = k ? h0 : nghw;
+            h1 = k ? nghw : h1;
+            sub0 = brk ? ii : sub0;
+            ++ii;
+        }
+        out_rs = rs;
+        out_cnt = cnt;
+        lo = fbrk ? t : (ext ? min(lo, t) : lo);
+        hw = fbrk ? 0u : (hw | (uint32_t)ext);
+        rs = brk ? last : rs;
+        cnt = brk ? 1 : cnt + 1;
+        last = n;
+        return emit;
+    }
+
+    // open run at end of stream (valid when at least one interval was seen)
+    SPK_HD bool tail(int& out_rs, int& out_cnt) const {
+        out_rs = rs;
+        out_cnt = cnt;
+        return lo < kLim;
+    }
+};
+
 }  // namespace spk

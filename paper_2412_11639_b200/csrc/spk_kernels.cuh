@@ -14,7 +14,8 @@ using spk_run_t = ::spk_run;
 constexpr int kSegThreads = 64;  // 2 warps: fine-grained blocks balance 148 SMs
 constexpr int kBatch = 8;        // 32-frame groups per prefetch batch
 constexpr int kExpThreads = 128;
-constexpr int kExpPix = 16;      // pixels per expand thread (one 16-B u8 store)
+constexpr int kExpPix = 8;       // pixels per expand thread
+constexpr int kFinThreads = 128;
 constexpr int kCausalWarps = 2;  // warps per TFI/TFP block
 
 struct SegArgs {
@@ -30,7 +31,21 @@ struct SegArgs {
     int32_t* last;
 };
 
+// K2b: run values + run table from the run lists
+struct FinArgs {
+    spk_run_t* runs;  // in: {start, intervals}; out (u8/f32): {start, value bits}
+    double* vals;     // out (f64): value per run, same indexing as runs
+    int32_t* tbl;     // out: [nchunks][npix] run covering frame c*kChunk, -1 = none
+    const uint32_t* counts;
+    const int32_t* last;
+    int64_t npix;
+    int frames;
+    int cap;
+    int nchunks;
+};
+
 struct ExpArgs {
+    const double* vals;
     const spk_run_t* runs;
     const int32_t* tbl;
     const uint32_t* counts;
@@ -59,6 +74,8 @@ template <int METHOD>
 __global__ void k_segment(SegArgs a);
 template <int METHOD, typename OUT>
 __global__ void k_fixup(SegArgs a, OUT* out, size_t out_pitch);
+template <typename OUT>
+__global__ void k_finalize(FinArgs a);
 template <typename OUT>
 __global__ void k_expand(ExpArgs a);
 template <int METHOD, typename OUT>

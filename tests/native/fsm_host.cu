@@ -43,3 +43,43 @@ extern "C" long fsm_runs(const uint8_t* bits, long frames, int method, long* sta
     }
     return em.n;
 }
+
+// The branch-free Scan<METHOD> automaton of the segment kernel: runs as
+// (start, intervals); a run ends where the next starts, the last at the final
+// spike.
+extern "C" long scan_runs(const uint8_t* bits, long frames, int method, long* start, long* end,
+                          long* cnt, long cap) {
+    long n = 0, last = -1;
+    auto go = [&](auto& sc) {
+        sc.init();
+        for (long f = 0; f < frames; ++f) {
+            if (!bits[f]) continue;
+            int rs, c;
+            if (sc.step((int)f, rs, c)) {
+                if (n < cap) {
+                    start[n] = rs;
+                    cnt[n] = c;
+                }
+                ++n;
+            }
+            last = f;
+        }
+        int rs, c;
+        if (sc.tail(rs, c)) {
+            if (n < cap) {
+                start[n] = rs;
+                cnt[n] = c;
+            }
+            ++n;
+        }
+    };
+    if (method == 0) {
+        spk::Scan<spk::kFSR> sc;
+        go(sc);
+    } else {
+        spk::Scan<spk::kSSR> sc;
+        go(sc);
+    }
+    for (long k = 0; k < n && k < cap; ++k) end[k] = (k + 1 < n) ? start[k + 1] : last;
+    return n;
+}

@@ -28,13 +28,18 @@ def fsm():
     h.fsm_runs.argtypes = [C.c_void_p, C.c_long, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                            C.c_long]
 
-    def run(bits, m):
-        cap = bits.size + 1
-        s, e, c = (np.zeros(cap, np.int64) for _ in range(3))
-        n = h.fsm_runs(bits.ctypes.data, bits.size, m, s.ctypes.data, e.ctypes.data,
-                       c.ctypes.data, cap)
-        return s[:n], e[:n], c[:n]
-    return run
+    h.scan_runs.restype = C.c_long
+    h.scan_runs.argtypes = h.fsm_runs.argtypes
+
+    def make(fn):
+        def run(bits, m):
+            cap = bits.size + 1
+            s, e, c = (np.zeros(cap, np.int64) for _ in range(3))
+            n = fn(bits.ctypes.data, bits.size, m, s.ctypes.data, e.ctypes.data,
+                   c.ctypes.data, cap)
+            return s[:n], e[:n], c[:n]
+        return run
+    return {"fsm": make(h.fsm_runs), "scan": make(h.scan_runs)}
 
 
 def if_stream(rng, t, segs, flips):
@@ -50,8 +55,10 @@ def if_stream(rng, t, segs, flips):
     return b ^ (rng.random(t) < flips).astype(np.uint8)
 
 
+@pytest.mark.parametrize("kind", ["fsm", "scan"])
 @pytest.mark.parametrize("family", ["noise", "if", "if_noisy", "if_rare_flips"])
-def test_fsm_matches_oracle(fsm, oracle, family):
+def test_fsm_matches_oracle(fsm, oracle, family, kind):
+    run = fsm[kind]
     rng = np.random.default_rng(hash(family) % 2**32)
     for _ in range(2500):
         t = int(rng.integers(0, 700))
@@ -61,17 +68,18 @@ def test_fsm_matches_oracle(fsm, oracle, family):
             flips = {"if": 0.0, "if_noisy": 0.03, "if_rare_flips": 0.002}[family]
             b = if_stream(rng, t, int(rng.integers(1, 5)), flips)
         for m in (0, 1):
-            got, want = fsm(b, m), oracle.runs(b, m)
+            got, want = run(b, m), oracle.runs(b, m)
             assert all(np.array_equal(x, y) for x, y in zip(got, want)), (family, m, t)
 
 
-def test_fsm_golden_rows(fsm, golden_dir):
+@pytest.mark.parametrize("kind", ["fsm", "scan"])
+def test_fsm_golden_rows(fsm, golden_dir, kind):
     z = np.load(golden_dir / "rows.npz")
     for name in sorted({k.split("/")[0] for k in z.files}):
         bits = z[f"{name}/bits"]
         for m, tag in ((0, "fsr"), (1, "ssr")):
             s, e, n = z[f"{name}/{tag}_seg"]
             keep = n > 0
-            got = fsm(bits, m)
+            got = fsm[kind](bits, m)
             assert np.array_equal(got[0], s[keep]) and np.array_equal(got[1], e[keep]) \
                 and np.array_equal(got[2], n[keep]), (name, tag)

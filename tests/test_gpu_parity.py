@@ -235,6 +235,7 @@ def test_launch_count_and_determinism():
     assert capi.lib().spk_launch_count(1) == 3  # segment + expand + fixup
     b = run(v, "fsr")
     assert torch.equal(a, b)
+    capi.lib().spk_launch_count(1)
     run(v, "tfp")
     assert capi.lib().spk_launch_count(1) == 1
 
