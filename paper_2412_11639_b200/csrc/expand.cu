@@ -12,15 +12,19 @@
 // the tail [last spike, T), reconstruct.cpp:391-393).
 //
 // K3 k_expand: every output value is piecewise constant in time per pixel.
-// A thread owns kExpPix consecutive pixels of one kChunk-frame chunk and keeps
-// their current values packed in registers, so the steady state is one
-// vector store per frame (8 B for u8) and a pointer bump.  The warp walks the
-// frames in lockstep -- the next stop is the warp-wide minimum of the lanes'
-// next change frames (REDUX) -- so every store instruction writes whole
-// 128-B lines of one frame row (no partial-sector read-modify-write in L2).
-// At a change a lane takes the value it preloaded for its pixel's next run
-// and issues the load of the run after that, two runs ahead of use.
+// A lane owns P consecutive pixels of one kChunk-frame chunk and keeps their
+// current values packed in registers: the steady state is one vector store
+// per frame (16 B for u8: a warp writes 512 contiguous bytes of a frame row
+// per instruction) and a pointer bump, with all lanes of a warp on the same
+// frame so every store covers whole 128-B lines.  Value changes are not
+// handled in the frame loop (a data-dependent branch there would serialise
+// the warp at almost every frame of a moving scene).  Instead, per sub-tile
+// of F frames, each lane first buckets its pixels' changes by frame into
+// lane-private shared memory (phase A: per-pixel loops over the run lists,
+// with the record loads prefetched two runs ahead), then walks the F frames
+// and merges a frame's pending changes with one masked select (phase B).
 #include <climits>
+#include <type_traits>
 
 #include "spk_common.cuh"
 #include "spk_kernels.cuh"
@@ -47,37 +51,6 @@ template <>
 struct RunVal<double> {
     using T = double;
     __device__ static T load(const spk_run_t*, const double* vp, int r) { return vp[r]; }
-};
-
-template <typename OUT, int P>
-struct Pack;  // P values -> the thread's per-frame store
-template <>
-struct Pack<uint8_t, 8> {
-    static constexpr int N = 2;  // 32-bit words
-    __device__ static void pack(const uint32_t (&v)[8], uint32_t (&o)[N]) {
-        o[0] = v[0] | v[1] << 8 | v[2] << 16 | v[3] << 24;
-        o[1] = v[4] | v[5] << 8 | v[6] << 16 | v[7] << 24;
-    }
-};
-template <>
-struct Pack<float, 8> {
-    static constexpr int N = 8;
-    __device__ static void pack(const uint32_t (&v)[8], uint32_t (&o)[N]) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = v[i];
-    }
-};
-template <>
-struct Pack<double, 8> {
-    static constexpr int N = 16;
-    __device__ static void pack(const double (&v)[8], uint32_t (&o)[N]) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const unsigned long long b = __double_as_longlong(v[i]);
-            o[2 * i] = (uint32_t)b;
-            o[2 * i + 1] = (uint32_t)(b >> 32);
-        }
-    }
 };
 
 template <int N>
@@ -136,20 +109,47 @@ template __global__ void k_finalize<float>(FinArgs);
 template __global__ void k_finalize<double>(FinArgs);
 
 // -------------------------------------------------------------- K3 expand --
+// Geometry per output type: P pixels per lane (one 16-B store per frame for
+// u8, 32/64 B for f32/f64) and F frames per sub-tile.
+template <typename OUT>
+struct ExpGeo;
+template <>
+struct ExpGeo<uint8_t> {
+    static constexpr int P = 16, F = 32;
+};
+template <>
+struct ExpGeo<float> {
+    static constexpr int P = 8, F = 16;
+};
+template <>
+struct ExpGeo<double> {
+    static constexpr int P = 8, F = 8;
+};
+
+template <typename OUT>
+__host__ __device__ constexpr int exp_smem_per_lane() {
+    return ExpGeo<OUT>::F * (ExpGeo<OUT>::P * (int)sizeof(OUT) + 4);
+}
+
 template <typename OUT>
 __global__ void __launch_bounds__(kExpThreads) k_expand(ExpArgs a) {
-    constexpr int P = kExpPix;
-    using V = typename RunVal<OUT>::T;
-    using PK = Pack<OUT, P>;
+    constexpr int P = ExpGeo<OUT>::P;
+    constexpr int F = ExpGeo<OUT>::F;
+    constexpr int NW = P * (int)sizeof(OUT) / 4;  // 32-bit words per lane-frame
+    using V = typename RunVal<OUT>::T;            // u8/f32: 32-bit word, f64: double
+    using S = typename std::conditional<sizeof(OUT) == 1, uint8_t, V>::type;  // D element
+    extern __shared__ __align__(16) unsigned char sm[];
+    // lane-private scratch: D[F][P] pending values, M[F] pending-pixel masks
+    unsigned char* mine = sm + (size_t)threadIdx.x * exp_smem_per_lane<OUT>();
+    S* D = reinterpret_cast<S*>(mine);
+    uint32_t* Mk = reinterpret_cast<uint32_t*>(mine + F * P * sizeof(OUT));
+
     const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * P;
-    // whole warps out of range leave; partial warps keep every lane in the
-    // lockstep loop (inactive lanes never change and never store)
-    if (((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * P >= a.npix) return;
     const int c = a.chunk0 + (int)blockIdx.y;
     const int f0 = c << kChunkLog2;
-    if (f0 >= a.frames) return;  // uniform across the block
+    if (p0 >= a.npix || f0 >= a.frames) return;  // no cross-lane traffic: lanes may leave
     const int f1 = min(a.frames, f0 + kChunk);
-    const int np = (int)max((int64_t)0, min((int64_t)P, a.npix - p0));
+    const int np = (int)min((int64_t)P, a.npix - p0);
 
     int ridx[P], nst[P], nnst[P], rcnt[P];
     V val[P], nval[P], nnval[P];
@@ -180,59 +180,118 @@ __global__ void __launch_bounds__(kExpThreads) k_expand(ExpArgs a) {
             }
         }
     }
-    int nc = INT_MAX;
+    // current values, packed as the lane's per-frame store
+    uint32_t words[NW];
+    if constexpr (sizeof(OUT) == 1) {
 #pragma unroll
-    for (int i = 0; i < P; ++i) nc = min(nc, nst[i]);
+        for (int k = 0; k < NW; ++k)
+            words[k] = (val[4 * k] & 0xffu) | (val[4 * k + 1] & 0xffu) << 8 |
+                       (val[4 * k + 2] & 0xffu) << 16 | (val[4 * k + 3] & 0xffu) << 24;
+    } else if constexpr (sizeof(OUT) == 4) {
+#pragma unroll
+        for (int k = 0; k < NW; ++k) words[k] = (uint32_t)val[k];
+    } else {
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            const unsigned long long b = __double_as_longlong((double)val[k]);
+            words[2 * k] = (uint32_t)b;
+            words[2 * k + 1] = (uint32_t)(b >> 32);
+        }
+    }
+#pragma unroll
+    for (int f = 0; f < F; ++f) Mk[f] = 0u;
 
-    uint32_t words[PK::N];
-    PK::pack(val, words);
     const size_t step = a.pitch * sizeof(OUT);
     char* ptr = reinterpret_cast<char*>(a.out) + ((size_t)f0 * a.pitch + (size_t)p0) * sizeof(OUT);
     const bool vec_ok = a.vec_ok && np == P;
-    int f = f0;
-    for (;;) {
-        const int stop = (int)__reduce_min_sync(kFull, (unsigned)min(nc, f1));
-        if (vec_ok) {
-#pragma unroll 4
-            for (; f < stop; ++f, ptr += step) st_words(ptr, words);
-        } else {
-            for (; f < stop; ++f, ptr += step) {
-                OUT* o = reinterpret_cast<OUT*>(ptr);
-#pragma unroll
-                for (int i = 0; i < P; ++i)
-                    if (i < np) {
-                        if constexpr (sizeof(OUT) == 8)
-                            o[i] = val[i];
-                        else if constexpr (sizeof(OUT) == 4)
-                            o[i] = __uint_as_float(val[i]);
-                        else
-                            o[i] = (OUT)val[i];
-                    }
-            }
-        }
-        if (f >= f1) break;
-        if (nc == f) {  // this lane has pixels whose next run starts at f
-            nc = INT_MAX;
+
+    for (int t0 = f0; t0 < f1; t0 += F) {
+        const int t1 = min(f1, t0 + F);
+        // phase A: bucket this sub-tile's value changes by frame
+        bool more = true;
+        while (more) {
+            more = false;
 #pragma unroll
             for (int i = 0; i < P; ++i) {
-                if (nst[i] == f) {
-                    const int64_t p = p0 + i;
+                if (nst[i] < t1) {
+                    const int fo = nst[i] - t0;
+                    D[fo * P + i] = (S)nval[i];
+                    Mk[fo] |= 1u << i;
                     const int r = ++ridx[i];
-                    val[i] = nval[i];
                     nst[i] = nnst[i];
                     nval[i] = nnval[i];
                     nnst[i] = INT_MAX;
                     if (r + 2 < rcnt[i]) {  // prefetch two runs ahead
+                        const int64_t p = p0 + i;
                         const spk_run_t* rp = a.runs + p * a.cap;
                         nnst[i] = (int)rp[r + 2].start;
-                        nnval[i] = RunVal<OUT>::load(rp, a.vals ? a.vals + p * a.cap : nullptr, r + 2);
+                        nnval[i] =
+                            RunVal<OUT>::load(rp, a.vals ? a.vals + p * a.cap : nullptr, r + 2);
                     }
+                    more |= nst[i] < t1;
                 }
-                nc = min(nc, nst[i]);
             }
-            PK::pack(val, words);
+        }
+        // phase B: frames in order, one store per frame, pending changes merged
+        const int nf = t1 - t0;
+#pragma unroll 4
+        for (int fo = 0; fo < nf; ++fo) {
+            const uint32_t m = Mk[fo];
+            if (m) {
+                Mk[fo] = 0u;
+                if constexpr (sizeof(OUT) == 1) {
+                    const uint4 d = *reinterpret_cast<const uint4*>(D + fo * P);
+                    const uint32_t dw[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t nib = (m >> (4 * k)) & 0xfu;
+                        const uint32_t bm = ((nib * 0x00204081u) & 0x01010101u) * 0xffu;
+                        words[k] = (words[k] & ~bm) | (dw[k] & bm);
+                    }
+                } else if constexpr (sizeof(OUT) == 4) {
+#pragma unroll
+                    for (int i = 0; i < P; ++i)
+                        if (m & (1u << i)) words[i] = D[fo * P + i];
+                } else {
+#pragma unroll
+                    for (int i = 0; i < P; ++i)
+                        if (m & (1u << i)) {
+                            const unsigned long long b = __double_as_longlong(D[fo * P + i]);
+                            words[2 * i] = (uint32_t)b;
+                            words[2 * i + 1] = (uint32_t)(b >> 32);
+                        }
+                }
+            }
+            if (vec_ok) {
+                st_words(ptr, words);
+            } else {
+                OUT* o = reinterpret_cast<OUT*>(ptr);
+#pragma unroll
+                for (int i = 0; i < P; ++i)
+                    if (i < np) {
+                        if constexpr (sizeof(OUT) == 1)
+                            o[i] = (OUT)((words[i >> 2] >> ((i & 3) * 8)) & 0xffu);
+                        else if constexpr (sizeof(OUT) == 4)
+                            o[i] = __uint_as_float(words[i]);
+                        else
+                            o[i] = __longlong_as_double((long long)((unsigned long long)words[2 * i] |
+                                                                    (unsigned long long)words[2 * i + 1] << 32));
+                    }
+            }
+            ptr += step;
         }
     }
+}
+
+size_t expand_smem_bytes(int out_size) {
+    const int per = out_size == 1 ? exp_smem_per_lane<uint8_t>()
+                  : out_size == 4 ? exp_smem_per_lane<float>()
+                                  : exp_smem_per_lane<double>();
+    return (size_t)per * kExpThreads;
+}
+
+int expand_pixels_per_lane(int out_size) {
+    return out_size == 1 ? ExpGeo<uint8_t>::P : out_size == 4 ? ExpGeo<float>::P : ExpGeo<double>::P;
 }
 
 template __global__ void k_expand<uint8_t>(ExpArgs);

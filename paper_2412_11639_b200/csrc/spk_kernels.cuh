@@ -14,7 +14,6 @@ using spk_run_t = ::spk_run;
 constexpr int kSegThreads = 64;  // 2 warps: fine-grained blocks balance 148 SMs
 constexpr int kBatch = 8;        // 32-frame groups per prefetch batch
 constexpr int kExpThreads = 128;
-constexpr int kExpPix = 8;       // pixels per expand thread
 constexpr int kFinThreads = 128;
 constexpr int kCausalWarps = 2;  // warps per TFI/TFP block
 
@@ -78,6 +77,8 @@ template <typename OUT>
 __global__ void k_finalize(FinArgs a);
 template <typename OUT>
 __global__ void k_expand(ExpArgs a);
+size_t expand_smem_bytes(int out_size);   // dynamic shared memory of k_expand<OUT>
+int expand_pixels_per_lane(int out_size);
 template <int METHOD, typename OUT>
 __global__ void k_causal(CausalArgs a);
 

@@ -232,7 +232,7 @@ def test_launch_count_and_determinism():
     v = spk.synth("static", 1, 400, 250, 2000)
     capi.lib().spk_launch_count(1)
     a = run(v, "fsr")
-    assert capi.lib().spk_launch_count(1) == 3  # segment + expand + fixup
+    assert capi.lib().spk_launch_count(1) == 4  # segment + finalize + expand + fixup
     b = run(v, "fsr")
     assert torch.equal(a, b)
     capi.lib().spk_launch_count(1)
