@@ -109,154 +109,214 @@ template __global__ void k_finalize<float>(FinArgs);
 template __global__ void k_finalize<double>(FinArgs);
 
 // -------------------------------------------------------------- K3 expand --
-// Geometry per output type: P pixels per lane (one 16-B store per frame for
-// u8, 32/64 B for f32/f64) and F frames per sub-tile.
+// Per output type: P pixels per lane, F frames per sub-tile, K-deep record
+// ring per pixel.
 template <typename OUT>
 struct ExpGeo;
 template <>
 struct ExpGeo<uint8_t> {
-    static constexpr int P = 16, F = 32;
+    static constexpr int P = 8, F = 16, K = 4;
 };
 template <>
 struct ExpGeo<float> {
-    static constexpr int P = 8, F = 16;
+    static constexpr int P = 8, F = 8, K = 4;
 };
 template <>
 struct ExpGeo<double> {
-    static constexpr int P = 8, F = 8;
+    static constexpr int P = 8, F = 8, K = 4;
 };
 
+// Lane-private shared memory, interleaved by lane (element e of lane j is at
+// slot e*32 + j) so that lanes touching the same element never share a bank.
+//   ring[P][K]  upcoming runs of each pixel: {start, value} (u8/f32: 8 B,
+//               f64: 16 B), refilled with cp.async as runs are consumed
+//   cur[P]      index of the run each pixel is in (int), cnt[P] its run count
+//   D[F][P]     values of pending changes, M[F] pixel mask per frame
 template <typename OUT>
-__host__ __device__ constexpr int exp_smem_per_lane() {
-    return ExpGeo<OUT>::F * (ExpGeo<OUT>::P * (int)sizeof(OUT) + 4);
+struct ExpSmem {
+    static constexpr int P = ExpGeo<OUT>::P, F = ExpGeo<OUT>::F, K = ExpGeo<OUT>::K;
+    static constexpr int RE = sizeof(OUT) == 8 ? 16 : 8;  // ring entry bytes
+    static constexpr int ring = P * K * RE;
+    static constexpr int cur = P * 4, cnt = P * 4;
+    static constexpr int d = F * P * (int)sizeof(OUT);
+    static constexpr int m = F * 4;
+    static constexpr int per_lane = ring + cur + cnt + d + m;
+    static constexpr int per_warp = 32 * per_lane;
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 template <typename OUT>
 __global__ void __launch_bounds__(kExpThreads) k_expand(ExpArgs a) {
-    constexpr int P = ExpGeo<OUT>::P;
-    constexpr int F = ExpGeo<OUT>::F;
+    using G = ExpSmem<OUT>;
+    constexpr int P = G::P, F = G::F, K = G::K;
     constexpr int NW = P * (int)sizeof(OUT) / 4;  // 32-bit words per lane-frame
-    using V = typename RunVal<OUT>::T;            // u8/f32: 32-bit word, f64: double
-    using S = typename std::conditional<sizeof(OUT) == 1, uint8_t, V>::type;  // D element
     extern __shared__ __align__(16) unsigned char sm[];
-    // lane-private scratch: D[F][P] pending values, M[F] pending-pixel masks
-    unsigned char* mine = sm + (size_t)threadIdx.x * exp_smem_per_lane<OUT>();
-    S* D = reinterpret_cast<S*>(mine);
-    uint32_t* Mk = reinterpret_cast<uint32_t*>(mine + F * P * sizeof(OUT));
+    const int lane = threadIdx.x & 31;
+    unsigned char* wbase = sm + (size_t)(threadIdx.x >> 5) * G::per_warp;
+    // element accessors (interleaved by lane)
+    unsigned char* ring_b = wbase;
+    int* cur_b = reinterpret_cast<int*>(wbase + 32 * G::ring);
+    int* cnt_b = reinterpret_cast<int*>(wbase + 32 * (G::ring + G::cur));
+    unsigned char* d_b = wbase + 32 * (G::ring + G::cur + G::cnt);
+    uint32_t* m_b = reinterpret_cast<uint32_t*>(wbase + 32 * (G::ring + G::cur + G::cnt + G::d));
+    auto ring_at = [&](int i, int q) -> unsigned char* {  // entry for run q of pixel i
+        return ring_b + ((size_t)((i * K + (q & (K - 1))) * 32 + lane)) * G::RE;
+    };
+    auto ring_start = [&](int i, int q) -> int { return *reinterpret_cast<const int*>(ring_at(i, q)); };
+    auto CUR = [&](int i) -> int& { return cur_b[i * 32 + lane]; };
+    auto CNT = [&](int i) -> int& { return cnt_b[i * 32 + lane]; };
+    auto M = [&](int f) -> uint32_t& { return m_b[f * 32 + lane]; };
 
     const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * P;
     const int c = a.chunk0 + (int)blockIdx.y;
     const int f0 = c << kChunkLog2;
-    if (p0 >= a.npix || f0 >= a.frames) return;  // no cross-lane traffic: lanes may leave
+    if (p0 >= a.npix || f0 >= a.frames) return;  // lanes never exchange data
     const int f1 = min(a.frames, f0 + kChunk);
     const int np = (int)min((int64_t)P, a.npix - p0);
 
-    int ridx[P], nst[P], nnst[P], rcnt[P];
-    V val[P], nval[P], nnval[P];
+    // issue the copy of run q of pixel i into its ring slot
+    auto fetch = [&](int i, int q) {
+        const int64_t p = p0 + i;
+        unsigned char* dst = ring_at(i, q);
+        const spk_run_t* rp = a.runs + p * a.cap + q;
+        if constexpr (sizeof(OUT) == 8) {
+            cp_async4(dst, &rp->start);
+            cp_async8(dst + 8, a.vals + p * a.cap + q);
+        } else {
+            cp_async8(dst, rp);
+        }
+    };
+
+    uint32_t words[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) words[k] = 0u;
 #pragma unroll
     for (int i = 0; i < P; ++i) {
-        val[i] = nval[i] = nnval[i] = V(0);
-        nst[i] = nnst[i] = INT_MAX;
-        ridx[i] = -1;
-        rcnt[i] = 0;
+        int r = -1, cnt = 0;
         if (i < np) {
             const int64_t p = p0 + i;
-            const uint32_t cnt = a.counts[p];
-            if (cnt > 0 && cnt <= (uint32_t)a.cap) {  // overflowed pixels: k_fixup
-                const spk_run_t* rp = a.runs + p * a.cap;
-                const double* vp = a.vals ? a.vals + p * a.cap : nullptr;
-                const int r = a.tbl[(int64_t)c * a.npix + p];
-                rcnt[i] = (int)cnt;
-                ridx[i] = r;
-                if (r >= 0) val[i] = RunVal<OUT>::load(rp, vp, r);
-                if (r + 1 < (int)cnt) {
-                    nst[i] = (int)rp[r + 1].start;
-                    nval[i] = RunVal<OUT>::load(rp, vp, r + 1);
+            const uint32_t n = a.counts[p];
+            if (n > 0 && n <= (uint32_t)a.cap) {  // overflowed pixels: k_fixup
+                cnt = (int)n;
+                r = a.tbl[(int64_t)c * a.npix + p];
+                if (r >= 0) {  // value at the chunk start
+                    if constexpr (sizeof(OUT) == 1)
+                        words[i >> 2] |= (a.runs[p * a.cap + r].intervals & 0xffu) << ((i & 3) * 8);
+                    else if constexpr (sizeof(OUT) == 4)
+                        words[i] = a.runs[p * a.cap + r].intervals;
+                    else {
+                        const unsigned long long b = __double_as_longlong(a.vals[p * a.cap + r]);
+                        words[2 * i] = (uint32_t)b;
+                        words[2 * i + 1] = (uint32_t)(b >> 32);
+                    }
                 }
-                if (r + 2 < (int)cnt) {
-                    nnst[i] = (int)rp[r + 2].start;
-                    nnval[i] = RunVal<OUT>::load(rp, vp, r + 2);
-                }
+                for (int q = r + 1; q < min(cnt, r + 1 + K); ++q) fetch(i, q);
             }
         }
+        CUR(i) = r;
+        CNT(i) = cnt;
     }
-    // current values, packed as the lane's per-frame store
-    uint32_t words[NW];
-    if constexpr (sizeof(OUT) == 1) {
+    cp_async_commit();
 #pragma unroll
-        for (int k = 0; k < NW; ++k)
-            words[k] = (val[4 * k] & 0xffu) | (val[4 * k + 1] & 0xffu) << 8 |
-                       (val[4 * k + 2] & 0xffu) << 16 | (val[4 * k + 3] & 0xffu) << 24;
-    } else if constexpr (sizeof(OUT) == 4) {
-#pragma unroll
-        for (int k = 0; k < NW; ++k) words[k] = (uint32_t)val[k];
-    } else {
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-            const unsigned long long b = __double_as_longlong((double)val[k]);
-            words[2 * k] = (uint32_t)b;
-            words[2 * k + 1] = (uint32_t)(b >> 32);
-        }
-    }
-#pragma unroll
-    for (int f = 0; f < F; ++f) Mk[f] = 0u;
+    for (int f = 0; f < F; ++f) M(f) = 0u;
 
     const size_t step = a.pitch * sizeof(OUT);
     char* ptr = reinterpret_cast<char*>(a.out) + ((size_t)f0 * a.pitch + (size_t)p0) * sizeof(OUT);
     const bool vec_ok = a.vec_ok && np == P;
 
+    cp_async_wait<0>();
+    // Ring safety: run q of a pixel is requested when run q-K is consumed.
+    // After wait_group 1 at a phase-A start, every request older than the
+    // previous phase A has landed, so consuming q is safe unless the pixel
+    // consumed >= K runs over this and the previous phase A; then wait for
+    // all requests.  Per-pixel 4-bit counters of consumed runs: nprev, ncur.
+    uint32_t ncur = 0;
     for (int t0 = f0; t0 < f1; t0 += F) {
         const int t1 = min(f1, t0 + F);
-        // phase A: bucket this sub-tile's value changes by frame
-        bool more = true;
-        while (more) {
-            more = false;
+        // phase A: bucket this sub-tile's changes by frame
+        cp_async_wait<1>();
+        uint32_t nprev = ncur;
+        ncur = 0;
+        // before reading a ring entry of pixel i: wait if it may still be in flight
+        auto ensure = [&](int i) {
+            if (((nprev >> (4 * i)) & 15u) + ((ncur >> (4 * i)) & 15u) >= (uint32_t)K) {
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                nprev = ncur = 0;
+            }
+        };
+        uint32_t todo = 0;
 #pragma unroll
-            for (int i = 0; i < P; ++i) {
-                if (nst[i] < t1) {
-                    const int fo = nst[i] - t0;
-                    D[fo * P + i] = (S)nval[i];
-                    Mk[fo] |= 1u << i;
-                    const int r = ++ridx[i];
-                    nst[i] = nnst[i];
-                    nval[i] = nnval[i];
-                    nnst[i] = INT_MAX;
-                    if (r + 2 < rcnt[i]) {  // prefetch two runs ahead
-                        const int64_t p = p0 + i;
-                        const spk_run_t* rp = a.runs + p * a.cap;
-                        nnst[i] = (int)rp[r + 2].start;
-                        nnval[i] =
-                            RunVal<OUT>::load(rp, a.vals ? a.vals + p * a.cap : nullptr, r + 2);
-                    }
-                    more |= nst[i] < t1;
-                }
+        for (int i = 0; i < P; ++i) {
+            const int q = CUR(i) + 1;
+            if (q < CNT(i)) {
+                ensure(i);
+                if (ring_start(i, q) < t1) todo |= 1u << i;
             }
         }
+        while (todo) {
+            const int i = __ffs(todo) - 1;
+            const int q = CUR(i) + 1;  // run starting inside this sub-tile (entry ensured)
+            const unsigned char* e = ring_at(i, q);
+            const int fo = *reinterpret_cast<const int*>(e) - t0;
+            if constexpr (sizeof(OUT) == 1)
+                d_b[((fo * P + i) >> 2) * 128 + lane * 4 + (i & 3)] = (uint8_t)reinterpret_cast<const uint32_t*>(e)[1];
+            else if constexpr (sizeof(OUT) == 4)
+                reinterpret_cast<uint32_t*>(d_b)[(fo * P + i) * 32 + lane] = reinterpret_cast<const uint32_t*>(e)[1];
+            else
+                reinterpret_cast<double*>(d_b)[(fo * P + i) * 32 + lane] = *reinterpret_cast<const double*>(e + 8);
+            M(fo) |= 1u << i;
+            CUR(i) = q;
+            ncur += 1u << (4 * i);
+            const int cnt = CNT(i);
+            if (q + K < cnt) fetch(i, q + K);  // refill the slot just consumed
+            bool again = false;
+            if (q + 1 < cnt) {
+                ensure(i);
+                again = ring_start(i, q + 1) < t1;
+            }
+            if (!again) todo &= todo - 1;
+        }
+        cp_async_commit();
         // phase B: frames in order, one store per frame, pending changes merged
         const int nf = t1 - t0;
 #pragma unroll 4
         for (int fo = 0; fo < nf; ++fo) {
-            const uint32_t m = Mk[fo];
+            const uint32_t m = M(fo);
             if (m) {
-                Mk[fo] = 0u;
+                M(fo) = 0u;
                 if constexpr (sizeof(OUT) == 1) {
-                    const uint4 d = *reinterpret_cast<const uint4*>(D + fo * P);
-                    const uint32_t dw[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
+                    for (int k = 0; k < NW; ++k) {
+                        const uint32_t dw = reinterpret_cast<const uint32_t*>(d_b)[(fo * NW + k) * 32 + lane];
                         const uint32_t nib = (m >> (4 * k)) & 0xfu;
                         const uint32_t bm = ((nib * 0x00204081u) & 0x01010101u) * 0xffu;
-                        words[k] = (words[k] & ~bm) | (dw[k] & bm);
+                        words[k] = (words[k] & ~bm) | (dw & bm);
                     }
                 } else if constexpr (sizeof(OUT) == 4) {
 #pragma unroll
                     for (int i = 0; i < P; ++i)
-                        if (m & (1u << i)) words[i] = D[fo * P + i];
+                        if (m & (1u << i)) words[i] = reinterpret_cast<const uint32_t*>(d_b)[(fo * P + i) * 32 + lane];
                 } else {
 #pragma unroll
                     for (int i = 0; i < P; ++i)
                         if (m & (1u << i)) {
-                            const unsigned long long b = __double_as_longlong(D[fo * P + i]);
+                            const unsigned long long b = __double_as_longlong(
+                                reinterpret_cast<const double*>(d_b)[(fo * P + i) * 32 + lane]);
                             words[2 * i] = (uint32_t)b;
                             words[2 * i + 1] = (uint32_t)(b >> 32);
                         }
@@ -284,10 +344,10 @@ __global__ void __launch_bounds__(kExpThreads) k_expand(ExpArgs a) {
 }
 
 size_t expand_smem_bytes(int out_size) {
-    const int per = out_size == 1 ? exp_smem_per_lane<uint8_t>()
-                  : out_size == 4 ? exp_smem_per_lane<float>()
-                                  : exp_smem_per_lane<double>();
-    return (size_t)per * kExpThreads;
+    const int per = out_size == 1 ? ExpSmem<uint8_t>::per_warp
+                  : out_size == 4 ? ExpSmem<float>::per_warp
+                                  : ExpSmem<double>::per_warp;
+    return (size_t)per * (kExpThreads / 32);
 }
 
 int expand_pixels_per_lane(int out_size) {
