@@ -126,22 +126,23 @@ struct ExpGeo<double> {
     static constexpr int P = 8, F = 8, K = 4;
 };
 
-// Lane-private shared memory, interleaved by lane (element e of lane j is at
-// slot e*32 + j) so that lanes touching the same element never share a bank.
-//   ring[P][K]  upcoming runs of each pixel: {start, value} (u8/f32: 8 B,
+// Lane-private shared memory, interleaved by lane so that lanes touching the
+// same element never share a bank (element e of lane j at slot e*32 + j):
+//   ring[P][K]  upcoming runs of each pixel, {start, value} (u8/f32: 8 B,
 //               f64: 16 B), refilled with cp.async as runs are consumed
-//   cur[P]      index of the run each pixel is in (int), cnt[P] its run count
-//   D[F][P]     values of pending changes, M[F] pixel mask per frame
+//   D[F]        per frame of the sub-tile: the lane's pending values (P * OUT)
+//   B[F]        per frame: u8 -> byte mask of the pending pixels (8 B),
+//               f32/f64 -> pixel bit mask (4 B)
 template <typename OUT>
 struct ExpSmem {
     static constexpr int P = ExpGeo<OUT>::P, F = ExpGeo<OUT>::F, K = ExpGeo<OUT>::K;
     static constexpr int RE = sizeof(OUT) == 8 ? 16 : 8;  // ring entry bytes
-    static constexpr int ring = P * K * RE;
-    static constexpr int cur = P * 4, cnt = P * 4;
-    static constexpr int d = F * P * (int)sizeof(OUT);
-    static constexpr int m = F * 4;
-    static constexpr int per_lane = ring + cur + cnt + d + m;
-    static constexpr int per_warp = 32 * per_lane;
+    static constexpr int DE = P * (int)sizeof(OUT);       // D element bytes
+    static constexpr int BE = sizeof(OUT) == 1 ? 8 : 4;   // B element bytes
+    static constexpr int ring = P * K * RE * 32;
+    static constexpr int d = F * DE * 32;
+    static constexpr int b = F * BE * 32;
+    static constexpr int per_warp = ring + d + b;
 };
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -168,19 +169,14 @@ __global__ void __launch_bounds__(kExpThreads) k_expand(ExpArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int lane = threadIdx.x & 31;
     unsigned char* wbase = sm + (size_t)(threadIdx.x >> 5) * G::per_warp;
-    // element accessors (interleaved by lane)
     unsigned char* ring_b = wbase;
-    int* cur_b = reinterpret_cast<int*>(wbase + 32 * G::ring);
-    int* cnt_b = reinterpret_cast<int*>(wbase + 32 * (G::ring + G::cur));
-    unsigned char* d_b = wbase + 32 * (G::ring + G::cur + G::cnt);
-    uint32_t* m_b = reinterpret_cast<uint32_t*>(wbase + 32 * (G::ring + G::cur + G::cnt + G::d));
-    auto ring_at = [&](int i, int q) -> unsigned char* {  // entry for run q of pixel i
-        return ring_b + ((size_t)((i * K + (q & (K - 1))) * 32 + lane)) * G::RE;
+    unsigned char* d_b = wbase + G::ring;
+    unsigned char* b_b = wbase + G::ring + G::d;
+    auto ring_at = [&](int i, int q) -> unsigned char* {  // entry of run q of pixel i
+        return ring_b + ((i * K + (q & (K - 1))) * 32 + lane) * G::RE;
     };
-    auto ring_start = [&](int i, int q) -> int { return *reinterpret_cast<const int*>(ring_at(i, q)); };
-    auto CUR = [&](int i) -> int& { return cur_b[i * 32 + lane]; };
-    auto CNT = [&](int i) -> int& { return cnt_b[i * 32 + lane]; };
-    auto M = [&](int f) -> uint32_t& { return m_b[f * 32 + lane]; };
+    auto d_at = [&](int fo) -> unsigned char* { return d_b + (fo * 32 + lane) * G::DE; };
+    auto b_at = [&](int fo) -> unsigned char* { return b_b + (fo * 32 + lane) * G::BE; };
 
     const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * P;
     const int c = a.chunk0 + (int)blockIdx.y;
@@ -189,137 +185,136 @@ __global__ void __launch_bounds__(kExpThreads) k_expand(ExpArgs a) {
     const int f1 = min(a.frames, f0 + kChunk);
     const int np = (int)min((int64_t)P, a.npix - p0);
 
-    // issue the copy of run q of pixel i into its ring slot
-    auto fetch = [&](int i, int q) {
-        const int64_t p = p0 + i;
+    const spk_run_t* runs0 = a.runs + p0 * a.cap;
+    const double* vals0 = a.vals ? a.vals + p0 * a.cap : nullptr;
+    auto fetch = [&](int i, int q) {  // request run q of pixel i into its ring slot
         unsigned char* dst = ring_at(i, q);
-        const spk_run_t* rp = a.runs + p * a.cap + q;
+        const size_t off = (size_t)i * a.cap + q;
         if constexpr (sizeof(OUT) == 8) {
-            cp_async4(dst, &rp->start);
-            cp_async8(dst + 8, a.vals + p * a.cap + q);
+            cp_async4(dst, &runs0[off].start);
+            cp_async8(dst + 8, vals0 + off);
         } else {
-            cp_async8(dst, rp);
+            cp_async8(dst, runs0 + off);
         }
     };
 
+    int rr[P], cn[P], ns[P];  // current run, run count, start of the next run
     uint32_t words[NW];
 #pragma unroll
     for (int k = 0; k < NW; ++k) words[k] = 0u;
 #pragma unroll
     for (int i = 0; i < P; ++i) {
-        int r = -1, cnt = 0;
+        rr[i] = -1;
+        cn[i] = 0;
+        ns[i] = INT_MAX;
         if (i < np) {
             const int64_t p = p0 + i;
             const uint32_t n = a.counts[p];
             if (n > 0 && n <= (uint32_t)a.cap) {  // overflowed pixels: k_fixup
-                cnt = (int)n;
-                r = a.tbl[(int64_t)c * a.npix + p];
+                cn[i] = (int)n;
+                const int r = a.tbl[(int64_t)c * a.npix + p];
+                rr[i] = r;
                 if (r >= 0) {  // value at the chunk start
+                    const size_t off = (size_t)i * a.cap + r;
                     if constexpr (sizeof(OUT) == 1)
-                        words[i >> 2] |= (a.runs[p * a.cap + r].intervals & 0xffu) << ((i & 3) * 8);
+                        words[i >> 2] |= (runs0[off].intervals & 0xffu) << ((i & 3) * 8);
                     else if constexpr (sizeof(OUT) == 4)
-                        words[i] = a.runs[p * a.cap + r].intervals;
+                        words[i] = runs0[off].intervals;
                     else {
-                        const unsigned long long b = __double_as_longlong(a.vals[p * a.cap + r]);
+                        const unsigned long long b = __double_as_longlong(vals0[off]);
                         words[2 * i] = (uint32_t)b;
                         words[2 * i + 1] = (uint32_t)(b >> 32);
                     }
                 }
-                for (int q = r + 1; q < min(cnt, r + 1 + K); ++q) fetch(i, q);
+                for (int q = r + 1; q < min((int)n, r + 1 + K); ++q) fetch(i, q);
             }
         }
-        CUR(i) = r;
-        CNT(i) = cnt;
     }
     cp_async_commit();
 #pragma unroll
-    for (int f = 0; f < F; ++f) M(f) = 0u;
+    for (int f = 0; f < F; ++f) {
+        if constexpr (sizeof(OUT) == 1)
+            *reinterpret_cast<uint2*>(b_at(f)) = make_uint2(0u, 0u);
+        else
+            *reinterpret_cast<uint32_t*>(b_at(f)) = 0u;
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+        if (rr[i] + 1 < cn[i]) ns[i] = *reinterpret_cast<const int*>(ring_at(i, rr[i] + 1));
 
     const size_t step = a.pitch * sizeof(OUT);
     char* ptr = reinterpret_cast<char*>(a.out) + ((size_t)f0 * a.pitch + (size_t)p0) * sizeof(OUT);
     const bool vec_ok = a.vec_ok && np == P;
 
-    cp_async_wait<0>();
     // Ring safety: run q of a pixel is requested when run q-K is consumed.
     // After wait_group 1 at a phase-A start, every request older than the
-    // previous phase A has landed, so consuming q is safe unless the pixel
-    // consumed >= K runs over this and the previous phase A; then wait for
-    // all requests.  Per-pixel 4-bit counters of consumed runs: nprev, ncur.
+    // previous phase A has landed, so reading run q is safe unless the pixel
+    // consumed >= K runs over this and the previous phase A (then wait for
+    // all).  Per-pixel 4-bit counters of consumed runs: nprev, ncur.
     uint32_t ncur = 0;
     for (int t0 = f0; t0 < f1; t0 += F) {
         const int t1 = min(f1, t0 + F);
-        // phase A: bucket this sub-tile's changes by frame
+        // phase A: bucket this sub-tile's value changes by frame
         cp_async_wait<1>();
         uint32_t nprev = ncur;
         ncur = 0;
-        // before reading a ring entry of pixel i: wait if it may still be in flight
-        auto ensure = [&](int i) {
-            if (((nprev >> (4 * i)) & 15u) + ((ncur >> (4 * i)) & 15u) >= (uint32_t)K) {
-                asm volatile("cp.async.wait_all;" ::: "memory");
-                nprev = ncur = 0;
-            }
-        };
-        uint32_t todo = 0;
 #pragma unroll
         for (int i = 0; i < P; ++i) {
-            const int q = CUR(i) + 1;
-            if (q < CNT(i)) {
-                ensure(i);
-                if (ring_start(i, q) < t1) todo |= 1u << i;
+            while (ns[i] < t1) {  // run q starts inside this sub-tile
+                const int q = rr[i] + 1;
+                const unsigned char* e = ring_at(i, q);
+                const int fo = ns[i] - t0;
+                if constexpr (sizeof(OUT) == 1) {
+                    d_at(fo)[i] = (uint8_t)reinterpret_cast<const uint32_t*>(e)[1];
+                    b_at(fo)[i] = 0xffu;
+                } else if constexpr (sizeof(OUT) == 4) {
+                    reinterpret_cast<uint32_t*>(d_at(fo))[i] = reinterpret_cast<const uint32_t*>(e)[1];
+                    *reinterpret_cast<uint32_t*>(b_at(fo)) |= 1u << i;
+                } else {
+                    reinterpret_cast<double*>(d_at(fo))[i] = *reinterpret_cast<const double*>(e + 8);
+                    *reinterpret_cast<uint32_t*>(b_at(fo)) |= 1u << i;
+                }
+                rr[i] = q;
+                ncur += 1u << (4 * i);
+                if (q + K < cn[i]) fetch(i, q + K);  // refill the slot just consumed
+                if (q + 1 < cn[i]) {
+                    if (((nprev >> (4 * i)) & 15u) + ((ncur >> (4 * i)) & 15u) >= (uint32_t)K) {
+                        asm volatile("cp.async.wait_all;" ::: "memory");
+                        nprev = ncur = 0;
+                    }
+                    ns[i] = *reinterpret_cast<const int*>(ring_at(i, q + 1));
+                } else {
+                    ns[i] = INT_MAX;
+                }
             }
-        }
-        while (todo) {
-            const int i = __ffs(todo) - 1;
-            const int q = CUR(i) + 1;  // run starting inside this sub-tile (entry ensured)
-            const unsigned char* e = ring_at(i, q);
-            const int fo = *reinterpret_cast<const int*>(e) - t0;
-            if constexpr (sizeof(OUT) == 1)
-                d_b[((fo * P + i) >> 2) * 128 + lane * 4 + (i & 3)] = (uint8_t)reinterpret_cast<const uint32_t*>(e)[1];
-            else if constexpr (sizeof(OUT) == 4)
-                reinterpret_cast<uint32_t*>(d_b)[(fo * P + i) * 32 + lane] = reinterpret_cast<const uint32_t*>(e)[1];
-            else
-                reinterpret_cast<double*>(d_b)[(fo * P + i) * 32 + lane] = *reinterpret_cast<const double*>(e + 8);
-            M(fo) |= 1u << i;
-            CUR(i) = q;
-            ncur += 1u << (4 * i);
-            const int cnt = CNT(i);
-            if (q + K < cnt) fetch(i, q + K);  // refill the slot just consumed
-            bool again = false;
-            if (q + 1 < cnt) {
-                ensure(i);
-                again = ring_start(i, q + 1) < t1;
-            }
-            if (!again) todo &= todo - 1;
         }
         cp_async_commit();
-        // phase B: frames in order, one store per frame, pending changes merged
+        // phase B: frames in order, one store per frame, pending values merged
         const int nf = t1 - t0;
 #pragma unroll 4
         for (int fo = 0; fo < nf; ++fo) {
-            const uint32_t m = M(fo);
-            if (m) {
-                M(fo) = 0u;
-                if constexpr (sizeof(OUT) == 1) {
+            if constexpr (sizeof(OUT) == 1) {
+                const uint2 dv = *reinterpret_cast<const uint2*>(d_at(fo));
+                const uint2 bm = *reinterpret_cast<const uint2*>(b_at(fo));
+                *reinterpret_cast<uint2*>(b_at(fo)) = make_uint2(0u, 0u);
+                words[0] = (words[0] & ~bm.x) | (dv.x & bm.x);
+                words[1] = (words[1] & ~bm.y) | (dv.y & bm.y);
+            } else {
+                const uint32_t m = *reinterpret_cast<const uint32_t*>(b_at(fo));
+                if (m) {
+                    *reinterpret_cast<uint32_t*>(b_at(fo)) = 0u;
+                    const uint32_t* dw = reinterpret_cast<const uint32_t*>(d_at(fo));
 #pragma unroll
-                    for (int k = 0; k < NW; ++k) {
-                        const uint32_t dw = reinterpret_cast<const uint32_t*>(d_b)[(fo * NW + k) * 32 + lane];
-                        const uint32_t nib = (m >> (4 * k)) & 0xfu;
-                        const uint32_t bm = ((nib * 0x00204081u) & 0x01010101u) * 0xffu;
-                        words[k] = (words[k] & ~bm) | (dw & bm);
-                    }
-                } else if constexpr (sizeof(OUT) == 4) {
-#pragma unroll
-                    for (int i = 0; i < P; ++i)
-                        if (m & (1u << i)) words[i] = reinterpret_cast<const uint32_t*>(d_b)[(fo * P + i) * 32 + lane];
-                } else {
-#pragma unroll
-                    for (int i = 0; i < P; ++i)
-                        if (m & (1u << i)) {
-                            const unsigned long long b = __double_as_longlong(
-                                reinterpret_cast<const double*>(d_b)[(fo * P + i) * 32 + lane]);
-                            words[2 * i] = (uint32_t)b;
-                            words[2 * i + 1] = (uint32_t)(b >> 32);
+                    for (int i = 0; i < P; ++i) {
+                        const bool take = (m >> i) & 1u;
+                        if constexpr (sizeof(OUT) == 4) {
+                            words[i] = take ? dw[i] : words[i];
+                        } else {
+                            words[2 * i] = take ? dw[2 * i] : words[2 * i];
+                            words[2 * i + 1] = take ? dw[2 * i + 1] : words[2 * i + 1];
                         }
+                    }
                 }
             }
             if (vec_ok) {
