@@ -169,7 +169,8 @@ int launch_expand(const SegArgs& sa, const double* vals, OUT* out, size_t out_pi
     e.out = out;
     e.pitch = out_pitch;
     e.vec_ok = ((reinterpret_cast<uintptr_t>(out) | (out_pitch * sizeof(OUT))) & 15) == 0;
-    const int64_t per_block = (int64_t)kExpThreads * expand_pixels_per_lane(sizeof(OUT));
+    const int nthr = expand_threads(sizeof(OUT));
+    const int64_t per_block = (int64_t)nthr * expand_pixels_per_lane(sizeof(OUT));
     const unsigned bx = (unsigned)((sa.npix + per_block - 1) / per_block);
     const size_t smem = expand_smem_bytes(sizeof(OUT));
     if (smem > 48 * 1024)
@@ -178,7 +179,7 @@ int launch_expand(const SegArgs& sa, const double* vals, OUT* out, size_t out_pi
     for (int c0 = 0; c0 < sa.nchunks; c0 += 65535) {
         e.chunk0 = c0;
         const unsigned by = (unsigned)std::min(65535, sa.nchunks - c0);
-        k_expand<OUT><<<dim3(bx, by), kExpThreads, smem, s>>>(e);
+        k_expand<OUT><<<dim3(bx, by), nthr, smem, s>>>(e);
         SPK_LAUNCHED("k_expand");
     }
     return SPK_OK;

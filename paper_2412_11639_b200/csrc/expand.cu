@@ -109,205 +109,227 @@ template __global__ void k_finalize<float>(FinArgs);
 template __global__ void k_finalize<double>(FinArgs);
 
 // -------------------------------------------------------------- K3 expand --
-// Per output type: P pixels per lane, F frames per sub-tile, K-deep record
-// ring per pixel.
+// Per output type: P pixels per lane, F frames per sub-tile, K-deep run ring
+// per pixel, WARPS per block.
 template <typename OUT>
 struct ExpGeo;
 template <>
 struct ExpGeo<uint8_t> {
-    static constexpr int P = 8, F = 16, K = 4;
+    static constexpr int P = 8, F = 16, K = 4, WARPS = 4;
 };
 template <>
 struct ExpGeo<float> {
-    static constexpr int P = 8, F = 8, K = 4;
+    static constexpr int P = 8, F = 16, K = 4, WARPS = 2;
 };
 template <>
 struct ExpGeo<double> {
-    static constexpr int P = 8, F = 8, K = 4;
+    static constexpr int P = 8, F = 8, K = 4, WARPS = 2;
 };
 
-// Lane-private shared memory, interleaved by lane so that lanes touching the
-// same element never share a bank (element e of lane j at slot e*32 + j):
-//   ring[P][K]  upcoming runs of each pixel, {start, value} (u8/f32: 8 B,
-//               f64: 16 B), refilled with cp.async as runs are consumed
-//   D[F]        per frame of the sub-tile: the lane's pending values (P * OUT)
-//   B[F]        per frame: u8 -> byte mask of the pending pixels (8 B),
-//               f32/f64 -> pixel bit mask (4 B)
+// Per-warp shared memory.  A warp owns S = 32*P pixel slots; slot
+// s = i*32 + lane is pixel i of lane `lane` (pixel p0(lane) + i), so slot
+// arrays are bank-interleaved by lane.
+//   ring[K][S]  the next K runs of each slot, {start, value} (8 B; f64 16 B),
+//               refilled with cp.async as runs are consumed
+//   cur[S], cnt[S], nxt[S]  run the slot is in, its run count, the start
+//               frame of its next run (INT_MAX = none)
+//   D[F][32]    per frame and lane: the pending values of its P pixels
+//   B[F][32]    per frame and lane: byte i = 0xff if pixel i changes there
 template <typename OUT>
 struct ExpSmem {
     static constexpr int P = ExpGeo<OUT>::P, F = ExpGeo<OUT>::F, K = ExpGeo<OUT>::K;
-    static constexpr int RE = sizeof(OUT) == 8 ? 16 : 8;  // ring entry bytes
-    static constexpr int DE = P * (int)sizeof(OUT);       // D element bytes
-    static constexpr int BE = sizeof(OUT) == 1 ? 8 : 4;   // B element bytes
-    static constexpr int ring = P * K * RE * 32;
-    static constexpr int d = F * DE * 32;
-    static constexpr int b = F * BE * 32;
-    static constexpr int per_warp = ring + d + b;
+    static constexpr int S = 32 * P;
+    static constexpr int RE = sizeof(OUT) == 8 ? 16 : 8;
+    static constexpr int DE = P * (int)sizeof(OUT);
+    static constexpr int ring = K * S * RE;
+    static constexpr int cur = S * 4, cnt = S * 4, nxt = S * 4;
+    static constexpr int d = F * 32 * DE;
+    static constexpr int b = F * 32 * 8;
+    static constexpr int per_warp = ring + cur + cnt + nxt + d + b;
 };
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
-                 "l"(gmem)
-                 : "memory");
+__device__ __forceinline__ void cp_async8(uint32_t saddr, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
-                 "l"(gmem)
-                 : "memory");
+__device__ __forceinline__ void cp_async4(uint32_t saddr, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <typename OUT>
-__global__ void __launch_bounds__(kExpThreads) k_expand(ExpArgs a) {
+__global__ void __launch_bounds__(ExpGeo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
     using G = ExpSmem<OUT>;
-    constexpr int P = G::P, F = G::F, K = G::K;
+    constexpr int P = G::P, F = G::F, K = G::K, S = G::S;
     constexpr int NW = P * (int)sizeof(OUT) / 4;  // 32-bit words per lane-frame
     extern __shared__ __align__(16) unsigned char sm[];
     const int lane = threadIdx.x & 31;
-    unsigned char* wbase = sm + (size_t)(threadIdx.x >> 5) * G::per_warp;
-    unsigned char* ring_b = wbase;
-    unsigned char* d_b = wbase + G::ring;
-    unsigned char* b_b = wbase + G::ring + G::d;
-    auto ring_at = [&](int i, int q) -> unsigned char* {  // entry of run q of pixel i
-        return ring_b + ((i * K + (q & (K - 1))) * 32 + lane) * G::RE;
-    };
-    auto d_at = [&](int fo) -> unsigned char* { return d_b + (fo * 32 + lane) * G::DE; };
-    auto b_at = [&](int fo) -> unsigned char* { return b_b + (fo * 32 + lane) * G::BE; };
+    unsigned char* wb = sm + (size_t)(threadIdx.x >> 5) * G::per_warp;
+    unsigned char* ring = wb;
+    int* CUR = reinterpret_cast<int*>(wb + G::ring);
+    int* CNT = CUR + S;
+    int* NXT = CNT + S;
+    unsigned char* D = wb + G::ring + G::cur + G::cnt + G::nxt;
+    unsigned char* B = D + G::d;
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
 
-    const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * P;
+    // warp geometry: lane l owns pixels pw + l*P + i
+    const int64_t pw = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * P;
+    const int64_t p0 = pw + (int64_t)lane * P;
     const int c = a.chunk0 + (int)blockIdx.y;
     const int f0 = c << kChunkLog2;
-    if (p0 >= a.npix || f0 >= a.frames) return;  // lanes never exchange data
+    if (pw >= a.npix || f0 >= a.frames) return;  // warp-uniform
     const int f1 = min(a.frames, f0 + kChunk);
-    const int np = (int)min((int64_t)P, a.npix - p0);
+    const int np = (int)max((int64_t)0, min((int64_t)P, a.npix - p0));
 
-    const spk_run_t* runs0 = a.runs + p0 * a.cap;
-    const double* vals0 = a.vals ? a.vals + p0 * a.cap : nullptr;
-    auto fetch = [&](int i, int q) {  // request run q of pixel i into its ring slot
-        unsigned char* dst = ring_at(i, q);
-        const size_t off = (size_t)i * a.cap + q;
+    auto entry = [&](int s, int q) -> unsigned char* { return ring + ((q & (K - 1)) * S + s) * G::RE; };
+    auto fetch = [&](int s, int q) {  // request run q of slot s
+        const int64_t p = pw + (int64_t)(s & 31) * P + (s >> 5);
+        const size_t off = (size_t)p * a.cap + q;
+        const uint32_t dst = ring_s + (uint32_t)(((q & (K - 1)) * S + s) * G::RE);
         if constexpr (sizeof(OUT) == 8) {
-            cp_async4(dst, &runs0[off].start);
-            cp_async8(dst + 8, vals0 + off);
+            cp_async4(dst, &a.runs[off].start);
+            cp_async8(dst + 8, a.vals + off);
         } else {
-            cp_async8(dst, runs0 + off);
+            cp_async8(dst, a.runs + off);
         }
     };
 
-    int rr[P], cn[P], ns[P];  // current run, run count, start of the next run
     uint32_t words[NW];
 #pragma unroll
     for (int k = 0; k < NW; ++k) words[k] = 0u;
 #pragma unroll
     for (int i = 0; i < P; ++i) {
-        rr[i] = -1;
-        cn[i] = 0;
-        ns[i] = INT_MAX;
+        const int s = i * 32 + lane;
+        int r = -1, n = 0;
         if (i < np) {
             const int64_t p = p0 + i;
-            const uint32_t n = a.counts[p];
-            if (n > 0 && n <= (uint32_t)a.cap) {  // overflowed pixels: k_fixup
-                cn[i] = (int)n;
-                const int r = a.tbl[(int64_t)c * a.npix + p];
-                rr[i] = r;
+            const uint32_t cn = a.counts[p];
+            if (cn > 0 && cn <= (uint32_t)a.cap) {  // overflowed pixels: k_fixup
+                n = (int)cn;
+                r = a.tbl[(int64_t)c * a.npix + p];
                 if (r >= 0) {  // value at the chunk start
-                    const size_t off = (size_t)i * a.cap + r;
+                    const size_t off = (size_t)p * a.cap + r;
                     if constexpr (sizeof(OUT) == 1)
-                        words[i >> 2] |= (runs0[off].intervals & 0xffu) << ((i & 3) * 8);
+                        words[i >> 2] |= (a.runs[off].intervals & 0xffu) << ((i & 3) * 8);
                     else if constexpr (sizeof(OUT) == 4)
-                        words[i] = runs0[off].intervals;
+                        words[i] = a.runs[off].intervals;
                     else {
-                        const unsigned long long b = __double_as_longlong(vals0[off]);
+                        const unsigned long long b = __double_as_longlong(a.vals[off]);
                         words[2 * i] = (uint32_t)b;
                         words[2 * i + 1] = (uint32_t)(b >> 32);
                     }
                 }
-                for (int q = r + 1; q < min((int)n, r + 1 + K); ++q) fetch(i, q);
+                for (int q = r + 1; q < min(n, r + 1 + K); ++q) fetch(s, q);
             }
         }
+        CUR[s] = r;
+        CNT[s] = n;
     }
     cp_async_commit();
 #pragma unroll
-    for (int f = 0; f < F; ++f) {
-        if constexpr (sizeof(OUT) == 1)
-            *reinterpret_cast<uint2*>(b_at(f)) = make_uint2(0u, 0u);
-        else
-            *reinterpret_cast<uint32_t*>(b_at(f)) = 0u;
-    }
-    cp_async_wait<0>();
+    for (int f = 0; f < F; ++f) *reinterpret_cast<uint2*>(B + (f * 32 + lane) * 8) = make_uint2(0u, 0u);
+    cp_async_wait_all();
 #pragma unroll
-    for (int i = 0; i < P; ++i)
-        if (rr[i] + 1 < cn[i]) ns[i] = *reinterpret_cast<const int*>(ring_at(i, rr[i] + 1));
+    for (int i = 0; i < P; ++i) {
+        const int s = i * 32 + lane;
+        const int q = CUR[s] + 1;
+        NXT[s] = q < CNT[s] ? *reinterpret_cast<const int*>(entry(s, q)) : INT_MAX;
+    }
+    __syncwarp();
 
     const size_t step = a.pitch * sizeof(OUT);
     char* ptr = reinterpret_cast<char*>(a.out) + ((size_t)f0 * a.pitch + (size_t)p0) * sizeof(OUT);
     const bool vec_ok = a.vec_ok && np == P;
 
-    // Ring safety: run q of a pixel is requested when run q-K is consumed.
-    // After wait_group 1 at a phase-A start, every request older than the
-    // previous phase A has landed, so reading run q is safe unless the pixel
-    // consumed >= K runs over this and the previous phase A (then wait for
-    // all).  Per-pixel 4-bit counters of consumed runs: nprev, ncur.
-    uint32_t ncur = 0;
     for (int t0 = f0; t0 < f1; t0 += F) {
         const int t1 = min(f1, t0 + F);
-        // phase A: bucket this sub-tile's value changes by frame
-        cp_async_wait<1>();
-        uint32_t nprev = ncur;
-        ncur = 0;
+        // ---- phase A (warp-cooperative): every value change of the warp's
+        // pixels inside [t0, t1) goes to its owner's D/B bucket.  Pending slots
+        // are compacted with ballots and spread over all 32 lanes; a round
+        // consumes one run per pending slot.  The ring of a slot holds runs
+        // requested at least K rounds (or one phase) ago; before reading an
+        // entry requested in this phase, all lanes drain their copies.
+        cp_async_wait_all();
+        __syncwarp();
+        for (int round = 1;; ++round) {
+            uint32_t bal[P];
+            int tot = 0;
 #pragma unroll
-        for (int i = 0; i < P; ++i) {
-            while (ns[i] < t1) {  // run q starts inside this sub-tile
-                const int q = rr[i] + 1;
-                const unsigned char* e = ring_at(i, q);
-                const int fo = ns[i] - t0;
-                if constexpr (sizeof(OUT) == 1) {
-                    d_at(fo)[i] = (uint8_t)reinterpret_cast<const uint32_t*>(e)[1];
-                    b_at(fo)[i] = 0xffu;
-                } else if constexpr (sizeof(OUT) == 4) {
-                    reinterpret_cast<uint32_t*>(d_at(fo))[i] = reinterpret_cast<const uint32_t*>(e)[1];
-                    *reinterpret_cast<uint32_t*>(b_at(fo)) |= 1u << i;
-                } else {
-                    reinterpret_cast<double*>(d_at(fo))[i] = *reinterpret_cast<const double*>(e + 8);
-                    *reinterpret_cast<uint32_t*>(b_at(fo)) |= 1u << i;
-                }
-                rr[i] = q;
-                ncur += 1u << (4 * i);
-                if (q + K < cn[i]) fetch(i, q + K);  // refill the slot just consumed
-                if (q + 1 < cn[i]) {
-                    if (((nprev >> (4 * i)) & 15u) + ((ncur >> (4 * i)) & 15u) >= (uint32_t)K) {
-                        asm volatile("cp.async.wait_all;" ::: "memory");
-                        nprev = ncur = 0;
-                    }
-                    ns[i] = *reinterpret_cast<const int*>(ring_at(i, q + 1));
-                } else {
-                    ns[i] = INT_MAX;
-                }
+            for (int i = 0; i < P; ++i) {
+                bal[i] = __ballot_sync(kFull, NXT[i * 32 + lane] < t1);
+                tot += __popc(bal[i]);
             }
+            if (tot == 0) break;
+            for (int k = lane; k < tot; k += 32) {
+                // k-th pending slot: row i = first row whose prefix covers k,
+                // column = (k - before)-th set bit of that row's ballot
+                int i = P - 1, before = 0, acc = 0;
+                uint32_t bi = bal[P - 1];
+                bool found = false;
+#pragma unroll
+                for (int j = 0; j < P; ++j) {
+                    const int pc = __popc(bal[j]);
+                    if (!found && k < acc + pc) {
+                        i = j;
+                        bi = bal[j];
+                        before = acc;
+                        found = true;
+                    }
+                    acc += pc;
+                }
+                const int col = __fns(bi, 0, k - before + 1);
+                const int s = i * 32 + col;
+                const int q = CUR[s] + 1;
+                const unsigned char* e = entry(s, q);
+                const int fo = *reinterpret_cast<const int*>(e) - t0;
+                unsigned char* dcell = D + (fo * 32 + col) * G::DE;
+                if constexpr (sizeof(OUT) == 8)
+                    reinterpret_cast<double*>(dcell)[i] = *reinterpret_cast<const double*>(e + 8);
+                else if constexpr (sizeof(OUT) == 4)
+                    reinterpret_cast<uint32_t*>(dcell)[i] = reinterpret_cast<const uint32_t*>(e)[1];
+                else
+                    dcell[i] = (uint8_t)reinterpret_cast<const uint32_t*>(e)[1];
+                B[(fo * 32 + col) * 8 + i] = 0xffu;
+                CUR[s] = q;
+                const int n = CNT[s];
+                if (q + K < n) fetch(s, q + K);  // refill the slot just consumed
+                NXT[s] = INT_MAX;
+                if (q + 1 < n) NXT[s] = -1 - q;  // next start read after the drain check
+            }
+            __syncwarp();
+            if (round % K == 0) {  // the next entries may have been requested this phase
+                cp_async_wait_all();
+                __syncwarp();
+            }
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+                const int s = i * 32 + lane;
+                const int v = NXT[s];
+                if (v < 0) NXT[s] = *reinterpret_cast<const int*>(entry(s, -1 - v + 1));
+            }
+            __syncwarp();
         }
         cp_async_commit();
-        // phase B: frames in order, one store per frame, pending values merged
+        // ---- phase B: frames in order, one store per frame, pending merged
         const int nf = t1 - t0;
 #pragma unroll 4
         for (int fo = 0; fo < nf; ++fo) {
+            const unsigned char* dcell = D + (fo * 32 + lane) * G::DE;
+            uint2* bcell = reinterpret_cast<uint2*>(B + (fo * 32 + lane) * 8);
+            const uint2 bm = *bcell;
             if constexpr (sizeof(OUT) == 1) {
-                const uint2 dv = *reinterpret_cast<const uint2*>(d_at(fo));
-                const uint2 bm = *reinterpret_cast<const uint2*>(b_at(fo));
-                *reinterpret_cast<uint2*>(b_at(fo)) = make_uint2(0u, 0u);
+                const uint2 dv = *reinterpret_cast<const uint2*>(dcell);
+                *bcell = make_uint2(0u, 0u);
                 words[0] = (words[0] & ~bm.x) | (dv.x & bm.x);
                 words[1] = (words[1] & ~bm.y) | (dv.y & bm.y);
             } else {
-                const uint32_t m = *reinterpret_cast<const uint32_t*>(b_at(fo));
-                if (m) {
-                    *reinterpret_cast<uint32_t*>(b_at(fo)) = 0u;
-                    const uint32_t* dw = reinterpret_cast<const uint32_t*>(d_at(fo));
+                if (bm.x | bm.y) {
+                    *bcell = make_uint2(0u, 0u);
+                    const uint32_t* dw = reinterpret_cast<const uint32_t*>(dcell);
 #pragma unroll
                     for (int i = 0; i < P; ++i) {
-                        const bool take = (m >> i) & 1u;
+                        const bool take = ((i < 4 ? bm.x : bm.y) >> ((i & 3) * 8)) & 1u;
                         if constexpr (sizeof(OUT) == 4) {
                             words[i] = take ? dw[i] : words[i];
                         } else {
@@ -339,10 +361,15 @@ __global__ void __launch_bounds__(kExpThreads) k_expand(ExpArgs a) {
 }
 
 size_t expand_smem_bytes(int out_size) {
-    const int per = out_size == 1 ? ExpSmem<uint8_t>::per_warp
-                  : out_size == 4 ? ExpSmem<float>::per_warp
-                                  : ExpSmem<double>::per_warp;
-    return (size_t)per * (kExpThreads / 32);
+    return out_size == 1 ? (size_t)ExpSmem<uint8_t>::per_warp * ExpGeo<uint8_t>::WARPS
+         : out_size == 4 ? (size_t)ExpSmem<float>::per_warp * ExpGeo<float>::WARPS
+                         : (size_t)ExpSmem<double>::per_warp * ExpGeo<double>::WARPS;
+}
+
+int expand_threads(int out_size) {
+    return 32 * (out_size == 1 ? ExpGeo<uint8_t>::WARPS
+               : out_size == 4 ? ExpGeo<float>::WARPS
+                               : ExpGeo<double>::WARPS);
 }
 
 int expand_pixels_per_lane(int out_size) {

@@ -79,6 +79,7 @@ template <typename OUT>
 __global__ void k_expand(ExpArgs a);
 size_t expand_smem_bytes(int out_size);   // dynamic shared memory of k_expand<OUT>
 int expand_pixels_per_lane(int out_size);
+int expand_threads(int out_size);
 template <int METHOD, typename OUT>
 __global__ void k_causal(CausalArgs a);
 
