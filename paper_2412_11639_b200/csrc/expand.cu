@@ -115,7 +115,7 @@ template <typename OUT>
 struct ExpGeo;
 template <>
 struct ExpGeo<uint8_t> {
-    static constexpr int P = 8, F = 16, K = 4, WARPS = 4;
+    static constexpr int P = 8, F = 16, K = 4, WARPS = 2;
 };
 template <>
 struct ExpGeo<float> {
@@ -145,7 +145,8 @@ struct ExpSmem {
     static constexpr int cur = S * 4, cnt = S * 4, nxt = S * 4;
     static constexpr int d = F * 32 * DE;
     static constexpr int b = F * 32 * 8;
-    static constexpr int per_warp = ring + cur + cnt + nxt + d + b;
+    static constexpr int queue = S * 2;
+    static constexpr int per_warp = ring + cur + cnt + nxt + d + b + queue;
 };
 
 __device__ __forceinline__ void cp_async8(uint32_t saddr, const void* gmem) {
@@ -171,6 +172,7 @@ __global__ void __launch_bounds__(ExpGeo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
     int* NXT = CNT + S;
     unsigned char* D = wb + G::ring + G::cur + G::cnt + G::nxt;
     unsigned char* B = D + G::d;
+    uint16_t* Q = reinterpret_cast<uint16_t*>(B + G::b);
     const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
 
     // warp geometry: lane l owns pixels pw + l*P + i
@@ -253,33 +255,39 @@ __global__ void __launch_bounds__(ExpGeo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
         cp_async_wait_all();
         __syncwarp();
         for (int round = 1;; ++round) {
-            uint32_t bal[P];
-            int tot = 0;
+            if (round > 1 && (round - 1) % K == 0) {  // entries requested in this phase
+                cp_async_wait_all();
+                __syncwarp();
+            }
+            // own pending slots; a slot consumed last round (NXT < 0) first
+            // learns its next start from the ring
+            uint32_t own = 0;
 #pragma unroll
             for (int i = 0; i < P; ++i) {
-                bal[i] = __ballot_sync(kFull, NXT[i * 32 + lane] < t1);
-                tot += __popc(bal[i]);
-            }
-            if (tot == 0) break;
-            for (int k = lane; k < tot; k += 32) {
-                // k-th pending slot: row i = first row whose prefix covers k,
-                // column = (k - before)-th set bit of that row's ballot
-                int i = P - 1, before = 0, acc = 0;
-                uint32_t bi = bal[P - 1];
-                bool found = false;
-#pragma unroll
-                for (int j = 0; j < P; ++j) {
-                    const int pc = __popc(bal[j]);
-                    if (!found && k < acc + pc) {
-                        i = j;
-                        bi = bal[j];
-                        before = acc;
-                        found = true;
-                    }
-                    acc += pc;
+                const int s = i * 32 + lane;
+                int v = NXT[s];
+                if (v < 0) {
+                    v = *reinterpret_cast<const int*>(entry(s, -v));
+                    NXT[s] = v;
                 }
-                const int col = __fns(bi, 0, k - before + 1);
-                const int s = i * 32 + col;
+                if (v < t1) own |= 1u << i;
+            }
+            // warp-exclusive prefix of the pending counts -> queue positions
+            const int cnt_l = __popc(own);
+            int incl = cnt_l;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += y;
+            }
+            const int tot = __shfl_sync(kFull, incl, 31);
+            if (tot == 0) break;
+            int pos = incl - cnt_l;
+            for (uint32_t m = own; m; m &= m - 1) Q[pos++] = (uint16_t)((__ffs(m) - 1) * 32 + lane);
+            __syncwarp();
+            for (int k = lane; k < tot; k += 32) {
+                const int s = Q[k];
+                const int i = s >> 5, col = s & 31;
                 const int q = CUR[s] + 1;
                 const unsigned char* e = entry(s, q);
                 const int fo = *reinterpret_cast<const int*>(e) - t0;
@@ -294,25 +302,34 @@ __global__ void __launch_bounds__(ExpGeo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
                 CUR[s] = q;
                 const int n = CNT[s];
                 if (q + K < n) fetch(s, q + K);  // refill the slot just consumed
-                NXT[s] = INT_MAX;
-                if (q + 1 < n) NXT[s] = -1 - q;  // next start read after the drain check
-            }
-            __syncwarp();
-            if (round % K == 0) {  // the next entries may have been requested this phase
-                cp_async_wait_all();
-                __syncwarp();
-            }
-#pragma unroll
-            for (int i = 0; i < P; ++i) {
-                const int s = i * 32 + lane;
-                const int v = NXT[s];
-                if (v < 0) NXT[s] = *reinterpret_cast<const int*>(entry(s, -1 - v + 1));
+                NXT[s] = q + 1 < n ? -(q + 1) : INT_MAX;
             }
             __syncwarp();
         }
         cp_async_commit();
         // ---- phase B: frames in order, one store per frame, pending merged
         const int nf = t1 - t0;
+        if constexpr (sizeof(OUT) == 1) {
+            if (nf == F && vec_ok) {  // steady state: batch the bucket reads for ILP
+                uint2 dv[F], bm[F];
+#pragma unroll
+                for (int fo = 0; fo < F; ++fo) {
+                    dv[fo] = *reinterpret_cast<const uint2*>(D + (fo * 32 + lane) * G::DE);
+                    bm[fo] = *reinterpret_cast<const uint2*>(B + (fo * 32 + lane) * 8);
+                }
+#pragma unroll
+                for (int fo = 0; fo < F; ++fo)
+                    *reinterpret_cast<uint2*>(B + (fo * 32 + lane) * 8) = make_uint2(0u, 0u);
+#pragma unroll
+                for (int fo = 0; fo < F; ++fo) {
+                    words[0] = (words[0] & ~bm[fo].x) | (dv[fo].x & bm[fo].x);
+                    words[1] = (words[1] & ~bm[fo].y) | (dv[fo].y & bm[fo].y);
+                    st_words(ptr, words);
+                    ptr += step;
+                }
+                continue;
+            }
+        }
 #pragma unroll 4
         for (int fo = 0; fo < nf; ++fo) {
             const unsigned char* dcell = D + (fo * 32 + lane) * G::DE;
