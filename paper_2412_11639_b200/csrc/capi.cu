@@ -136,42 +136,69 @@ int launch_segment(int method, const SegArgs& a, cudaStream_t s) {
     return SPK_OK;
 }
 
+// exclusive scan of n uint32 counts (three small launches)
+int launch_scan(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_t s) {
+    const int64_t nb = (n + kScanBlock - 1) / kScanBlock;
+    Scratch sums(s);
+    SPK_CK(sums.alloc((size_t)nb * sizeof(uint32_t)));
+    uint32_t* sp = static_cast<uint32_t*>(sums.p);
+    k_scan_blocks<<<(unsigned)nb, kScanBlock, 0, s>>>(in, out, sp, n);
+    SPK_LAUNCHED("k_scan_blocks");
+    k_scan_sums<<<1, kScanBlock, 0, s>>>(sp, nb);
+    SPK_LAUNCHED("k_scan_sums");
+    k_scan_add<<<(unsigned)nb, kScanBlock, 0, s>>>(out, sp, n);
+    SPK_LAUNCHED("k_scan_add");
+    return SPK_OK;
+}
+
+// K2b + scan + K2c + K3: run lists -> frames
 template <typename OUT>
-int launch_finalize(const SegArgs& sa, double* vals, cudaStream_t s) {
+int launch_expand(const SegArgs& sa, OUT* out, size_t out_pitch, cudaStream_t s) {
+    constexpr int GP = 32 * Geo<OUT>::P;
+    const int ngroups = (int)((sa.npix + GP - 1) / GP);
+    const int64_t nbins = (int64_t)sa.nchunks * ngroups * kBins;
+    Scratch vals(s), tblv(s), bins(s), offs(s), stream(s);
+    if (sizeof(OUT) == 8) SPK_CK(vals.alloc((size_t)sa.npix * sa.cap * sizeof(double)));
+    SPK_CK(tblv.alloc((size_t)sa.nchunks * sa.npix * sizeof(OUT)));
+    SPK_CK(bins.alloc((size_t)nbins * sizeof(uint32_t)));
+    SPK_CK(offs.alloc((size_t)nbins * sizeof(uint32_t)));
+    SPK_CK(stream.alloc((size_t)sa.npix * sa.cap * sizeof(Change<OUT>)));
     FinArgs f;
     f.runs = sa.runs;
-    f.vals = vals;
-    f.tbl = sa.tbl;
+    f.vals = static_cast<double*>(vals.p);
     f.counts = sa.counts;
     f.last = sa.last;
     f.npix = sa.npix;
     f.frames = sa.frames;
     f.cap = sa.cap;
     f.nchunks = sa.nchunks;
-    const unsigned blocks = (unsigned)((sa.npix + kFinThreads - 1) / kFinThreads);
-    k_finalize<OUT><<<blocks, kFinThreads, 0, s>>>(f);
-    SPK_LAUNCHED("k_finalize");
-    return SPK_OK;
-}
+    f.ngroups = ngroups;
+    f.tblv = tblv.p;
+    f.bins = static_cast<uint32_t*>(bins.p);
+    f.offs = static_cast<const uint32_t*>(offs.p);
+    f.stream = stream.p;
+    k_fin_values<OUT><<<ngroups, GP, 0, s>>>(f);
+    SPK_LAUNCHED("k_fin_values");
+    int rc = launch_scan(f.bins, static_cast<uint32_t*>(offs.p), nbins, s);
+    if (rc) return rc;
+    k_fin_scatter<OUT><<<ngroups, GP, 0, s>>>(f);
+    SPK_LAUNCHED("k_fin_scatter");
+    mark(1, s);
 
-template <typename OUT>
-int launch_expand(const SegArgs& sa, const double* vals, OUT* out, size_t out_pitch,
-                  cudaStream_t s) {
     ExpArgs e;
-    e.vals = vals;
-    e.runs = sa.runs;
-    e.tbl = sa.tbl;
-    e.counts = sa.counts;
-    e.last = sa.last;
+    e.tblv = tblv.p;
+    e.bins = f.bins;
+    e.offs = f.offs;
+    e.stream = stream.p;
     e.npix = sa.npix;
     e.frames = sa.frames;
-    e.cap = sa.cap;
+    e.nchunks = sa.nchunks;
+    e.ngroups = ngroups;
     e.out = out;
     e.pitch = out_pitch;
     e.vec_ok = ((reinterpret_cast<uintptr_t>(out) | (out_pitch * sizeof(OUT))) & 15) == 0;
-    const int nthr = expand_threads(sizeof(OUT));
-    const int64_t per_block = (int64_t)nthr * expand_pixels_per_lane(sizeof(OUT));
-    const unsigned bx = (unsigned)((sa.npix + per_block - 1) / per_block);
+    const int warps = Geo<OUT>::WARPS;
+    const unsigned bx = (unsigned)((ngroups + warps - 1) / warps);
     const size_t smem = expand_smem_bytes(sizeof(OUT));
     if (smem > 48 * 1024)
         SPK_CK(cudaFuncSetAttribute(k_expand<OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -179,7 +206,7 @@ int launch_expand(const SegArgs& sa, const double* vals, OUT* out, size_t out_pi
     for (int c0 = 0; c0 < sa.nchunks; c0 += 65535) {
         e.chunk0 = c0;
         const unsigned by = (unsigned)std::min(65535, sa.nchunks - c0);
-        k_expand<OUT><<<dim3(bx, by), nthr, smem, s>>>(e);
+        k_expand<OUT><<<dim3(bx, by), warps * 32, smem, s>>>(e);
         SPK_LAUNCHED("k_expand");
     }
     return SPK_OK;
@@ -256,23 +283,16 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
     a.frames = (int)g->frames;
     a.cap = run_capacity(g->frames);
     a.nchunks = (int)((g->frames + kChunk - 1) / kChunk);
-    Scratch runs(s), tbl(s), counts(s), last(s);
+    Scratch runs(s), counts(s), last(s);
     SPK_CK(runs.alloc((size_t)npix * a.cap * sizeof(spk_run_t)));
-    SPK_CK(tbl.alloc((size_t)npix * a.nchunks * sizeof(int32_t)));
     SPK_CK(counts.alloc((size_t)npix * sizeof(uint32_t)));
     SPK_CK(last.alloc((size_t)npix * sizeof(int32_t)));
     a.runs = static_cast<spk_run_t*>(runs.p);
-    a.tbl = static_cast<int32_t*>(tbl.p);
     a.counts = static_cast<uint32_t*>(counts.p);
     a.last = static_cast<int32_t*>(last.p);
     mark(0, s);
-    Scratch vals(s);
-    if (sizeof(OUT) == 8) SPK_CK(vals.alloc((size_t)npix * a.cap * sizeof(double)));
     if ((rc = launch_segment(method, a, s))) return rc;
-    if ((rc = launch_finalize<OUT>(a, static_cast<double*>(vals.p), s))) return rc;
-    mark(1, s);
-    if ((rc = launch_expand<OUT>(a, static_cast<const double*>(vals.p), out, out_pitch, s)))
-        return rc;
+    if ((rc = launch_expand<OUT>(a, out, out_pitch, s))) return rc;
     mark(2, s);
     rc = launch_fixup<OUT>(method, a, out, out_pitch, s);
     mark(3, s);
@@ -324,10 +344,7 @@ int spk_segment(const spk_geom* g, const void* d_planes, int method, spk_run* d_
     a.frames = (int)g->frames;
     a.cap = (int)run_cap;
     a.nchunks = (int)((g->frames + kChunk - 1) / kChunk);
-    Scratch tbl(s);
-    SPK_CK(tbl.alloc((size_t)npix * a.nchunks * sizeof(int32_t)));
     a.runs = d_runs;
-    a.tbl = static_cast<int32_t*>(tbl.p);
     a.counts = d_counts;
     a.last = d_last;
     return launch_segment(method, a, s);

@@ -13,8 +13,6 @@ using spk_run_t = ::spk_run;
 
 constexpr int kSegThreads = 64;  // 2 warps: fine-grained blocks balance 148 SMs
 constexpr int kBatch = 8;        // 32-frame groups per prefetch batch
-constexpr int kExpThreads = 128;
-constexpr int kFinThreads = 128;
 constexpr int kCausalWarps = 2;  // warps per TFI/TFP block
 
 struct SegArgs {
@@ -25,33 +23,77 @@ struct SegArgs {
     int cap;  // runs per pixel in `runs`
     int nchunks;
     spk_run_t* runs;
-    int32_t* tbl;
     uint32_t* counts;
     int32_t* last;
 };
 
-// K2b: run values + run table from the run lists
+// Geometry of the expand stage per output type: a warp owns a group of
+// GP = 32*P consecutive pixels (P per lane) and walks one kChunk-frame chunk
+// in sub-tiles of kSub frames (kBins sub-tiles per chunk).
+constexpr int kSub = 16;
+constexpr int kBins = kChunk / kSub;
+template <typename OUT>
+struct Geo;
+template <>
+struct Geo<uint8_t> {
+    static constexpr int P = 16, WARPS = 4;
+};
+template <>
+struct Geo<float> {
+    static constexpr int P = 8, WARPS = 2;
+};
+template <>
+struct Geo<double> {
+    static constexpr int P = 8, WARPS = 1;
+};
+
+// One value change of the frame-sorted change stream: frame offset in the
+// chunk (fo), pixel in the group (pix) and the new value.
+template <typename OUT>
+struct Change;
+template <>
+struct Change<uint8_t> {  // (fo << 17) | (pix << 8) | value
+    uint32_t w;
+};
+template <>
+struct Change<float> {
+    uint32_t key;  // (fo << 16) | pix
+    uint32_t bits;
+};
+template <>
+struct __align__(16) Change<double> {
+    uint32_t key;
+    uint32_t pad;
+    double v;
+};
+
+// K2b/K2c: run lists -> run values, value at every chunk start, and the
+// change stream sorted by (chunk, group, sub-tile)
 struct FinArgs {
-    spk_run_t* runs;  // in: {start, intervals}; out (u8/f32): {start, value bits}
-    double* vals;     // out (f64): value per run, same indexing as runs
-    int32_t* tbl;     // out: [nchunks][npix] run covering frame c*kChunk, -1 = none
+    spk_run_t* runs;  // in: {start, intervals}; pass 1 writes value bits (u8/f32)
+    double* vals;     // f64 run values (same indexing as runs)
     const uint32_t* counts;
     const int32_t* last;
     int64_t npix;
     int frames;
     int cap;
     int nchunks;
+    int ngroups;
+    void* tblv;        // [nchunks][npix] OUT: value at frame c*kChunk
+    uint32_t* bins;    // [nchunks][ngroups][kBins] change counts (pass 1)
+    const uint32_t* offs;  // exclusive prefix of bins (pass 2)
+    void* stream;      // Change<OUT>[total]
 };
 
 struct ExpArgs {
-    const double* vals;
-    const spk_run_t* runs;
-    const int32_t* tbl;
-    const uint32_t* counts;
-    const int32_t* last;
+    const void* tblv;
+    const uint32_t* bins;
+    const uint32_t* offs;
+    const void* stream;
     int64_t npix;
     int frames;
-    int cap;
+    int nchunks;
+    int ngroups;
     int chunk0;  // first chunk of this launch (blockIdx.y offset)
     void* out;
     size_t pitch;  // elements between frames
@@ -74,12 +116,16 @@ __global__ void k_segment(SegArgs a);
 template <int METHOD, typename OUT>
 __global__ void k_fixup(SegArgs a, OUT* out, size_t out_pitch);
 template <typename OUT>
-__global__ void k_finalize(FinArgs a);
+__global__ void k_fin_values(FinArgs a);
+template <typename OUT>
+__global__ void k_fin_scatter(FinArgs a);
 template <typename OUT>
 __global__ void k_expand(ExpArgs a);
-size_t expand_smem_bytes(int out_size);   // dynamic shared memory of k_expand<OUT>
-int expand_pixels_per_lane(int out_size);
-int expand_threads(int out_size);
+size_t expand_smem_bytes(int out_size);  // dynamic shared memory of k_expand<OUT>
+__global__ void k_scan_blocks(const uint32_t* in, uint32_t* out, uint32_t* sums, int64_t n);
+__global__ void k_scan_sums(uint32_t* sums, int64_t nb);
+__global__ void k_scan_add(uint32_t* out, const uint32_t* sums, int64_t n);
+constexpr int kScanBlock = 1024;
 template <int METHOD, typename OUT>
 __global__ void k_causal(CausalArgs a);
 
