@@ -20,6 +20,19 @@
 
 namespace spk {
 
+namespace {
+
+// predicated 8-byte store of a closed run: no branch in the scan loop
+__device__ __forceinline__ void st_run_if(bool pred, spk_run_t* addr, int rs, int cnt) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+        "@p st.global.v2.u32 [%1], {%2, %3};\n\t}" ::"r"((uint32_t)pred),
+        "l"(addr), "r"(rs), "r"(cnt)
+        : "memory");
+}
+
+}  // namespace
+
 template <int METHOD>
 __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     const int lane = threadIdx.x & 31;
@@ -70,10 +83,9 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
                     const int c = __clz(w);
                     w ^= 0x80000000u >> c;
                     int rs, cnt;
-                    if (sc.step(base + c, rs, cnt)) {
-                        rp[min(nrun, capm1)] = spk_run_t{(uint32_t)rs, (uint32_t)cnt};
-                        ++nrun;
-                    }
+                    const bool e = sc.step(base + c, rs, cnt);
+                    st_run_if(e, rp + min(nrun, capm1), rs, cnt);
+                    nrun += (int)e;
                 }
             }
         }

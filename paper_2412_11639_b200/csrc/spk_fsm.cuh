@@ -235,15 +235,17 @@ struct Scan {
         h0 = h1 = 0;
     }
 
-    // returns true when the run (rs, cnt) closed before this spike
+    // returns true when the run (rs, cnt) closed before this spike.  Written
+    // with bitwise logic only (no && / ||), so the compiler emits selects,
+    // not divergent branches.
     SPK_HD bool step(int n, int& out_rs, int& out_cnt) {
         const int t = n - last;
         const int d = t - lo;
         const bool in = (uint32_t)d <= hw;
-        const bool ext = !in && hw == 0 && (uint32_t)(d + 1) <= 2u;
-        const bool fbrk = !in && !ext;
+        const bool ext = (!in) & (hw == 0u) & ((uint32_t)(d + 1) <= 2u);
+        const bool fbrk = !(in | ext);
         bool brk = fbrk;
-        bool emit = fbrk && lo < kLim;
+        bool emit = fbrk & (lo < kLim);
         if (METHOD == kSSR) {
             const bool k = (t & 1) != 0;
             const int l = k ? l1 : l0;
@@ -252,15 +254,17 @@ struct Scan {
             const bool stale = l < sub0;
             const int gap = ii - l;
             const int gd = gap - glo;
-            const bool gempty = stale || glo >= kLim;
-            const bool gin = !gempty && (uint32_t)gd <= ghw;
-            const bool gext = !gempty && !gin && ghw == 0 && (uint32_t)(gd + 1) <= 2u;
-            const bool sbrk = !fbrk && !gempty && !gin && !gext;
-            brk = fbrk || sbrk;
-            emit = emit || sbrk;
-            const bool fresh = stale || brk;
-            const int nglo = fresh ? kNoPair : (glo >= kLim ? gap : (gext ? min(glo, gap) : glo));
-            const uint32_t nghw = (fresh || glo >= kLim) ? 0u : (ghw | (uint32_t)gext);
+            const bool gnone = glo >= kLim;
+            const bool gempty = stale | gnone;
+            const bool gin = (!gempty) & ((uint32_t)gd <= ghw);
+            const bool gext = (!gempty) & (!gin) & (ghw == 0u) & ((uint32_t)(gd + 1) <= 2u);
+            const bool sbrk = (!fbrk) & (!gempty) & (!gin) & (!gext);
+            brk = fbrk | sbrk;
+            emit = emit | sbrk;
+            const bool fresh = stale | brk;
+            const int keep = gext ? min(glo, gap) : glo;
+            const int nglo = fresh ? kNoPair : (gnone ? gap : keep);
+            const uint32_t nghw = (fresh | gnone) ? 0u : (ghw | (uint32_t)gext);
             l0 = k ? l0 : ii;
             l1 = k ? ii : l1;
             g0 = k ? g0 : nglo;
@@ -272,7 +276,8 @@ struct Scan {
         }
         out_rs = rs;
         out_cnt = cnt;
-        lo = fbrk ? t : (ext ? min(lo, t) : lo);
+        const int lext = ext ? min(lo, t) : lo;
+        lo = fbrk ? t : lext;
         hw = fbrk ? 0u : (hw | (uint32_t)ext);
         rs = brk ? last : rs;
         cnt = brk ? 1 : cnt + 1;
