@@ -79,13 +79,20 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
                 uint32_t w = transpose32(cur[j], lane);
                 if (!valid) w = 0;
                 const int base = (g0 + j) * 32;
-                while (w) {
-                    const int c = __clz(w);
-                    w ^= 0x80000000u >> c;
-                    int rs, cnt;
-                    const bool e = sc.step(base + c, rs, cnt);
-                    st_run_if(e, rp + min(nrun, capm1), rs, cnt);
-                    nrun += (int)e;
+                if constexpr (METHOD == kFSR) {
+                    fsr_word(sc, w, base, [&](bool e, int rs, int cnt) {
+                        st_run_if(e, rp + min(nrun, capm1), rs, cnt);
+                        nrun += (int)e;
+                    });
+                } else {
+                    while (w) {
+                        const int c = __clz(w);
+                        w ^= 0x80000000u >> c;
+                        int rs, cnt;
+                        const bool e = sc.step(base + c, rs, cnt);
+                        st_run_if(e, rp + min(nrun, capm1), rs, cnt);
+                        nrun += (int)e;
+                    }
                 }
             }
         }

@@ -293,4 +293,90 @@ struct Scan {
     }
 };
 
+// ---- bit helpers usable on host and device (the host build backs the CPU tests)
+SPK_HD int bit_clz(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return __clz(x);
+#else
+    return x ? __builtin_clz(x) : 32;
+#endif
+}
+SPK_HD int bit_ffs(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return __ffs(x);
+#else
+    return __builtin_ffs((int)x);
+#endif
+}
+SPK_HD int bit_popc(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return __popc(x);
+#else
+    return __builtin_popcount(x);
+#endif
+}
+// x >> min(s, 32)
+SPK_HD uint32_t bit_shr_clamp(uint32_t x, uint32_t, uint32_t s) {
+#ifdef __CUDA_ARCH__
+    return __funnelshift_rc(x, 0u, s);
+#else
+    return s >= 32u ? 0u : x >> s;
+#endif
+}
+
+// FSR over one 32-frame word (bit 31 = first frame), accepting spikes in
+// bulk.  While the open run's pair is [lo, lo+hw], a spike is in the run iff
+// its gap to the previous spike lies in the pair; bit-parallel over the word:
+//   * a spike has a predecessor at distance lo or lo+hw:  Q = S>>lo | S>>(lo+1)
+//   * no spike has another within lo-1 before it:          C = S & smear(S, lo-1)
+//   * the word's first spike is checked against `last` directly.
+// Everything before the first violating spike is accepted at once (cnt +=
+// popc, last = latest accepted); the violating spike -- a pair completion or
+// a break -- goes through the exact per-spike automaton, then the bulk test
+// resumes with the updated pair.  A word costs one iteration per event
+// instead of one per spike.
+// `emit(pred, rs, cnt)` stores a closed run when pred is true.
+template <class SC, class EMIT>
+SPK_HD void fsr_word(SC& sc, uint32_t S, int base, EMIT&& emit) {
+    if (!S) return;
+    const uint32_t So = S;
+    const uint32_t R1 = So >> 1, R2 = R1 | (R1 >> 1), R4 = R2 | (R2 >> 2), R8 = R4 | (R4 >> 4),
+                   R16 = R8 | (R8 >> 8), R32 = R16 | (R16 >> 16);
+    const int f = bit_clz(So);
+    const uint32_t fb = 0x80000000u >> f;
+    while (S) {
+        // ---- bulk: violations among the remaining spikes
+        const int lo = sc.lo;
+        const uint32_t hw = sc.hw;
+        const int L = lo - 1;  // gaps < lo are too short
+        uint32_t M;
+        if (L >= 32) {
+            M = R32;
+        } else {
+            const int k = 31 - bit_clz((uint32_t)(L > 1 ? L : 1));
+            const uint32_t Rk = k == 0 ? R1 : k == 1 ? R2 : k == 2 ? R4 : k == 3 ? R8 : R16;
+            M = L <= 0 ? 0u : (Rk | (Rk >> (L - (1 << k))));
+        }
+        const uint32_t Q = bit_shr_clamp(So, 0u, (uint32_t)lo) |
+                           (hw ? bit_shr_clamp(So, 0u, (uint32_t)lo + 1u) : 0u);
+        const int d0 = base + f - sc.last;
+        const bool bad0 = ((S & fb) != 0u) & ((uint32_t)(d0 - lo) > hw);
+        const uint32_t V = (S & M) | (S & ~Q & ~fb) | (bad0 ? fb : 0u);
+        const uint32_t p = V ? (uint32_t)bit_clz(V) : 32u;
+        const uint32_t A = S & ~bit_shr_clamp(0xffffffffu, 0u, p);
+        if (A) {
+            sc.cnt += bit_popc(A);
+            sc.last = base + 32 - bit_ffs(A);
+            S &= ~A;
+        }
+        if (!S) break;
+        // ---- the violating spike through the exact automaton
+        const int c = bit_clz(S);
+        S ^= 0x80000000u >> c;
+        int rs, cnt;
+        const bool e = sc.step(base + c, rs, cnt);
+        emit(e, rs, cnt);
+    }
+}
+
 }  // namespace spk

@@ -83,3 +83,53 @@ extern "C" long scan_runs(const uint8_t* bits, long frames, int method, long* st
     for (long k = 0; k < n && k < cap; ++k) end[k] = (k + 1 < n) ? start[k + 1] : last;
     return n;
 }
+
+// The segment kernel's word-level driver: 32-frame words with the first frame
+// in bit 31; FSR through fsr_word (bulk acceptance), SSR spike by spike.
+extern "C" long word_runs(const uint8_t* bits, long frames, int method, long* start, long* end,
+                          long* cnt, long cap) {
+    long n = 0, last = -1;
+    auto put = [&](bool e, int rs, int c) {
+        if (e) {
+            if (n < cap) {
+                start[n] = rs;
+                cnt[n] = c;
+            }
+            ++n;
+        }
+    };
+    auto go = [&](auto& sc, bool bulk) {
+        sc.init();
+        for (long base = 0; base < frames; base += 32) {
+            uint32_t w = 0;
+            for (int b = 0; b < 32 && base + b < frames; ++b)
+                if (bits[base + b]) {
+                    w |= 0x80000000u >> b;
+                    last = base + b;
+                }
+            if (bulk) {
+                spk::fsr_word(sc, w, (int)base, put);
+            } else {
+                while (w) {
+                    const int c = spk::bit_clz(w);
+                    w ^= 0x80000000u >> c;
+                    int rs, cc;
+                    const bool e = sc.step((int)base + c, rs, cc);
+                    put(e, rs, cc);
+                }
+            }
+        }
+        int rs, c;
+        const bool e = sc.tail(rs, c);
+        put(e, rs, c);
+    };
+    if (method == 0) {
+        spk::Scan<spk::kFSR> sc;
+        go(sc, true);
+    } else {
+        spk::Scan<spk::kSSR> sc;
+        go(sc, false);
+    }
+    for (long k = 0; k < n && k < cap; ++k) end[k] = (k + 1 < n) ? start[k + 1] : last;
+    return n;
+}

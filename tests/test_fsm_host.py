@@ -19,7 +19,8 @@ HDR = ROOT / "paper_2412_11639_b200" / "csrc" / "spk_fsm.cuh"
 
 @pytest.fixture(scope="module")
 def fsm():
-    if not LIB.exists() or LIB.stat().st_mtime < max(SRC.stat().st_mtime, HDR.stat().st_mtime):
+    if not LIB.exists() or LIB.stat().st_mtime < max(SRC.stat().st_mtime, HDR.stat().st_mtime,
+                                                      (HDR.parent / "spk_common.cuh").stat().st_mtime):
         subprocess.run(["nvcc", "-O2", "-std=c++17", "-arch=sm_100a", "-Xcompiler", "-fPIC",
                         "-shared", "-diag-suppress", "20011", f"-I{ROOT / 'include'}", "-o",
                         str(LIB), str(SRC)], check=True)
@@ -30,6 +31,8 @@ def fsm():
 
     h.scan_runs.restype = C.c_long
     h.scan_runs.argtypes = h.fsm_runs.argtypes
+    h.word_runs.restype = C.c_long
+    h.word_runs.argtypes = h.fsm_runs.argtypes
 
     def make(fn):
         def run(bits, m):
@@ -39,7 +42,7 @@ def fsm():
                    c.ctypes.data, cap)
             return s[:n], e[:n], c[:n]
         return run
-    return {"fsm": make(h.fsm_runs), "scan": make(h.scan_runs)}
+    return {"fsm": make(h.fsm_runs), "scan": make(h.scan_runs), "word": make(h.word_runs)}
 
 
 def if_stream(rng, t, segs, flips):
@@ -55,7 +58,7 @@ def if_stream(rng, t, segs, flips):
     return b ^ (rng.random(t) < flips).astype(np.uint8)
 
 
-@pytest.mark.parametrize("kind", ["fsm", "scan"])
+@pytest.mark.parametrize("kind", ["fsm", "scan", "word"])
 @pytest.mark.parametrize("family", ["noise", "if", "if_noisy", "if_rare_flips"])
 def test_fsm_matches_oracle(fsm, oracle, family, kind):
     run = fsm[kind]
@@ -72,7 +75,7 @@ def test_fsm_matches_oracle(fsm, oracle, family, kind):
             assert all(np.array_equal(x, y) for x, y in zip(got, want)), (family, m, t)
 
 
-@pytest.mark.parametrize("kind", ["fsm", "scan"])
+@pytest.mark.parametrize("kind", ["fsm", "scan", "word"])
 def test_fsm_golden_rows(fsm, golden_dir, kind):
     z = np.load(golden_dir / "rows.npz")
     for name in sorted({k.split("/")[0] for k in z.files}):
