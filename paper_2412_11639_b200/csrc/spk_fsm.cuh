@@ -315,6 +315,10 @@ SPK_HD int bit_popc(uint32_t x) {
     return __builtin_popcount(x);
 #endif
 }
+// cond ? a : b without a branch
+SPK_HD uint32_t bit_sel(bool cond, uint32_t a, uint32_t b) {
+    return b ^ ((a ^ b) & (0u - (uint32_t)cond));
+}
 // x >> min(s, 32)
 SPK_HD uint32_t bit_shr_clamp(uint32_t x, uint32_t, uint32_t s) {
 #ifdef __CUDA_ARCH__
@@ -345,30 +349,30 @@ SPK_HD void fsr_word(SC& sc, uint32_t S, int base, EMIT&& emit) {
     const int f = bit_clz(So);
     const uint32_t fb = 0x80000000u >> f;
     while (S) {
-        // ---- bulk: violations among the remaining spikes
+        // ---- bulk: violations among the remaining spikes (selects only)
         const int lo = sc.lo;
         const uint32_t hw = sc.hw;
-        const int L = lo - 1;  // gaps < lo are too short
-        uint32_t M;
-        if (L >= 32) {
-            M = R32;
-        } else {
-            const int k = 31 - bit_clz((uint32_t)(L > 1 ? L : 1));
-            const uint32_t Rk = k == 0 ? R1 : k == 1 ? R2 : k == 2 ? R4 : k == 3 ? R8 : R16;
-            M = L <= 0 ? 0u : (Rk | (Rk >> (L - (1 << k))));
-        }
+        const int L = lo - 1;  // gaps < lo are too short: smear S by 1..L
+        uint32_t Rk = R1;
+        Rk = bit_sel(L >= 2, R2, Rk);
+        Rk = bit_sel(L >= 4, R4, Rk);
+        Rk = bit_sel(L >= 8, R8, Rk);
+        Rk = bit_sel(L >= 16, R16, Rk);
+        const uint32_t Lc = (uint32_t)(L < 1 ? 1 : (L > 31 ? 31 : L));
+        const uint32_t pk = 0x80000000u >> bit_clz(Lc);  // largest power of two <= Lc
+        uint32_t M = Rk | (Rk >> (Lc - pk));
+        M = bit_sel(L >= 32, R32, M);
+        M = bit_sel(L <= 0, 0u, M);
         const uint32_t Q = bit_shr_clamp(So, 0u, (uint32_t)lo) |
-                           (hw ? bit_shr_clamp(So, 0u, (uint32_t)lo + 1u) : 0u);
+                           bit_sel(hw != 0u, bit_shr_clamp(So, 0u, (uint32_t)lo + 1u), 0u);
         const int d0 = base + f - sc.last;
         const bool bad0 = ((S & fb) != 0u) & ((uint32_t)(d0 - lo) > hw);
-        const uint32_t V = (S & M) | (S & ~Q & ~fb) | (bad0 ? fb : 0u);
+        const uint32_t V = (S & M) | (S & ~Q & ~fb) | bit_sel(bad0, fb, 0u);
         const uint32_t p = V ? (uint32_t)bit_clz(V) : 32u;
         const uint32_t A = S & ~bit_shr_clamp(0xffffffffu, 0u, p);
-        if (A) {
-            sc.cnt += bit_popc(A);
-            sc.last = base + 32 - bit_ffs(A);
-            S &= ~A;
-        }
+        sc.cnt += bit_popc(A);
+        sc.last = A ? base + 32 - bit_ffs(A) : sc.last;
+        S &= ~A;
         if (!S) break;
         // ---- the violating spike through the exact automaton
         const int c = bit_clz(S);
