@@ -112,6 +112,27 @@ void ensure_pool(int dev) {
     done.fetch_or(bit);
 }
 
+constexpr int kParts = 2;
+constexpr int64_t kSplitPixels = 1 << 16;
+
+// per (thread, device) auxiliary stream and events for the pipelined path
+int aux_resources(int dev, cudaStream_t& aux, cudaEvent_t* ev) {
+    struct Res {
+        cudaStream_t s = nullptr;
+        cudaEvent_t e[kParts + 2] = {};
+    };
+    thread_local Res res[16];
+    if (dev < 0 || dev >= 16) return fail(SPK_EINVAL, "spk: device index >= 16");
+    Res& r = res[dev];
+    if (!r.s) {
+        SPK_CK(cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking));
+        for (auto& e : r.e) SPK_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    aux = r.s;
+    for (int i = 0; i < kParts + 2; ++i) ev[i] = r.e[i];
+    return SPK_OK;
+}
+
 // RAII stream-ordered scratch
 struct Scratch {
     void* p = nullptr;
@@ -157,15 +178,13 @@ int launch_expand(const SegArgs& sa, OUT* out, size_t out_pitch, cudaStream_t s)
     constexpr int GP = 32 * Geo<OUT>::P;
     const int ngroups = (int)((sa.npix + GP - 1) / GP);
     const int64_t nbins = (int64_t)sa.nchunks * ngroups * kBins;
-    Scratch vals(s), tblv(s), bins(s), offs(s), stream(s);
-    if (sizeof(OUT) == 8) SPK_CK(vals.alloc((size_t)sa.npix * sa.cap * sizeof(double)));
+    Scratch tblv(s), bins(s), offs(s), stream(s);
     SPK_CK(tblv.alloc((size_t)sa.nchunks * sa.npix * sizeof(OUT)));
     SPK_CK(bins.alloc((size_t)nbins * sizeof(uint32_t)));
     SPK_CK(offs.alloc((size_t)nbins * sizeof(uint32_t)));
     SPK_CK(stream.alloc((size_t)sa.npix * sa.cap * sizeof(Change<OUT>)));
     FinArgs f;
     f.runs = sa.runs;
-    f.vals = static_cast<double*>(vals.p);
     f.counts = sa.counts;
     f.last = sa.last;
     f.npix = sa.npix;
@@ -290,13 +309,44 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
     a.runs = static_cast<spk_run_t*>(runs.p);
     a.counts = static_cast<uint32_t*>(counts.p);
     a.last = static_cast<int32_t*>(last.p);
-    mark(0, s);
-    if ((rc = launch_segment(method, a, s))) return rc;
-    if ((rc = launch_expand<OUT>(a, out, out_pitch, s))) return rc;
-    mark(2, s);
-    rc = launch_fixup<OUT>(method, a, out, out_pitch, s);
-    mark(3, s);
-    return rc;
+
+    // K2 is issue-bound, K2b..K3 are latency/HBM-bound: with enough pixels
+    // the volume is cut into pixel parts (multiples of 512 pixels) and the
+    // expand of part k runs on an auxiliary stream while K2 scans part k+1.
+    const int nparts = (npix >= kSplitPixels && !g_timing) ? kParts : 1;
+    if (nparts == 1) {
+        mark(0, s);
+        if ((rc = launch_segment(method, a, s))) return rc;
+        if ((rc = launch_expand<OUT>(a, out, out_pitch, s))) return rc;
+        mark(2, s);
+        rc = launch_fixup<OUT>(method, a, out, out_pitch, s);
+        mark(3, s);
+        return rc;
+    }
+    cudaStream_t aux;
+    cudaEvent_t ev[kParts + 2];
+    if ((rc = aux_resources(dev, aux, ev))) return rc;
+    SPK_CK(cudaEventRecord(ev[0], s));  // fork: aux sees the allocations above
+    SPK_CK(cudaStreamWaitEvent(aux, ev[0], 0));
+    for (int k = 0; k < nparts; ++k) {
+        const int64_t b0 = std::min(npix, ((npix * k / nparts) + 511) / 512 * 512);
+        const int64_t b1 = k + 1 == nparts ? npix : std::min(npix, ((npix * (k + 1) / nparts) + 511) / 512 * 512);
+        if (b1 <= b0) continue;
+        SegArgs ak = a;
+        ak.planes = static_cast<const char*>(planes) + b0 / 8;
+        ak.npix = b1 - b0;
+        ak.runs = a.runs + b0 * a.cap;
+        ak.counts = a.counts + b0;
+        ak.last = a.last + b0;
+        if ((rc = launch_segment(method, ak, s))) return rc;
+        SPK_CK(cudaEventRecord(ev[k + 1], s));
+        SPK_CK(cudaStreamWaitEvent(aux, ev[k + 1], 0));
+        if ((rc = launch_expand<OUT>(ak, out + b0, out_pitch, aux))) return rc;
+        if ((rc = launch_fixup<OUT>(method, ak, out + b0, out_pitch, aux))) return rc;
+    }
+    SPK_CK(cudaEventRecord(ev[kParts + 1], aux));  // join before the frees on s
+    SPK_CK(cudaStreamWaitEvent(s, ev[kParts + 1], 0));
+    return SPK_OK;
 }
 
 }  // namespace

@@ -11,13 +11,15 @@
 // otherwise.  To make the changes cheap to find, they are sorted by time once:
 //
 //   K2b k_fin_values  (block = one pixel group of GP = 32*P pixels)
-//       per pixel: run value 255*N/span (reconstruct.cpp:124; f64 bit-exact,
-//       u8 via the exact round-half-away integer form), the value at every
-//       chunk start (tblv), and per (chunk, group, sub-tile) the number of
-//       run starts (bins; shared-memory histogram per chunk, no global atomics)
+//       per pixel: the value at every chunk start (tblv) and, per (chunk,
+//       group, sub-tile), the number of run starts (bins; shared-memory
+//       histogram per chunk, no global atomics)
 //   scan              exclusive prefix of bins -> offs
 //   K2c k_fin_scatter the change stream: every run start as (frame offset,
-//       pixel, value), grouped by (chunk, group, sub-tile)
+//       pixel, value), grouped by (chunk, group, sub-tile).  Run values are
+//       255*N/span (reconstruct.cpp:124): f64 bit-exact, u8 via the exact
+//       round-half-away integer form; both passes recompute them (cheaper
+//       than writing them back to the run lists).
 //   K3  k_expand      one warp per (group, chunk): per sub-tile of kSub
 //       frames, the warp reads that sub-tile's changes (contiguous, coalesced)
 //       into per-frame value/mask buckets in shared memory, then every lane
@@ -31,13 +33,6 @@
 namespace spk {
 
 namespace {
-
-template <typename OUT>
-__device__ __forceinline__ uint32_t out_bits(OUT v);
-template <>
-__device__ __forceinline__ uint32_t out_bits<uint8_t>(uint8_t v) { return v; }
-template <>
-__device__ __forceinline__ uint32_t out_bits<float>(float v) { return __float_as_uint(v); }
 
 __device__ __forceinline__ void st_v4(char* p, uint4 v) {
     asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
@@ -58,8 +53,7 @@ __global__ void __launch_bounds__(32 * Geo<OUT>::P) k_fin_values(FinArgs a) {
     const bool valid = p < a.npix;
     int n = valid ? (int)a.counts[p] : 0;
     if (n > a.cap) n = 0;  // overflowed: k_fixup rewrites this pixel
-    spk_run_t* rp = a.runs + (valid ? p * a.cap : 0);
-    double* vp = a.vals ? a.vals + (valid ? p * a.cap : 0) : nullptr;
+    const spk_run_t* rp = a.runs + (valid ? p * a.cap : 0);
     const int lastp = valid ? a.last[p] : 0;
     OUT* tb = reinterpret_cast<OUT*>(a.tblv);
 
@@ -81,13 +75,8 @@ __global__ void __launch_bounds__(32 * Geo<OUT>::P) k_fin_values(FinArgs a) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 if (k < n && (int)cur.start < cend) {
-                    const OUT val = OutVal<OUT>::run(cur.intervals, nx[j].start - cur.start);
-                    if constexpr (sizeof(OUT) == 8)
-                        vp[k] = val;
-                    else
-                        rp[k].intervals = out_bits<OUT>(val);
+                    v = OutVal<OUT>::run(cur.intervals, nx[j].start - cur.start);
                     atomicAdd(&hist[((int)cur.start - c0) / kSub], 1u);
-                    v = val;
                     cur = nx[j];
                     ++k;
                 }
@@ -110,7 +99,7 @@ __global__ void __launch_bounds__(32 * Geo<OUT>::P) k_fin_scatter(FinArgs a) {
     int n = valid ? (int)a.counts[p] : 0;
     if (n > a.cap) n = 0;
     const spk_run_t* rp = a.runs + (valid ? p * a.cap : 0);
-    const double* vp = a.vals ? a.vals + (valid ? p * a.cap : 0) : nullptr;
+    const int lastp = valid ? a.last[p] : 0;
     Change<OUT>* st = reinterpret_cast<Change<OUT>*>(a.stream);
 
     int k = 0;
@@ -121,25 +110,28 @@ __global__ void __launch_bounds__(32 * Geo<OUT>::P) k_fin_scatter(FinArgs a) {
         const int c0 = c << kChunkLog2;
         const int cend = min(a.frames, c0 + kChunk);
         while (k < n) {
-            spk_run_t r[4];
+            // runs k..k+3 and the start of k+4 (a run's value needs the next start)
+            spk_run_t r[5];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) r[j] = k + j < n ? rp[k + j] : spk_run_t{0x7fffffffu, 0u};
+            for (int j = 0; j < 5; ++j)
+                r[j] = k + j < n ? rp[k + j] : spk_run_t{k + j == n ? (uint32_t)lastp : 0x7fffffffu, 0u};
             bool more = true;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 if (more && k < n && (int)r[j].start < cend) {
                     const uint32_t fo = r[j].start - (uint32_t)c0;
                     const uint32_t pos = atomicAdd(&cursor[fo / kSub], 1u);
+                    const OUT val = OutVal<OUT>::run(r[j].intervals, r[j + 1].start - r[j].start);
                     Change<OUT> ch;
                     if constexpr (sizeof(OUT) == 1) {
-                        ch.w = fo << 17 | (uint32_t)t << 8 | (r[j].intervals & 0xffu);
+                        ch.w = fo << 17 | (uint32_t)t << 8 | (uint32_t)val;
                     } else if constexpr (sizeof(OUT) == 4) {
                         ch.key = fo << 16 | (uint32_t)t;
-                        ch.bits = r[j].intervals;
+                        ch.bits = __float_as_uint(val);
                     } else {
                         ch.key = fo << 16 | (uint32_t)t;
                         ch.pad = 0;
-                        ch.v = vp[k];
+                        ch.v = val;
                     }
                     st[pos] = ch;
                     ++k;

@@ -70,8 +70,7 @@ struct __align__(16) Change<double> {
 // K2b/K2c: run lists -> run values, value at every chunk start, and the
 // change stream sorted by (chunk, group, sub-tile)
 struct FinArgs {
-    spk_run_t* runs;  // in: {start, intervals}; pass 1 writes value bits (u8/f32)
-    double* vals;     // f64 run values (same indexing as runs)
+    const spk_run_t* runs;  // {start, intervals} per pixel (K2 output)
     const uint32_t* counts;
     const int32_t* last;
     int64_t npix;
