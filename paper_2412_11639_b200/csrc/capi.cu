@@ -113,7 +113,8 @@ void ensure_pool(int dev) {
 }
 
 constexpr int kParts = 2;
-constexpr int64_t kSplitPixels = 1 << 16;
+// only volumes large enough to keep every SM busy with half the pixels
+constexpr int64_t kSplitPixels = 1 << 19;
 
 // per (thread, device) auxiliary stream and events for the pipelined path
 int aux_resources(int dev, cudaStream_t& aux, cudaEvent_t* ev) {
