@@ -173,17 +173,39 @@ int launch_scan(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_t s) {
     return SPK_OK;
 }
 
-// K2b + scan + K2c + K3: run lists -> frames
+// workspaces of the expand stage (allocated before K2, which fills `bins`)
 template <typename OUT>
-int launch_expand(const SegArgs& sa, OUT* out, size_t out_pitch, cudaStream_t s) {
+struct ExpandWork {
+    Scratch tblv, bins, offs, stream;
+    int ngroups = 0;
+    int64_t nbins = 0;
+    explicit ExpandWork(cudaStream_t s) : tblv(s), bins(s), offs(s), stream(s) {}
+};
+
+template <typename OUT>
+int prepare_expand(SegArgs& sa, ExpandWork<OUT>& w, cudaStream_t s) {
     constexpr int GP = 32 * Geo<OUT>::P;
-    const int ngroups = (int)((sa.npix + GP - 1) / GP);
-    const int64_t nbins = (int64_t)sa.nchunks * ngroups * kBins;
-    Scratch tblv(s), bins(s), offs(s), stream(s);
-    SPK_CK(tblv.alloc((size_t)sa.nchunks * sa.npix * sizeof(OUT)));
-    SPK_CK(bins.alloc((size_t)nbins * sizeof(uint32_t)));
-    SPK_CK(offs.alloc((size_t)nbins * sizeof(uint32_t)));
-    SPK_CK(stream.alloc((size_t)sa.npix * sa.cap * sizeof(Change<OUT>)));
+    w.ngroups = (int)((sa.npix + GP - 1) / GP);
+    w.nbins = (int64_t)sa.nchunks * w.ngroups * kBins;
+    SPK_CK(w.tblv.alloc((size_t)sa.nchunks * sa.npix * sizeof(OUT)));
+    SPK_CK(w.bins.alloc((size_t)w.nbins * sizeof(uint32_t)));
+    SPK_CK(w.offs.alloc((size_t)w.nbins * sizeof(uint32_t)));
+    SPK_CK(w.stream.alloc((size_t)sa.npix * sa.cap * sizeof(Change<OUT>)));
+    SPK_CK(cudaMemsetAsync(w.bins.p, 0, (size_t)w.nbins * sizeof(uint32_t), s));
+    sa.bins = static_cast<uint32_t*>(w.bins.p);
+    sa.ngroups = w.ngroups;
+    sa.gshift = GP == 512 ? 9 : 8;
+    return SPK_OK;
+}
+
+// scan + K2c + K3: run lists (+ K2's histogram) -> frames
+template <typename OUT>
+int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pitch,
+                  cudaStream_t s) {
+    constexpr int GP = 32 * Geo<OUT>::P;
+    int rc = launch_scan(static_cast<const uint32_t*>(w.bins.p), static_cast<uint32_t*>(w.offs.p),
+                         w.nbins, s);
+    if (rc) return rc;
     FinArgs f;
     f.runs = sa.runs;
     f.counts = sa.counts;
@@ -192,33 +214,28 @@ int launch_expand(const SegArgs& sa, OUT* out, size_t out_pitch, cudaStream_t s)
     f.frames = sa.frames;
     f.cap = sa.cap;
     f.nchunks = sa.nchunks;
-    f.ngroups = ngroups;
-    f.tblv = tblv.p;
-    f.bins = static_cast<uint32_t*>(bins.p);
-    f.offs = static_cast<const uint32_t*>(offs.p);
-    f.stream = stream.p;
-    k_fin_values<OUT><<<ngroups, GP, 0, s>>>(f);
-    SPK_LAUNCHED("k_fin_values");
-    int rc = launch_scan(f.bins, static_cast<uint32_t*>(offs.p), nbins, s);
-    if (rc) return rc;
-    k_fin_scatter<OUT><<<ngroups, GP, 0, s>>>(f);
+    f.ngroups = w.ngroups;
+    f.tblv = w.tblv.p;
+    f.offs = static_cast<const uint32_t*>(w.offs.p);
+    f.stream = w.stream.p;
+    k_fin_scatter<OUT><<<w.ngroups, GP, 0, s>>>(f);
     SPK_LAUNCHED("k_fin_scatter");
     mark(1, s);
 
     ExpArgs e;
-    e.tblv = tblv.p;
-    e.bins = f.bins;
+    e.tblv = w.tblv.p;
+    e.bins = static_cast<const uint32_t*>(w.bins.p);
     e.offs = f.offs;
-    e.stream = stream.p;
+    e.stream = w.stream.p;
     e.npix = sa.npix;
     e.frames = sa.frames;
     e.nchunks = sa.nchunks;
-    e.ngroups = ngroups;
+    e.ngroups = w.ngroups;
     e.out = out;
     e.pitch = out_pitch;
     e.vec_ok = ((reinterpret_cast<uintptr_t>(out) | (out_pitch * sizeof(OUT))) & 15) == 0;
     const int warps = Geo<OUT>::WARPS;
-    const unsigned bx = (unsigned)((ngroups + warps - 1) / warps);
+    const unsigned bx = (unsigned)((w.ngroups + warps - 1) / warps);
     const size_t smem = expand_smem_bytes(sizeof(OUT));
     if (smem > 48 * 1024)
         SPK_CK(cudaFuncSetAttribute(k_expand<OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -315,10 +332,15 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
     // the volume is cut into pixel parts (multiples of 512 pixels) and the
     // expand of part k runs on an auxiliary stream while K2 scans part k+1.
     const int nparts = (npix >= kSplitPixels && !g_timing) ? kParts : 1;
+    a.bins = nullptr;
+    a.ngroups = 0;
+    a.gshift = 0;
     if (nparts == 1) {
+        ExpandWork<OUT> w(s);
+        if ((rc = prepare_expand<OUT>(a, w, s))) return rc;
         mark(0, s);
         if ((rc = launch_segment(method, a, s))) return rc;
-        if ((rc = launch_expand<OUT>(a, out, out_pitch, s))) return rc;
+        if ((rc = launch_expand<OUT>(a, w, out, out_pitch, s))) return rc;
         mark(2, s);
         rc = launch_fixup<OUT>(method, a, out, out_pitch, s);
         mark(3, s);
@@ -339,10 +361,14 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
         ak.runs = a.runs + b0 * a.cap;
         ak.counts = a.counts + b0;
         ak.last = a.last + b0;
+        ExpandWork<OUT> w(aux);
+        if ((rc = prepare_expand<OUT>(ak, w, aux))) return rc;
+        SPK_CK(cudaEventRecord(ev[k + 1], aux));  // workspaces ready -> K2 may fill bins
+        SPK_CK(cudaStreamWaitEvent(s, ev[k + 1], 0));
         if ((rc = launch_segment(method, ak, s))) return rc;
         SPK_CK(cudaEventRecord(ev[k + 1], s));
         SPK_CK(cudaStreamWaitEvent(aux, ev[k + 1], 0));
-        if ((rc = launch_expand<OUT>(ak, out + b0, out_pitch, aux))) return rc;
+        if ((rc = launch_expand<OUT>(ak, w, out + b0, out_pitch, aux))) return rc;
         if ((rc = launch_fixup<OUT>(method, ak, out + b0, out_pitch, aux))) return rc;
     }
     SPK_CK(cudaEventRecord(ev[kParts + 1], aux));  // join before the frees on s
@@ -398,6 +424,9 @@ int spk_segment(const spk_geom* g, const void* d_planes, int method, spk_run* d_
     a.runs = d_runs;
     a.counts = d_counts;
     a.last = d_last;
+    a.bins = nullptr;
+    a.ngroups = 0;
+    a.gshift = 0;
     return launch_segment(method, a, s);
 }
 

@@ -10,16 +10,14 @@
 // store the packed current values of its pixels -- and touch only the changes
 // otherwise.  To make the changes cheap to find, they are sorted by time once:
 //
-//   K2b k_fin_values  (block = one pixel group of GP = 32*P pixels)
-//       per pixel: the value at every chunk start (tblv) and, per (chunk,
-//       group, sub-tile), the number of run starts (bins; shared-memory
-//       histogram per chunk, no global atomics)
+//   K2  (segment.cu) counts, while it emits runs, the run starts per (chunk,
+//       pixel group, sub-tile) -- bins, one predicated RED per run
 //   scan              exclusive prefix of bins -> offs
-//   K2c k_fin_scatter the change stream: every run start as (frame offset,
-//       pixel, value), grouped by (chunk, group, sub-tile).  Run values are
-//       255*N/span (reconstruct.cpp:124): f64 bit-exact, u8 via the exact
-//       round-half-away integer form; both passes recompute them (cheaper
-//       than writing them back to the run lists).
+//   K2c k_fin_scatter (block = one pixel group of GP = 32*P pixels) the value
+//       at every chunk start (tblv) and the change stream: every run start as
+//       (frame offset, pixel, value), grouped by (chunk, group, sub-tile).
+//       Run values are 255*N/span (reconstruct.cpp:124): f64 bit-exact, u8 via
+//       the exact round-half-away integer form.
 //   K3  k_expand      one warp per (group, chunk): per sub-tile of kSub
 //       frames, the warp reads that sub-tile's changes (contiguous, coalesced)
 //       into per-frame value/mask buckets in shared memory, then every lane
@@ -42,52 +40,11 @@ __device__ __forceinline__ void st_v4(char* p, uint4 v) {
 
 }  // namespace
 
-// ------------------------------------------------------------ K2b values --
-template <typename OUT>
-__global__ void __launch_bounds__(32 * Geo<OUT>::P) k_fin_values(FinArgs a) {
-    constexpr int GP = 32 * Geo<OUT>::P;
-    __shared__ uint32_t hist[kBins];
-    const int g = blockIdx.x;
-    const int t = threadIdx.x;
-    const int64_t p = (int64_t)g * GP + t;
-    const bool valid = p < a.npix;
-    int n = valid ? (int)a.counts[p] : 0;
-    if (n > a.cap) n = 0;  // overflowed: k_fixup rewrites this pixel
-    const spk_run_t* rp = a.runs + (valid ? p * a.cap : 0);
-    const int lastp = valid ? a.last[p] : 0;
-    OUT* tb = reinterpret_cast<OUT*>(a.tblv);
-
-    int k = 0;                                          // next run to value
-    spk_run_t cur = n > 0 ? rp[0] : spk_run_t{0x7fffffffu, 0u};
-    OUT v = OUT(0);                                     // value before `cur`
-    for (int c = 0; c < a.nchunks; ++c) {
-        if (t < kBins) hist[t] = 0;
-        __syncthreads();
-        const int c0 = c << kChunkLog2;
-        const int cend = min(a.frames, c0 + kChunk);
-        if (valid) tb[(int64_t)c * a.npix + p] = v;
-        while (k < n && (int)cur.start < cend) {
-            // the next few runs are loaded together to overlap their latency
-            spk_run_t nx[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                nx[j] = k + 1 + j < n ? rp[k + 1 + j] : spk_run_t{(uint32_t)lastp, 0u};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (k < n && (int)cur.start < cend) {
-                    v = OutVal<OUT>::run(cur.intervals, nx[j].start - cur.start);
-                    atomicAdd(&hist[((int)cur.start - c0) / kSub], 1u);
-                    cur = nx[j];
-                    ++k;
-                }
-            }
-        }
-        __syncthreads();
-        if (t < kBins) a.bins[((int64_t)c * a.ngroups + g) * kBins + t] = hist[t];
-    }
-}
-
 // ----------------------------------------------------------- K2c scatter --
+// Block = one pixel group; walks the chunks in order.  Per chunk: the value at
+// the chunk start (tblv) and every run start inside the chunk as a change at
+// its (sub-tile) slot; slots come from the exclusive scan of the histogram the
+// segment kernel counted (same bins, same order of runs).
 template <typename OUT>
 __global__ void __launch_bounds__(32 * Geo<OUT>::P) k_fin_scatter(FinArgs a) {
     constexpr int GP = 32 * Geo<OUT>::P;
@@ -96,32 +53,38 @@ __global__ void __launch_bounds__(32 * Geo<OUT>::P) k_fin_scatter(FinArgs a) {
     const int t = threadIdx.x;
     const int64_t p = (int64_t)g * GP + t;
     const bool valid = p < a.npix;
-    int n = valid ? (int)a.counts[p] : 0;
-    if (n > a.cap) n = 0;
+    const uint32_t cnt = valid ? a.counts[p] : 0u;
+    const bool over = cnt > (uint32_t)a.cap;  // k_fixup rewrites it: values are don't-care
+    const int n = (int)min(cnt, (uint32_t)a.cap);
     const spk_run_t* rp = a.runs + (valid ? p * a.cap : 0);
     const int lastp = valid ? a.last[p] : 0;
     Change<OUT>* st = reinterpret_cast<Change<OUT>*>(a.stream);
+    OUT* tb = reinterpret_cast<OUT*>(a.tblv);
 
     int k = 0;
+    OUT cur = OUT(0);  // value of the run covering the current frame (0 = lead)
     for (int c = 0; c < a.nchunks; ++c) {
         const int64_t b0 = ((int64_t)c * a.ngroups + g) * kBins;
         if (t < kBins) cursor[t] = a.offs[b0 + t];
         __syncthreads();
         const int c0 = c << kChunkLog2;
         const int cend = min(a.frames, c0 + kChunk);
+        if (valid) tb[(int64_t)c * a.npix + p] = cur;
         while (k < n) {
             // runs k..k+3 and the start of k+4 (a run's value needs the next start)
             spk_run_t r[5];
 #pragma unroll
             for (int j = 0; j < 5; ++j)
-                r[j] = k + j < n ? rp[k + j] : spk_run_t{k + j == n ? (uint32_t)lastp : 0x7fffffffu, 0u};
+                r[j] = k + j < n ? rp[k + j]
+                                 : spk_run_t{k + j == n ? (uint32_t)lastp : 0x7fffffffu, 0u};
             bool more = true;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 if (more && k < n && (int)r[j].start < cend) {
                     const uint32_t fo = r[j].start - (uint32_t)c0;
                     const uint32_t pos = atomicAdd(&cursor[fo / kSub], 1u);
-                    const OUT val = OutVal<OUT>::run(r[j].intervals, r[j + 1].start - r[j].start);
+                    const OUT val = over ? OUT(0)
+                                         : OutVal<OUT>::run(r[j].intervals, r[j + 1].start - r[j].start);
                     Change<OUT> ch;
                     if constexpr (sizeof(OUT) == 1) {
                         ch.w = fo << 17 | (uint32_t)t << 8 | (uint32_t)val;
@@ -134,6 +97,7 @@ __global__ void __launch_bounds__(32 * Geo<OUT>::P) k_fin_scatter(FinArgs a) {
                         ch.v = val;
                     }
                     st[pos] = ch;
+                    cur = val;
                     ++k;
                 } else {
                     more = false;
@@ -145,9 +109,6 @@ __global__ void __launch_bounds__(32 * Geo<OUT>::P) k_fin_scatter(FinArgs a) {
     }
 }
 
-template __global__ void k_fin_values<uint8_t>(FinArgs);
-template __global__ void k_fin_values<float>(FinArgs);
-template __global__ void k_fin_values<double>(FinArgs);
 template __global__ void k_fin_scatter<uint8_t>(FinArgs);
 template __global__ void k_fin_scatter<float>(FinArgs);
 template __global__ void k_fin_scatter<double>(FinArgs);
@@ -240,10 +201,36 @@ __global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
         off = __shfl_sync(kFull, sub < 32 ? off_lo : off_hi, sub & 31);
         n = __shfl_sync(kFull, sub < 32 ? cnt_lo : cnt_hi, sub & 31);
     };
+    // changes of the current sub-tile prefetched into registers (R per lane),
+    // loaded while the previous sub-tile's frames are being stored
+    constexpr int R = sizeof(OUT) == 8 ? 2 : 4;
     uint32_t off, n;
     bin_of(0, off, n);
-    Change<OUT> pre{};  // prefetched first change of the current sub-tile (per lane)
-    if ((uint32_t)lane < n) pre = st[off + lane];
+    Change<OUT> pre[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+        if ((uint32_t)(lane + 32 * i) < n) pre[i] = st[off + lane + 32 * i];
+
+    auto bucket = [&](const Change<OUT>& ch, int sub) {
+        uint32_t fo, pix;
+        if constexpr (sizeof(OUT) == 1) {
+            fo = ch.w >> 17;
+            pix = (ch.w >> 8) & 0x1ffu;
+        } else {
+            fo = ch.key >> 16;
+            pix = ch.key & 0xffffu;
+        }
+        const int fs = (int)fo - sub * kSub;  // frame within the sub-tile
+        const int own = (int)(pix / P), i = (int)(pix % P);
+        unsigned char* dcell = D + (fs * 32 + own) * G::DE;
+        if constexpr (sizeof(OUT) == 1)
+            dcell[i] = (uint8_t)ch.w;
+        else if constexpr (sizeof(OUT) == 4)
+            reinterpret_cast<uint32_t*>(dcell)[i] = ch.bits;
+        else
+            reinterpret_cast<double*>(dcell)[i] = ch.v;
+        B[(fs * 32 + own) * P + i] = 0xffu;
+    };
 
     for (int sub = 0; sub < kBins; ++sub) {
         const int t0 = f0 + sub * kSub;
@@ -251,32 +238,16 @@ __global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
         // ---- phase A: this sub-tile's changes -> owners' buckets
         uint32_t noff = 0, nn = 0;
         if (sub + 1 < kBins) bin_of(sub + 1, noff, nn);
-        for (uint32_t k = lane; k < n; k += 32) {
-            const Change<OUT> ch = k == (uint32_t)lane ? pre : st[off + k];
-            uint32_t fo, pix;
-            if constexpr (sizeof(OUT) == 1) {
-                fo = ch.w >> 17;
-                pix = (ch.w >> 8) & 0x1ffu;
-            } else {
-                fo = ch.key >> 16;
-                pix = ch.key & 0xffffu;
-            }
-            const int fs = (int)fo - sub * kSub;  // frame within the sub-tile
-            const int own = (int)(pix / P), i = (int)(pix % P);
-            unsigned char* dcell = D + (fs * 32 + own) * G::DE;
-            if constexpr (sizeof(OUT) == 1)
-                dcell[i] = (uint8_t)ch.w;
-            else if constexpr (sizeof(OUT) == 4)
-                reinterpret_cast<uint32_t*>(dcell)[i] = ch.bits;
-            else
-                reinterpret_cast<double*>(dcell)[i] = ch.v;
-            B[(fs * 32 + own) * P + i] = 0xffu;
-        }
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+            if ((uint32_t)(lane + 32 * i) < n) bucket(pre[i], sub);
+        for (uint32_t k = lane + 32 * R; k < n; k += 32) bucket(st[off + k], sub);
         __syncwarp();
-        // prefetch the next sub-tile's first changes while this one is stored
         off = noff;
         n = nn;
-        if ((uint32_t)lane < n) pre = st[off + lane];
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+            if ((uint32_t)(lane + 32 * i) < n) pre[i] = st[off + lane + 32 * i];
         // ---- phase B: frames in order, one store per frame
         const int nf = min(kSub, f1 - t0);
 #pragma unroll 4

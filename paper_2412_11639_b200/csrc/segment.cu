@@ -31,6 +31,15 @@ __device__ __forceinline__ void st_run_if(bool pred, spk_run_t* addr, int rs, in
         : "memory");
 }
 
+// predicated histogram increment (no return value: RED)
+__device__ __forceinline__ void red_if(bool pred, uint32_t* addr) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+        "@p red.global.add.u32 [%1], 1;\n\t}" ::"r"((uint32_t)pred),
+        "l"(addr)
+        : "memory");
+}
+
 }  // namespace
 
 template <int METHOD>
@@ -53,6 +62,16 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     Scan<METHOD> sc;
     sc.init();
     int nrun = 0;
+    // bins[(c * ngroups + g) * kBins + sub] for a run starting at frame rs
+    uint32_t* const binp = a.bins ? a.bins + (valid ? (p >> a.gshift) : 0) * kBins : nullptr;
+    const int64_t bin_row = (int64_t)a.ngroups * kBins;
+    auto emit = [&](bool e, int rs, int cnt) {
+        st_run_if(e, rp + min(nrun, capm1), rs, cnt);
+        if (binp)
+            red_if(e & (nrun <= capm1),
+                   binp + (rs >> kChunkLog2) * bin_row + ((rs & (kChunk - 1)) / kSub));
+        nrun += (int)e;
+    };
 
     uint32_t nxt[kBatch];
 #pragma unroll
@@ -80,18 +99,14 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
                 if (!valid) w = 0;
                 const int base = (g0 + j) * 32;
                 if constexpr (METHOD == kFSR) {
-                    fsr_word(sc, w, base, [&](bool e, int rs, int cnt) {
-                        st_run_if(e, rp + min(nrun, capm1), rs, cnt);
-                        nrun += (int)e;
-                    });
+                    fsr_word(sc, w, base, emit);
                 } else {
                     while (w) {
                         const int c = __clz(w);
                         w ^= 0x80000000u >> c;
                         int rs, cnt;
                         const bool e = sc.step(base + c, rs, cnt);
-                        st_run_if(e, rp + min(nrun, capm1), rs, cnt);
-                        nrun += (int)e;
+                        emit(e, rs, cnt);
                     }
                 }
             }
@@ -99,10 +114,8 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     }
     if (valid) {
         int rs, cnt;
-        if (sc.tail(rs, cnt)) {
-            rp[min(nrun, capm1)] = spk_run_t{(uint32_t)rs, (uint32_t)cnt};
-            ++nrun;
-        }
+        const bool e = sc.tail(rs, cnt);
+        emit(e, rs, cnt);
         a.counts[p] = (uint32_t)nrun;
         a.last[p] = sc.last == kNoSpike ? -1 : sc.last;
     }

@@ -25,6 +25,11 @@ struct SegArgs {
     spk_run_t* runs;
     uint32_t* counts;
     int32_t* last;
+    // optional (nullptr = off): per (chunk, pixel group, sub-tile) run-start
+    // histogram for the expand stage, counted as runs are emitted
+    uint32_t* bins;
+    int ngroups;
+    int gshift;  // log2 of the pixel-group size
 };
 
 // Geometry of the expand stage per output type: a warp owns a group of
@@ -67,8 +72,8 @@ struct __align__(16) Change<double> {
     double v;
 };
 
-// K2b/K2c: run lists -> run values, value at every chunk start, and the
-// change stream sorted by (chunk, group, sub-tile)
+// K2c: run lists -> value at every chunk start and the change stream sorted
+// by (chunk, group, sub-tile)
 struct FinArgs {
     const spk_run_t* runs;  // {start, intervals} per pixel (K2 output)
     const uint32_t* counts;
@@ -78,9 +83,8 @@ struct FinArgs {
     int cap;
     int nchunks;
     int ngroups;
-    void* tblv;        // [nchunks][npix] OUT: value at frame c*kChunk
-    uint32_t* bins;    // [nchunks][ngroups][kBins] change counts (pass 1)
-    const uint32_t* offs;  // exclusive prefix of bins (pass 2)
+    void* tblv;            // [nchunks][npix] OUT: value at frame c*kChunk
+    const uint32_t* offs;  // exclusive prefix of the K2 run-start histogram
     void* stream;      // Change<OUT>[total]
 };
 
@@ -114,8 +118,6 @@ template <int METHOD>
 __global__ void k_segment(SegArgs a);
 template <int METHOD, typename OUT>
 __global__ void k_fixup(SegArgs a, OUT* out, size_t out_pitch);
-template <typename OUT>
-__global__ void k_fin_values(FinArgs a);
 template <typename OUT>
 __global__ void k_fin_scatter(FinArgs a);
 template <typename OUT>

@@ -232,8 +232,8 @@ def test_launch_count_and_determinism():
     v = spk.synth("static", 1, 400, 250, 2000)
     capi.lib().spk_launch_count(1)
     a = run(v, "fsr")
-    # segment, fin_values, scan x3, fin_scatter, expand, fixup (one pixel part)
-    assert capi.lib().spk_launch_count(1) == 8
+    # segment, scan x3, fin_scatter, expand, fixup (one pixel part)
+    assert capi.lib().spk_launch_count(1) == 7
     b = run(v, "fsr")
     assert torch.equal(a, b)
     capi.lib().spk_launch_count(1)
