@@ -65,11 +65,12 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     // bins[(c * ngroups + g) * kBins + sub] for a run starting at frame rs
     uint32_t* const binp = a.bins ? a.bins + (valid ? (p >> a.gshift) : 0) * kBins : nullptr;
     const int64_t bin_row = (int64_t)a.ngroups * kBins;
+    // runs beyond the capacity are counted (overflow -> k_fixup) but neither
+    // stored nor binned, so the stored runs and the histogram always agree
     auto emit = [&](bool e, int rs, int cnt) {
-        st_run_if(e, rp + min(nrun, capm1), rs, cnt);
-        if (binp)
-            red_if(e & (nrun <= capm1),
-                   binp + (rs >> kChunkLog2) * bin_row + ((rs & (kChunk - 1)) / kSub));
+        const bool keep = e & (nrun <= capm1);
+        st_run_if(keep, rp + min(nrun, capm1), rs, cnt);
+        if (binp) red_if(keep, binp + (rs >> kChunkLog2) * bin_row + ((rs & (kChunk - 1)) / kSub));
         nrun += (int)e;
     };
 
