@@ -191,21 +191,16 @@ int prepare_expand(SegArgs& sa, ExpandWork<OUT>& w, cudaStream_t s) {
     SPK_CK(w.bins.alloc((size_t)w.nbins * sizeof(uint32_t)));
     SPK_CK(w.offs.alloc((size_t)w.nbins * sizeof(uint32_t)));
     SPK_CK(w.stream.alloc((size_t)sa.npix * sa.cap * sizeof(Change<OUT>)));
-    SPK_CK(cudaMemsetAsync(w.bins.p, 0, (size_t)w.nbins * sizeof(uint32_t), s));
-    sa.bins = static_cast<uint32_t*>(w.bins.p);
-    sa.ngroups = w.ngroups;
-    sa.gshift = GP == 512 ? 9 : 8;
+    // chunks before a pixel's first run keep value 0
+    SPK_CK(cudaMemsetAsync(w.tblv.p, 0, (size_t)sa.nchunks * sa.npix * sizeof(OUT), s));
     return SPK_OK;
 }
 
-// scan + K2c + K3: run lists (+ K2's histogram) -> frames
+// K2b + scan + K2c + K3: run lists -> frames
 template <typename OUT>
 int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pitch,
                   cudaStream_t s) {
     constexpr int GP = 32 * Geo<OUT>::P;
-    int rc = launch_scan(static_cast<const uint32_t*>(w.bins.p), static_cast<uint32_t*>(w.offs.p),
-                         w.nbins, s);
-    if (rc) return rc;
     FinArgs f;
     f.runs = sa.runs;
     f.counts = sa.counts;
@@ -215,10 +210,16 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     f.cap = sa.cap;
     f.nchunks = sa.nchunks;
     f.ngroups = w.ngroups;
+    f.bins = static_cast<uint32_t*>(w.bins.p);
     f.tblv = w.tblv.p;
     f.offs = static_cast<const uint32_t*>(w.offs.p);
     f.stream = w.stream.p;
-    k_fin_scatter<OUT><<<w.ngroups, GP, 0, s>>>(f);
+    const dim3 fgrid((unsigned)w.ngroups, (unsigned)((sa.nchunks + kFinWindow - 1) / kFinWindow));
+    k_fin_bins<GP><<<fgrid, kFinWarps * 32, 0, s>>>(f);
+    SPK_LAUNCHED("k_fin_bins");
+    int rc = launch_scan(f.bins, static_cast<uint32_t*>(w.offs.p), w.nbins, s);
+    if (rc) return rc;
+    k_fin_scatter<OUT><<<fgrid, kFinWarps * 32, 0, s>>>(f);
     SPK_LAUNCHED("k_fin_scatter");
     mark(1, s);
 
@@ -332,9 +333,6 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
     // the volume is cut into pixel parts (multiples of 512 pixels) and the
     // expand of part k runs on an auxiliary stream while K2 scans part k+1.
     const int nparts = (npix >= kSplitPixels && !g_timing) ? kParts : 1;
-    a.bins = nullptr;
-    a.ngroups = 0;
-    a.gshift = 0;
     if (nparts == 1) {
         ExpandWork<OUT> w(s);
         if ((rc = prepare_expand<OUT>(a, w, s))) return rc;
@@ -424,9 +422,6 @@ int spk_segment(const spk_geom* g, const void* d_planes, int method, spk_run* d_
     a.runs = d_runs;
     a.counts = d_counts;
     a.last = d_last;
-    a.bins = nullptr;
-    a.ngroups = 0;
-    a.gshift = 0;
     return launch_segment(method, a, s);
 }
 

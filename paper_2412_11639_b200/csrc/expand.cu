@@ -10,14 +10,15 @@
 // store the packed current values of its pixels -- and touch only the changes
 // otherwise.  To make the changes cheap to find, they are sorted by time once:
 //
-//   K2  (segment.cu) counts, while it emits runs, the run starts per (chunk,
-//       pixel group, sub-tile) -- bins, one predicated RED per run
+//   K2b k_fin_bins    run starts per (chunk, pixel group, sub-tile) -> bins
 //   scan              exclusive prefix of bins -> offs
-//   K2c k_fin_scatter (block = one pixel group of GP = 32*P pixels) the value
-//       at every chunk start (tblv) and the change stream: every run start as
-//       (frame offset, pixel, value), grouped by (chunk, group, sub-tile).
-//       Run values are 255*N/span (reconstruct.cpp:124): f64 bit-exact, u8 via
+//   K2c k_fin_scatter the value at every chunk start (tblv; chunks before the
+//       first run stay 0) and the change stream: every run start as (frame
+//       offset, pixel, value), grouped by (chunk, group, sub-tile).  Run
+//       values are 255*N/span (reconstruct.cpp:124): f64 bit-exact, u8 via
 //       the exact round-half-away integer form.
+//   (K2b/K2c: block = pixel group x chunk window, warp = one pixel, 32 runs
+//   per coalesced load, shared-memory counters.)
 //   K3  k_expand      one warp per (group, chunk): per sub-tile of kSub
 //       frames, the warp reads that sub-tile's changes (contiguous, coalesced)
 //       into per-frame value/mask buckets in shared memory, then every lane
@@ -40,72 +41,106 @@ __device__ __forceinline__ void st_v4(char* p, uint4 v) {
 
 }  // namespace
 
-// ----------------------------------------------------------- K2c scatter --
-// Block = one pixel group; walks the chunks in order.  Per chunk: the value at
-// the chunk start (tblv) and every run start inside the chunk as a change at
-// its (sub-tile) slot; slots come from the exclusive scan of the histogram the
-// segment kernel counted (same bins, same order of runs).
-template <typename OUT>
-__global__ void __launch_bounds__(32 * Geo<OUT>::P) k_fin_scatter(FinArgs a) {
-    constexpr int GP = 32 * Geo<OUT>::P;
-    __shared__ uint32_t cursor[kBins];
-    const int g = blockIdx.x;
-    const int t = threadIdx.x;
-    const int64_t p = (int64_t)g * GP + t;
-    const bool valid = p < a.npix;
-    const uint32_t cnt = valid ? a.counts[p] : 0u;
-    const bool over = cnt > (uint32_t)a.cap;  // k_fixup rewrites it: values are don't-care
-    const int n = (int)min(cnt, (uint32_t)a.cap);
-    const spk_run_t* rp = a.runs + (valid ? p * a.cap : 0);
-    const int lastp = valid ? a.last[p] : 0;
-    Change<OUT>* st = reinterpret_cast<Change<OUT>*>(a.stream);
-    OUT* tb = reinterpret_cast<OUT*>(a.tblv);
+// --------------------------------------------------- K2b histogram / K2c --
+// Both passes: block = one pixel group (GP pixels) x one window of
+// kFinWindow chunks; warp = one pixel at a time, reading its run list 32 runs
+// per load (lane k <- run b+k, coalesced).  The per-window counters live in
+// shared memory, so no global atomics.
 
-    int k = 0;
-    OUT cur = OUT(0);  // value of the run covering the current frame (0 = lead)
-    for (int c = 0; c < a.nchunks; ++c) {
-        const int64_t b0 = ((int64_t)c * a.ngroups + g) * kBins;
-        if (t < kBins) cursor[t] = a.offs[b0 + t];
-        __syncthreads();
-        const int c0 = c << kChunkLog2;
-        const int cend = min(a.frames, c0 + kChunk);
-        if (valid) tb[(int64_t)c * a.npix + p] = cur;
-        while (k < n) {
-            // runs k..k+3 and the start of k+4 (a run's value needs the next start)
-            spk_run_t r[5];
-#pragma unroll
-            for (int j = 0; j < 5; ++j)
-                r[j] = k + j < n ? rp[k + j]
-                                 : spk_run_t{k + j == n ? (uint32_t)lastp : 0x7fffffffu, 0u};
-            bool more = true;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (more && k < n && (int)r[j].start < cend) {
-                    const uint32_t fo = r[j].start - (uint32_t)c0;
-                    const uint32_t pos = atomicAdd(&cursor[fo / kSub], 1u);
-                    const OUT val = over ? OUT(0)
-                                         : OutVal<OUT>::run(r[j].intervals, r[j + 1].start - r[j].start);
-                    Change<OUT> ch;
-                    if constexpr (sizeof(OUT) == 1) {
-                        ch.w = fo << 17 | (uint32_t)t << 8 | (uint32_t)val;
-                    } else if constexpr (sizeof(OUT) == 4) {
-                        ch.key = fo << 16 | (uint32_t)t;
-                        ch.bits = __float_as_uint(val);
-                    } else {
-                        ch.key = fo << 16 | (uint32_t)t;
-                        ch.pad = 0;
-                        ch.v = val;
-                    }
-                    st[pos] = ch;
-                    cur = val;
-                    ++k;
-                } else {
-                    more = false;
-                }
+// K2b: run starts per (chunk, group, sub-tile)
+template <int GP>
+__global__ void __launch_bounds__(kFinWarps * 32) k_fin_bins(FinArgs a) {
+    __shared__ uint32_t hist[kFinWindow * kBins];
+    const int g = blockIdx.x;
+    const int cw0 = blockIdx.y * kFinWindow;
+    const int cw1 = min(a.nchunks, cw0 + kFinWindow);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kFinWindow * kBins; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int pl = warp; pl < GP; pl += kFinWarps) {
+        const int64_t p = (int64_t)g * GP + pl;
+        if (p >= a.npix) break;
+        const int n = (int)min(a.counts[p], (uint32_t)a.cap);
+        const spk_run_t* rp = a.runs + p * a.cap;
+        for (int b = 0; b < n; b += 32) {
+            const int k = b + lane;
+            if (k < n) {
+                const int st = (int)rp[k].start;
+                const int c = st >> kChunkLog2;
+                if (c >= cw0 && c < cw1)
+                    atomicAdd(&hist[(c - cw0) * kBins + ((st & (kChunk - 1)) / kSub)], 1u);
             }
-            if (!more) break;
         }
-        __syncthreads();
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < (cw1 - cw0) * kBins; i += blockDim.x) {
+        const int c = cw0 + i / kBins;
+        a.bins[((int64_t)c * a.ngroups + g) * kBins + (i % kBins)] = hist[i];
+    }
+}
+
+template __global__ void k_fin_bins<512>(FinArgs);
+template __global__ void k_fin_bins<256>(FinArgs);
+
+// K2c: the change stream and the value at every chunk start.  Run k's value
+// needs run k+1's start (or the last spike): it comes from the next lane.
+template <typename OUT>
+__global__ void __launch_bounds__(kFinWarps * 32) k_fin_scatter(FinArgs a) {
+    constexpr int GP = 32 * Geo<OUT>::P;
+    __shared__ uint32_t cursor[kFinWindow * kBins];
+    const int g = blockIdx.x;
+    const int cw0 = blockIdx.y * kFinWindow;
+    const int cw1 = min(a.nchunks, cw0 + kFinWindow);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < (cw1 - cw0) * kBins; i += blockDim.x)
+        cursor[i] = a.offs[((int64_t)(cw0 + i / kBins) * a.ngroups + g) * kBins + (i % kBins)];
+    __syncthreads();
+    Change<OUT>* stp = reinterpret_cast<Change<OUT>*>(a.stream);
+    OUT* tb = reinterpret_cast<OUT*>(a.tblv);
+    const int64_t f0w = (int64_t)cw0 << kChunkLog2, f1w = (int64_t)cw1 << kChunkLog2;
+    for (int pl = warp; pl < GP; pl += kFinWarps) {
+        const int64_t p = (int64_t)g * GP + pl;
+        if (p >= a.npix) break;
+        const uint32_t cnt = a.counts[p];
+        const bool over = cnt > (uint32_t)a.cap;  // k_fixup rewrites it: values don't matter
+        const int n = (int)min(cnt, (uint32_t)a.cap);
+        const spk_run_t* rp = a.runs + p * a.cap;
+        const int lastp = a.last[p];
+        for (int b = 0; b < n; b += 32) {
+            const int k = b + lane;
+            const spk_run_t r = k < n ? rp[k] : spk_run_t{0x7fffffffu, 0u};
+            const uint32_t nb = b + 32 < n ? rp[b + 32].start : (uint32_t)lastp;
+            uint32_t ns = __shfl_down_sync(kFull, r.start, 1);
+            if (lane == 31 || k + 1 >= n) ns = k + 1 < n ? ns : (uint32_t)lastp;
+            if (lane == 31 && k + 1 < n) ns = nb;
+            if (k >= n) continue;
+            const OUT val = over ? OUT(0) : OutVal<OUT>::run(r.intervals, ns - r.start);
+            const int st = (int)r.start;
+            // change at the run start
+            if (st >= f0w && st < f1w) {
+                const int c = st >> kChunkLog2;
+                const uint32_t fo = (uint32_t)(st - (c << kChunkLog2));
+                const uint32_t pos = atomicAdd(&cursor[(c - cw0) * kBins + fo / kSub], 1u);
+                Change<OUT> ch;
+                if constexpr (sizeof(OUT) == 1) {
+                    ch.w = fo << 17 | (uint32_t)pl << 8 | (uint32_t)val;
+                } else if constexpr (sizeof(OUT) == 4) {
+                    ch.key = fo << 16 | (uint32_t)pl;
+                    ch.bits = __float_as_uint(val);
+                } else {
+                    ch.key = fo << 16 | (uint32_t)pl;
+                    ch.pad = 0;
+                    ch.v = val;
+                }
+                stp[pos] = ch;
+            }
+            // chunk starts covered by this run: [start, next start), the last
+            // run also covers the tail
+            const int64_t hi = k + 1 < n ? (int64_t)ns : ((int64_t)a.nchunks << kChunkLog2);
+            int64_t cb = max(((int64_t)st + kChunk - 1) >> kChunkLog2, (int64_t)cw0);
+            const int64_t ce = min((hi - 1) >> kChunkLog2, (int64_t)cw1 - 1);
+            for (; cb <= ce; ++cb) tb[cb * a.npix + p] = val;
+        }
     }
 }
 

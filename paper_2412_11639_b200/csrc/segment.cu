@@ -31,15 +31,6 @@ __device__ __forceinline__ void st_run_if(bool pred, spk_run_t* addr, int rs, in
         : "memory");
 }
 
-// predicated histogram increment (no return value: RED)
-__device__ __forceinline__ void red_if(bool pred, uint32_t* addr) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
-        "@p red.global.add.u32 [%1], 1;\n\t}" ::"r"((uint32_t)pred),
-        "l"(addr)
-        : "memory");
-}
-
 }  // namespace
 
 template <int METHOD>
@@ -62,15 +53,9 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     Scan<METHOD> sc;
     sc.init();
     int nrun = 0;
-    // bins[(c * ngroups + g) * kBins + sub] for a run starting at frame rs
-    uint32_t* const binp = a.bins ? a.bins + (valid ? (p >> a.gshift) : 0) * kBins : nullptr;
-    const int64_t bin_row = (int64_t)a.ngroups * kBins;
-    // runs beyond the capacity are counted (overflow -> k_fixup) but neither
-    // stored nor binned, so the stored runs and the histogram always agree
+    // runs beyond the capacity are counted (overflow -> k_fixup) but not stored
     auto emit = [&](bool e, int rs, int cnt) {
-        const bool keep = e & (nrun <= capm1);
-        st_run_if(keep, rp + min(nrun, capm1), rs, cnt);
-        if (binp) red_if(keep, binp + (rs >> kChunkLog2) * bin_row + ((rs & (kChunk - 1)) / kSub));
+        st_run_if(e & (nrun <= capm1), rp + min(nrun, capm1), rs, cnt);
         nrun += (int)e;
     };
 

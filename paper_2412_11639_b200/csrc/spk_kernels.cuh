@@ -25,11 +25,6 @@ struct SegArgs {
     spk_run_t* runs;
     uint32_t* counts;
     int32_t* last;
-    // optional (nullptr = off): per (chunk, pixel group, sub-tile) run-start
-    // histogram for the expand stage, counted as runs are emitted
-    uint32_t* bins;
-    int ngroups;
-    int gshift;  // log2 of the pixel-group size
 };
 
 // Geometry of the expand stage per output type: a warp owns a group of
@@ -83,10 +78,13 @@ struct FinArgs {
     int cap;
     int nchunks;
     int ngroups;
-    void* tblv;            // [nchunks][npix] OUT: value at frame c*kChunk
-    const uint32_t* offs;  // exclusive prefix of the K2 run-start histogram
-    void* stream;      // Change<OUT>[total]
+    uint32_t* bins;        // [nchunks][ngroups][kBins] run starts per sub-tile (K2b)
+    void* tblv;            // [nchunks][npix] OUT: value at frame c*kChunk (K2c)
+    const uint32_t* offs;  // exclusive prefix of bins
+    void* stream;          // Change<OUT>[total] (K2c)
 };
+constexpr int kFinWarps = 16;     // K2b/K2c: warps per block (block = one pixel group)
+constexpr int kFinWindow = 128;   // chunks per shared-memory window (32 KB of counters)
 
 struct ExpArgs {
     const void* tblv;
@@ -118,6 +116,8 @@ template <int METHOD>
 __global__ void k_segment(SegArgs a);
 template <int METHOD, typename OUT>
 __global__ void k_fixup(SegArgs a, OUT* out, size_t out_pitch);
+template <int GP>
+__global__ void k_fin_bins(FinArgs a);
 template <typename OUT>
 __global__ void k_fin_scatter(FinArgs a);
 template <typename OUT>

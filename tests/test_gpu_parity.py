@@ -232,8 +232,8 @@ def test_launch_count_and_determinism():
     v = spk.synth("static", 1, 400, 250, 2000)
     capi.lib().spk_launch_count(1)
     a = run(v, "fsr")
-    # segment, scan x3, fin_scatter, expand, fixup (one pixel part)
-    assert capi.lib().spk_launch_count(1) == 7
+    # segment, fin_bins, scan x3, fin_scatter, expand, fixup (one pixel part)
+    assert capi.lib().spk_launch_count(1) == 8
     b = run(v, "fsr")
     assert torch.equal(a, b)
     capi.lib().spk_launch_count(1)
