@@ -62,12 +62,18 @@ __global__ void __launch_bounds__(kFinWarps * 32) k_fin_bins(FinArgs a) {
         if (p >= a.npix) break;
         const int n = (int)min(a.counts[p], (uint32_t)a.cap);
         const spk_run_t* rp = a.runs + p * a.cap;
-        for (int b = 0; b < n; b += 32) {
-            const int k = b + lane;
-            if (k < n) {
-                const int st = (int)rp[k].start;
+        for (int b = 0; b < n; b += 128) {
+            uint32_t sv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = b + 32 * u + lane;
+                sv[u] = k < n ? rp[k].start : 0xffffffffu;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int st = (int)sv[u];
                 const int c = st >> kChunkLog2;
-                if (c >= cw0 && c < cw1)
+                if (sv[u] != 0xffffffffu && c >= cw0 && c < cw1)
                     atomicAdd(&hist[(c - cw0) * kBins + ((st & (kChunk - 1)) / kSub)], 1u);
             }
         }
@@ -82,65 +88,71 @@ __global__ void __launch_bounds__(kFinWarps * 32) k_fin_bins(FinArgs a) {
 template __global__ void k_fin_bins<512>(FinArgs);
 template __global__ void k_fin_bins<256>(FinArgs);
 
-// K2c: the change stream and the value at every chunk start.  Run k's value
-// needs run k+1's start (or the last spike): it comes from the next lane.
+// K2c: the change stream and the value at every chunk start.  Thread = one
+// pixel, block = one pixel group walking the chunks in order, so the stream
+// slots of a chunk are all written while that chunk is processed (the 4-B
+// stores of a bin meet in L2).  Runs are read 8 at a time (run k's value needs
+// run k+1's start, or the last spike for the final run).
 template <typename OUT>
-__global__ void __launch_bounds__(kFinWarps * 32) k_fin_scatter(FinArgs a) {
+__global__ void __launch_bounds__(32 * Geo<OUT>::P) k_fin_scatter(FinArgs a) {
     constexpr int GP = 32 * Geo<OUT>::P;
-    __shared__ uint32_t cursor[kFinWindow * kBins];
+    constexpr int B = 8;
+    __shared__ uint32_t cursor[kBins];
     const int g = blockIdx.x;
-    const int cw0 = blockIdx.y * kFinWindow;
-    const int cw1 = min(a.nchunks, cw0 + kFinWindow);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < (cw1 - cw0) * kBins; i += blockDim.x)
-        cursor[i] = a.offs[((int64_t)(cw0 + i / kBins) * a.ngroups + g) * kBins + (i % kBins)];
-    __syncthreads();
-    Change<OUT>* stp = reinterpret_cast<Change<OUT>*>(a.stream);
+    const int t = threadIdx.x;
+    const int64_t p = (int64_t)g * GP + t;
+    const bool valid = p < a.npix;
+    const uint32_t cnt = valid ? a.counts[p] : 0u;
+    const bool over = cnt > (uint32_t)a.cap;  // k_fixup rewrites it: values don't matter
+    const int n = (int)min(cnt, (uint32_t)a.cap);
+    const spk_run_t* rp = a.runs + (valid ? p * a.cap : 0);
+    const int lastp = valid ? a.last[p] : 0;
+    Change<OUT>* st = reinterpret_cast<Change<OUT>*>(a.stream);
     OUT* tb = reinterpret_cast<OUT*>(a.tblv);
-    const int64_t f0w = (int64_t)cw0 << kChunkLog2, f1w = (int64_t)cw1 << kChunkLog2;
-    for (int pl = warp; pl < GP; pl += kFinWarps) {
-        const int64_t p = (int64_t)g * GP + pl;
-        if (p >= a.npix) break;
-        const uint32_t cnt = a.counts[p];
-        const bool over = cnt > (uint32_t)a.cap;  // k_fixup rewrites it: values don't matter
-        const int n = (int)min(cnt, (uint32_t)a.cap);
-        const spk_run_t* rp = a.runs + p * a.cap;
-        const int lastp = a.last[p];
-        for (int b = 0; b < n; b += 32) {
-            const int k = b + lane;
-            const spk_run_t r = k < n ? rp[k] : spk_run_t{0x7fffffffu, 0u};
-            const uint32_t nb = b + 32 < n ? rp[b + 32].start : (uint32_t)lastp;
-            uint32_t ns = __shfl_down_sync(kFull, r.start, 1);
-            if (lane == 31 || k + 1 >= n) ns = k + 1 < n ? ns : (uint32_t)lastp;
-            if (lane == 31 && k + 1 < n) ns = nb;
-            if (k >= n) continue;
-            const OUT val = over ? OUT(0) : OutVal<OUT>::run(r.intervals, ns - r.start);
-            const int st = (int)r.start;
-            // change at the run start
-            if (st >= f0w && st < f1w) {
-                const int c = st >> kChunkLog2;
-                const uint32_t fo = (uint32_t)(st - (c << kChunkLog2));
-                const uint32_t pos = atomicAdd(&cursor[(c - cw0) * kBins + fo / kSub], 1u);
-                Change<OUT> ch;
-                if constexpr (sizeof(OUT) == 1) {
-                    ch.w = fo << 17 | (uint32_t)pl << 8 | (uint32_t)val;
-                } else if constexpr (sizeof(OUT) == 4) {
-                    ch.key = fo << 16 | (uint32_t)pl;
-                    ch.bits = __float_as_uint(val);
-                } else {
-                    ch.key = fo << 16 | (uint32_t)pl;
-                    ch.pad = 0;
-                    ch.v = val;
-                }
-                stp[pos] = ch;
+
+    int k = 0;
+    OUT cur = OUT(0);  // value of the run covering the chunk start (0 = lead)
+    spk_run_t r[B + 1];
+    int have = 0;      // runs k..k+have-1 are in r[0..have)
+    for (int c = 0; c < a.nchunks; ++c) {
+        const int64_t b0 = ((int64_t)c * a.ngroups + g) * kBins;
+        if (t < kBins) cursor[t] = a.offs[b0 + t];
+        __syncthreads();
+        const int c0 = c << kChunkLog2;
+        const int cend = min(a.frames, c0 + kChunk);
+        if (valid && !over) tb[(int64_t)c * a.npix + p] = cur;
+        for (;;) {
+            if (k >= n) break;
+            if (have <= 1) {  // refill the window: runs k..k+B (B+1 for the next start)
+#pragma unroll
+                for (int j = 0; j <= B; ++j)
+                    r[j] = k + j < n ? rp[k + j]
+                                     : spk_run_t{k + j == n ? (uint32_t)lastp : 0x7fffffffu, 0u};
+                have = B;
             }
-            // chunk starts covered by this run: [start, next start), the last
-            // run also covers the tail
-            const int64_t hi = k + 1 < n ? (int64_t)ns : ((int64_t)a.nchunks << kChunkLog2);
-            int64_t cb = max(((int64_t)st + kChunk - 1) >> kChunkLog2, (int64_t)cw0);
-            const int64_t ce = min((hi - 1) >> kChunkLog2, (int64_t)cw1 - 1);
-            for (; cb <= ce; ++cb) tb[cb * a.npix + p] = val;
+            if ((int)r[0].start >= cend) break;
+            const uint32_t fo = r[0].start - (uint32_t)c0;
+            const uint32_t pos = atomicAdd(&cursor[fo / kSub], 1u);
+            const OUT val = over ? OUT(0) : OutVal<OUT>::run(r[0].intervals, r[1].start - r[0].start);
+            Change<OUT> ch;
+            if constexpr (sizeof(OUT) == 1) {
+                ch.w = fo << 17 | (uint32_t)t << 8 | (uint32_t)val;
+            } else if constexpr (sizeof(OUT) == 4) {
+                ch.key = fo << 16 | (uint32_t)t;
+                ch.bits = __float_as_uint(val);
+            } else {
+                ch.key = fo << 16 | (uint32_t)t;
+                ch.pad = 0;
+                ch.v = val;
+            }
+            st[pos] = ch;
+            cur = val;
+            ++k;
+#pragma unroll
+            for (int j = 0; j < B; ++j) r[j] = r[j + 1];
+            --have;
         }
+        __syncthreads();
     }
 }
 

@@ -48,8 +48,12 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 // (proj/src/io.cpp:78-81 applied to proj/src/reconstruct.cpp:124).  The
 // exact rational is never within 1/(2*span) of a .5 boundary unless it is on
 // it, so the integer form below equals the double path for every N <= span.
+// Computed as floor of the double quotient: both operands are exact (< 2^53)
+// and a non-integer quotient is >= 1/(2 span) >= 2^-30 from the next integer,
+// far above the division's rounding error (<= 2^-45), so the floor is exact
+// -- and much cheaper than a 64-bit integer division.
 __host__ __device__ __forceinline__ uint32_t run_u8(uint32_t n, uint32_t span) {
-    return (uint32_t)((510ull * n + span) / (2ull * span));
+    return (uint32_t)floor((510.0 * (double)n + (double)span) / (2.0 * (double)span));
 }
 
 __host__ __device__ __forceinline__ double run_f64(uint32_t n, uint32_t span) {

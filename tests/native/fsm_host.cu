@@ -5,6 +5,7 @@
 #include <cstdint>
 
 #include "../../paper_2412_11639_b200/csrc/spk_fsm.cuh"
+#include "../../paper_2412_11639_b200/csrc/spk_common.cuh"
 
 namespace {
 struct Collect {
@@ -132,4 +133,9 @@ extern "C" long word_runs(const uint8_t* bits, long frames, int method, long* st
     }
     for (long k = 0; k < n && k < cap; ++k) end[k] = (k + 1 < n) ? start[k + 1] : last;
     return n;
+}
+
+// the u8 run-value rule as compiled for the kernels
+extern "C" void host_run_u8(const uint32_t* n, const uint32_t* span, uint32_t* out, long m) {
+    for (long i = 0; i < m; ++i) out[i] = spk::run_u8(n[i], span[i]);
 }

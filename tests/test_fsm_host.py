@@ -86,3 +86,29 @@ def test_fsm_golden_rows(fsm, golden_dir, kind):
             got = fsm[kind](bits, m)
             assert np.array_equal(got[0], s[keep]) and np.array_equal(got[1], e[keep]) \
                 and np.array_equal(got[2], n[keep]), (name, tag)
+
+
+def test_run_u8_exact_vs_integer_rule(fsm):
+    """The kernels' u8 run value == round-half-away(255 N / span) computed with
+    exact integers (SURVEY finding 6), over random and boundary (N, span)."""
+    h = C.CDLL(str(LIB))
+    h.host_run_u8.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_long]
+    rng = np.random.default_rng(9)
+    span = np.concatenate([rng.integers(1, 1 << 29, 200000), rng.integers(1, 2000, 200000),
+                           np.arange(1, 3000)]).astype(np.uint32)
+    n = (rng.random(span.size) * (span.astype(np.float64) + 1)).astype(np.uint64)
+    n = np.minimum(n, span).astype(np.uint32)
+    n[:1000] = span[:1000]          # N == span -> 255
+    n[1000:2000] = 1                # smallest
+    # exact half ties: 255 N / span = k + 1/2  <=>  510 N = (2k+1) span
+    k = rng.integers(0, 255, 1000).astype(np.uint64)
+    ts = (rng.integers(1, 1 << 20, 1000) * 510).astype(np.uint64)
+    span[2000:3000] = ts.astype(np.uint32)
+    n[2000:3000] = ((2 * k + 1) * ts // 510).astype(np.uint32)
+    out = np.zeros(span.size, np.uint32)
+    h.host_run_u8(n.ctypes.data, span.ctypes.data, out.ctypes.data, span.size)
+    want = (510 * n.astype(np.uint64) + span) // (2 * span.astype(np.uint64))
+    assert np.array_equal(out, want.astype(np.uint32))
+    # and equals quantize() of the reference double
+    v = 255.0 * n.astype(np.float64) / span.astype(np.float64)
+    assert np.array_equal(out, np.floor(np.clip(v, 0, 255) + 0.5).astype(np.uint32))
