@@ -219,7 +219,7 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     SPK_LAUNCHED("k_fin_bins");
     int rc = launch_scan(f.bins, static_cast<uint32_t*>(w.offs.p), w.nbins, s);
     if (rc) return rc;
-    k_fin_scatter<OUT><<<w.ngroups, GP, 0, s>>>(f);
+    k_fin_scatter<OUT><<<w.ngroups, kFinWarps * 32, 0, s>>>(f);
     SPK_LAUNCHED("k_fin_scatter");
     mark(1, s);
 
