@@ -49,7 +49,7 @@ __device__ __forceinline__ void st_v4(char* p, uint4 v) {
 
 // K2b: run starts per (chunk, group, sub-tile)
 template <int GP>
-__global__ void __launch_bounds__(kFinWarps * 32) k_fin_bins(FinArgs a) {
+__global__ void __launch_bounds__(kFinWarps * 32, 2) k_fin_bins(FinArgs a) {
     __shared__ uint32_t hist[kFinWindow * kBins];
     const int g = blockIdx.x;
     const int cw0 = blockIdx.y * kFinWindow;
@@ -92,14 +92,14 @@ template __global__ void k_fin_bins<256>(FinArgs);
 // pixel group; it walks the chunks in windows of kScatWin chunks so that the
 // stream slots written concurrently by all blocks stay within a few MB (the
 // 4-B stores of a bin meet in L2).  Inside a window a warp serves its pixels
-// 8 at a time: one coalesced load of 32 runs per pixel (lane k <- run kp+k),
+// 4 at a time: one coalesced load of 32 runs per pixel (lane k <- run kp+k),
 // lanes 0..30 emit their run if it starts in the window (run k's value needs
 // run k+1's start = the next lane's), then the pixel's cursor advances.
 constexpr int kScatWin = 8;
 template <typename OUT>
-__global__ void __launch_bounds__(kFinWarps * 32) k_fin_scatter(FinArgs a) {
+__global__ void __launch_bounds__(kFinWarps * 32, 2) k_fin_scatter(FinArgs a) {
     constexpr int GP = 32 * Geo<OUT>::P;
-    constexpr int PX = 8;  // pixels in flight per warp
+    constexpr int PX = 4;  // pixels in flight per warp
     __shared__ uint32_t cursor[kScatWin * kBins];
     __shared__ int kp_s[GP];
     __shared__ OUT cur_s[GP];
