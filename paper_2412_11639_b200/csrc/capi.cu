@@ -176,10 +176,10 @@ int launch_scan(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_t s) {
 // workspaces of the expand stage (allocated before K2, which fills `bins`)
 template <typename OUT>
 struct ExpandWork {
-    Scratch tblv, bins, offs, stream;
+    Scratch tblv, bins, offs, cursor, stream;
     int ngroups = 0;
     int64_t nbins = 0;
-    explicit ExpandWork(cudaStream_t s) : tblv(s), bins(s), offs(s), stream(s) {}
+    explicit ExpandWork(cudaStream_t s) : tblv(s), bins(s), offs(s), cursor(s), stream(s) {}
 };
 
 template <typename OUT>
@@ -190,6 +190,7 @@ int prepare_expand(SegArgs& sa, ExpandWork<OUT>& w, cudaStream_t s) {
     SPK_CK(w.tblv.alloc((size_t)sa.nchunks * sa.npix * sizeof(OUT)));
     SPK_CK(w.bins.alloc((size_t)w.nbins * sizeof(uint32_t)));
     SPK_CK(w.offs.alloc((size_t)w.nbins * sizeof(uint32_t)));
+    SPK_CK(w.cursor.alloc((size_t)w.nbins * sizeof(uint32_t)));
     SPK_CK(w.stream.alloc((size_t)sa.npix * sa.cap * sizeof(Change<OUT>)));
     // chunks before a pixel's first run keep value 0
     SPK_CK(cudaMemsetAsync(w.tblv.p, 0, (size_t)sa.nchunks * sa.npix * sizeof(OUT), s));
@@ -219,7 +220,10 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     SPK_LAUNCHED("k_fin_bins");
     int rc = launch_scan(f.bins, static_cast<uint32_t*>(w.offs.p), w.nbins, s);
     if (rc) return rc;
-    k_fin_scatter<OUT><<<w.ngroups, kFinWarps * 32, 0, s>>>(f);
+    SPK_CK(cudaMemcpyAsync(w.cursor.p, w.offs.p, (size_t)w.nbins * sizeof(uint32_t),
+                           cudaMemcpyDeviceToDevice, s));
+    f.cursor = static_cast<uint32_t*>(w.cursor.p);
+    k_fin_scatter<OUT><<<(unsigned)((sa.npix + 255) / 256), 256, 0, s>>>(f);
     SPK_LAUNCHED("k_fin_scatter");
     mark(1, s);
 

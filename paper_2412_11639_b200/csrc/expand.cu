@@ -88,125 +88,68 @@ __global__ void __launch_bounds__(kFinWarps * 32, 2) k_fin_bins(FinArgs a) {
 template __global__ void k_fin_bins<512>(FinArgs);
 template __global__ void k_fin_bins<256>(FinArgs);
 
-// K2c: the change stream and the value at every chunk start.  Block = one
-// pixel group; it walks the chunks in windows of kScatWin chunks so that the
-// stream slots written concurrently by all blocks stay within a few MB (the
-// 4-B stores of a bin meet in L2).  Inside a window a warp serves its pixels
-// 4 at a time: one coalesced load of 32 runs per pixel (lane k <- run kp+k),
-// lanes 0..30 emit their run if it starts in the window (run k's value needs
-// run k+1's start = the next lane's), then the pixel's cursor advances.
-constexpr int kScatWin = 8;
+// K2c: the change stream and the value at every chunk start.  Thread = one
+// pixel, free-running (no block synchronisation): runs are read 8 at a time
+// (run k's value needs run k+1's start, or the last spike for the final run),
+// their stream slots are claimed with 8 independent atomics on a copy of the
+// scanned histogram, then the 8 changes are stored -- one memory round trip
+// per 8 runs.
 template <typename OUT>
-__global__ void __launch_bounds__(kFinWarps * 32, 2) k_fin_scatter(FinArgs a) {
+__global__ void __launch_bounds__(256) k_fin_scatter(FinArgs a) {
     constexpr int GP = 32 * Geo<OUT>::P;
-    constexpr int PX = 4;  // pixels in flight per warp
-    __shared__ uint32_t cursor[kScatWin * kBins];
-    __shared__ int kp_s[GP];
-    __shared__ OUT cur_s[GP];
-    const int g = blockIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int B = 8;
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= a.npix) return;
+    const int g = (int)(p / GP);
+    const uint32_t pl = (uint32_t)(p % GP);
+    const uint32_t cnt = a.counts[p];
+    const bool over = cnt > (uint32_t)a.cap;  // k_fixup rewrites it: values don't matter
+    const int n = (int)min(cnt, (uint32_t)a.cap);
+    const spk_run_t* rp = a.runs + p * a.cap;
+    const uint32_t lastp = (uint32_t)a.last[p];
     Change<OUT>* stp = reinterpret_cast<Change<OUT>*>(a.stream);
     OUT* tb = reinterpret_cast<OUT*>(a.tblv);
-    for (int i = threadIdx.x; i < GP; i += blockDim.x) {
-        kp_s[i] = 0;
-        cur_s[i] = OUT(0);
-    }
-    for (int cw0 = 0; cw0 < a.nchunks; cw0 += kScatWin) {
-        const int cw1 = min(a.nchunks, cw0 + kScatWin);
-        const int wend = min(a.frames, cw1 << kChunkLog2);
-        for (int i = threadIdx.x; i < (cw1 - cw0) * kBins; i += blockDim.x)
-            cursor[i] = a.offs[((int64_t)(cw0 + i / kBins) * a.ngroups + g) * kBins + (i % kBins)];
-        __syncthreads();
-        for (int pb = warp * PX; pb < GP; pb += kFinWarps * PX) {
-            int n[PX], kp[PX], lastp[PX];
-            bool over[PX];
-            const spk_run_t* rp[PX];
+    const int64_t total_frames = (int64_t)a.nchunks << kChunkLog2;
+    for (int k0 = 0; k0 < n; k0 += B) {
+        spk_run_t r[B + 1];
 #pragma unroll
-            for (int j = 0; j < PX; ++j) {
-                const int64_t p = (int64_t)g * GP + pb + j;
-                const bool valid = p < a.npix;
-                const uint32_t cnt = valid ? a.counts[p] : 0u;
-                over[j] = cnt > (uint32_t)a.cap;
-                n[j] = (int)min(cnt, (uint32_t)a.cap);
-                kp[j] = kp_s[pb + j];
-                lastp[j] = valid ? a.last[p] : 0;
-                rp[j] = a.runs + (valid ? p * a.cap : 0);
+        for (int j = 0; j <= B; ++j)
+            r[j] = k0 + j < n ? rp[k0 + j] : spk_run_t{k0 + j == n ? lastp : 0x7fffffffu, 0u};
+        uint32_t pos[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            if (k0 + j < n) {
+                const int st = (int)r[j].start;
+                const int c = st >> kChunkLog2;
+                const int bi = (st & (kChunk - 1)) / kSub;
+                pos[j] = atomicAdd(&a.cursor[((int64_t)c * a.ngroups + g) * kBins + bi], 1u);
             }
-            // tblv of the window's chunk starts before each pixel's first run
-            // in the window: covered by the run in progress (cur_s)
-            if (lane < PX) {
-                const int64_t p = (int64_t)g * GP + pb + lane;
-                const int kpj = kp_s[pb + lane];
-                if (p < a.npix && kpj > 0) {
-                    const uint32_t cnt = a.counts[p];
-                    if (cnt <= (uint32_t)a.cap) {
-                        const int nst = kpj < (int)cnt ? (int)a.runs[p * a.cap + kpj].start : 0x7fffffff;
-                        const int ce = min(cw1 - 1, (int)(((int64_t)min(nst, wend) - 1) >> kChunkLog2));
-                        const OUT v = cur_s[pb + lane];
-                        for (int c = cw0; c <= ce; ++c) tb[(int64_t)c * a.npix + p] = v;
-                    }
-                }
-            }
-            bool more = true;
-            while (__any_sync(kFull, more)) {
-                spk_run_t r[PX];
-                uint32_t nxt[PX];
-#pragma unroll
-                for (int j = 0; j < PX; ++j) {
-                    const int k = kp[j] + lane;
-                    r[j] = k < n[j] ? rp[j][k] : spk_run_t{0x7fffffffu, 0u};
-                }
-#pragma unroll
-                for (int j = 0; j < PX; ++j) {
-                    nxt[j] = __shfl_down_sync(kFull, r[j].start, 1);
-                    if (kp[j] + lane + 1 == n[j]) nxt[j] = (uint32_t)lastp[j];
-                }
-                more = false;
-#pragma unroll
-                for (int j = 0; j < PX; ++j) {
-                    const int k = kp[j] + lane;
-                    const bool go = lane < 31 && k < n[j] && (int)r[j].start < wend;
-                    const uint32_t bal = __ballot_sync(kFull, go);
-                    const int done = __popc(bal);
-                    if (go) {
-                        const int64_t p = (int64_t)g * GP + pb + j;
-                        const int st = (int)r[j].start;
-                        const OUT val = over[j] ? OUT(0) : OutVal<OUT>::run(r[j].intervals, nxt[j] - r[j].start);
-                        const int c = st >> kChunkLog2;
-                        const uint32_t fo = (uint32_t)(st - (c << kChunkLog2));
-                        const uint32_t pos = atomicAdd(&cursor[(c - cw0) * kBins + fo / kSub], 1u);
-                        Change<OUT> ch;
-                        const uint32_t pix = (uint32_t)(pb + j);
-                        if constexpr (sizeof(OUT) == 1) {
-                            ch.w = fo << 17 | pix << 8 | (uint32_t)val;
-                        } else if constexpr (sizeof(OUT) == 4) {
-                            ch.key = fo << 16 | pix;
-                            ch.bits = __float_as_uint(val);
-                        } else {
-                            ch.key = fo << 16 | pix;
-                            ch.pad = 0;
-                            ch.v = val;
-                        }
-                        stp[pos] = ch;
-                        if (!over[j]) {
-                            // chunk starts in [st, next start) of this window; the
-                            // final run also covers the tail
-                            const int64_t hi = k + 1 < n[j] ? (int64_t)nxt[j] : ((int64_t)cw1 << kChunkLog2);
-                            const int cb = (st + kChunk - 1) >> kChunkLog2;
-                            const int ce = (int)min((hi - 1) >> kChunkLog2, (int64_t)cw1 - 1);
-                            for (int cc = cb; cc <= ce; ++cc) tb[(int64_t)cc * a.npix + p] = val;
-                        }
-                        if (lane == 31 - __clz(bal)) cur_s[pb + j] = val;  // last emitted
-                    }
-                    kp[j] += done;
-                    more |= done == 31;
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < PX; ++j)
-                if (lane == 0) kp_s[pb + j] = kp[j];
         }
-        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            if (k0 + j < n) {
+                const int st = (int)r[j].start;
+                const uint32_t fo = (uint32_t)(st & (kChunk - 1));
+                const OUT val = over ? OUT(0) : OutVal<OUT>::run(r[j].intervals, r[j + 1].start - r[j].start);
+                Change<OUT> ch;
+                if constexpr (sizeof(OUT) == 1) {
+                    ch.w = fo << 17 | pl << 8 | (uint32_t)val;
+                } else if constexpr (sizeof(OUT) == 4) {
+                    ch.key = fo << 16 | pl;
+                    ch.bits = __float_as_uint(val);
+                } else {
+                    ch.key = fo << 16 | pl;
+                    ch.pad = 0;
+                    ch.v = val;
+                }
+                stp[pos[j]] = ch;
+                if (!over) {  // chunk starts in [start, next start); the last run covers the tail
+                    const int64_t hi = k0 + j + 1 < n ? (int64_t)r[j + 1].start : total_frames;
+                    for (int64_t cc = ((int64_t)st + kChunk - 1) >> kChunkLog2; cc <= (hi - 1) >> kChunkLog2; ++cc)
+                        tb[cc * a.npix + p] = val;
+                }
+            }
+        }
     }
 }
 

@@ -81,6 +81,7 @@ struct FinArgs {
     uint32_t* bins;        // [nchunks][ngroups][kBins] run starts per sub-tile (K2b)
     void* tblv;            // [nchunks][npix] OUT: value at frame c*kChunk (K2c)
     const uint32_t* offs;  // exclusive prefix of bins
+    uint32_t* cursor;      // K2c: running copy of offs (claimed with atomics)
     void* stream;          // Change<OUT>[total] (K2c)
 };
 constexpr int kFinWarps = 16;     // K2b/K2c: warps per block (block = one pixel group)
