@@ -35,9 +35,12 @@ __device__ __forceinline__ void st_run_if(bool pred, spk_run_t* addr, int rs, in
 
 template <int METHOD>
 __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
+    // transposed words of each warp: ring of kRing 32-frame words per lane
+    __shared__ uint32_t ring[kSegThreads / 32][kRing][32];
     const int lane = threadIdx.x & 31;
     const int64_t word = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (word * 32 >= a.npix) return;  // warp-uniform
+    uint32_t(*rg)[32] = ring[threadIdx.x >> 5];
     const int64_t p = word * 32 + lane;
     const bool valid = p < a.npix;
     const int frames = a.frames;
@@ -59,42 +62,56 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         nrun += (int)e;
     };
 
+    // Producer (warp-uniform): kBatch groups per refill, loads one batch ahead.
     uint32_t nxt[kBatch];
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
         const int f = j * 32 + rev;
         nxt[j] = f < frames ? __ldg(reinterpret_cast<const uint32_t*>(col + (size_t)f * pitch)) : 0u;
     }
-    for (int g0 = 0; g0 < ngroups; g0 += kBatch) {
-        uint32_t cur[kBatch];
-#pragma unroll
-        for (int j = 0; j < kBatch; ++j) cur[j] = nxt[j];
-        if (g0 + kBatch < ngroups) {
-#pragma unroll
-            for (int j = 0; j < kBatch; ++j) {
-                const int f = (g0 + kBatch + j) * 32 + rev;
-                nxt[j] = f < frames
-                             ? __ldg(reinterpret_cast<const uint32_t*>(col + (size_t)f * pitch))
-                             : 0u;
-            }
-        }
+    int produced = 0;  // groups transposed into the ring
+    auto produce = [&]() {
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
-            if (g0 + j < ngroups) {
-                uint32_t w = transpose32(cur[j], lane);
-                if (!valid) w = 0;
-                const int base = (g0 + j) * 32;
-                if constexpr (METHOD == kFSR) {
-                    fsr_word(sc, w, base, emit);
-                } else {
-                    while (w) {
-                        const int c = __clz(w);
-                        w ^= 0x80000000u >> c;
-                        int rs, cnt;
-                        const bool e = sc.step(base + c, rs, cnt);
-                        emit(e, rs, cnt);
-                    }
-                }
+            const uint32_t w = transpose32(nxt[j], lane);
+            rg[(produced + j) & (kRing - 1)][lane] = valid ? w : 0u;
+        }
+        produced += kBatch;
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            const int f = (produced + j) * 32 + rev;
+            nxt[j] = f < frames ? __ldg(reinterpret_cast<const uint32_t*>(col + (size_t)f * pitch)) : 0u;
+        }
+        __syncwarp();
+    };
+
+    // Consumers: every lane walks its own pixel through the words at its own
+    // pace -- one event (or one word) per iteration -- so a lane with many
+    // breaks does not hold the others back word by word; the ring bounds how
+    // far lanes may drift apart.
+    FsrWord cw;
+    cw.S = 0;
+    int wi = -1;  // current word of this lane
+    for (;;) {
+        const bool need = cw.S == 0 && wi + 1 < ngroups;
+        const bool waiting = need && wi + 1 >= produced;
+        const int lowest = (int)__reduce_min_sync(kFull, (unsigned)(need ? wi + 1 : (cw.S ? wi : 0x7fffffff)));
+        if (__any_sync(kFull, waiting) && produced < ngroups && produced + kBatch <= lowest + kRing)
+            produce();
+        if (!__any_sync(kFull, cw.S != 0 || wi + 1 < ngroups)) break;
+        if (cw.S == 0 && wi + 1 < produced) {
+            ++wi;
+            cw.load(rg[wi & (kRing - 1)][lane], wi * 32);
+        }
+        if (cw.S) {
+            if constexpr (METHOD == kFSR) {
+                cw.iterate(sc, emit);
+            } else {
+                const int c = __clz(cw.S);
+                cw.S ^= 0x80000000u >> c;
+                int rs, cnt;
+                const bool e = sc.step(cw.base + c, rs, cnt);
+                emit(e, rs, cnt);
             }
         }
     }

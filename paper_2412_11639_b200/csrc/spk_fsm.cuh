@@ -338,17 +338,29 @@ SPK_HD uint32_t bit_shr_clamp(uint32_t x, uint32_t, uint32_t s) {
 // popc, last = latest accepted); the violating spike -- a pair completion or
 // a break -- goes through the exact per-spike automaton, then the bulk test
 // resumes with the updated pair.  A word costs one iteration per event
-// instead of one per spike.
-// `emit(pred, rs, cnt)` stores a closed run when pred is true.
-template <class SC, class EMIT>
-SPK_HD void fsr_word(SC& sc, uint32_t S, int base, EMIT&& emit) {
-    if (!S) return;
-    const uint32_t So = S;
-    const uint32_t R1 = So >> 1, R2 = R1 | (R1 >> 1), R4 = R2 | (R2 >> 2), R8 = R4 | (R4 >> 4),
-                   R16 = R8 | (R8 >> 8), R32 = R16 | (R16 >> 16);
-    const int f = bit_clz(So);
-    const uint32_t fb = 0x80000000u >> f;
-    while (S) {
+// instead of one per spike.  FsrWord holds one word; iterate() does one bulk
+// test plus at most one event, so a caller can interleave words freely.
+struct FsrWord {
+    uint32_t So, S;                      // spikes of the word / not yet consumed
+    uint32_t R1, R2, R4, R8, R16, R32;   // So smeared by 1..2^k frames
+    uint32_t fb;                         // the word's first spike
+    int f, base;                         // its offset, the word's first frame
+
+    SPK_HD void load(uint32_t w, int b) {
+        So = S = w;
+        base = b;
+        R1 = So >> 1;
+        R2 = R1 | (R1 >> 1);
+        R4 = R2 | (R2 >> 2);
+        R8 = R4 | (R4 >> 4);
+        R16 = R8 | (R8 >> 8);
+        R32 = R16 | (R16 >> 16);
+        f = bit_clz(So | 1u);
+        fb = So ? (0x80000000u >> f) : 0u;
+    }
+
+    template <class SC, class EMIT>
+    SPK_HD void iterate(SC& sc, EMIT&& emit) {
         // ---- bulk: violations among the remaining spikes (selects only)
         const int lo = sc.lo;
         const uint32_t hw = sc.hw;
@@ -373,7 +385,7 @@ SPK_HD void fsr_word(SC& sc, uint32_t S, int base, EMIT&& emit) {
         sc.cnt += bit_popc(A);
         sc.last = A ? base + 32 - bit_ffs(A) : sc.last;
         S &= ~A;
-        if (!S) break;
+        if (!S) return;
         // ---- the violating spike through the exact automaton
         const int c = bit_clz(S);
         S ^= 0x80000000u >> c;
@@ -381,6 +393,15 @@ SPK_HD void fsr_word(SC& sc, uint32_t S, int base, EMIT&& emit) {
         const bool e = sc.step(base + c, rs, cnt);
         emit(e, rs, cnt);
     }
+};
+
+// `emit(pred, rs, cnt)` stores a closed run when pred is true.
+template <class SC, class EMIT>
+SPK_HD void fsr_word(SC& sc, uint32_t S, int base, EMIT&& emit) {
+    if (!S) return;
+    FsrWord w;
+    w.load(S, base);
+    while (w.S) w.iterate(sc, emit);
 }
 
 }  // namespace spk

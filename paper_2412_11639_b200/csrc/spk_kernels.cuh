@@ -13,6 +13,7 @@ using spk_run_t = ::spk_run;
 
 constexpr int kSegThreads = 64;  // 2 warps: fine-grained blocks balance 148 SMs
 constexpr int kBatch = 8;        // 32-frame groups per prefetch batch
+constexpr int kRing = 64;        // transposed words buffered per lane (lane drift bound)
 constexpr int kCausalWarps = 2;  // warps per TFI/TFP block
 
 struct SegArgs {
