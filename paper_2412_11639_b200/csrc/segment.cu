@@ -85,8 +85,29 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         __syncwarp();
     };
 
-    // Consumers: every lane walks its own pixel through the words at its own
-    // pace -- one event (or one word) per iteration -- so a lane with many
+    if constexpr (METHOD == kSSR) {
+        // SSR: spike by spike, the warp in lockstep over words (the per-spike
+        // step is long enough that independent progress does not pay off)
+        for (int g0 = 0; g0 < ngroups; g0 += kBatch) {
+            produce();
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                if (g0 + j < ngroups) {
+                    uint32_t w = rg[(g0 + j) & (kRing - 1)][lane];
+                    const int base = (g0 + j) * 32;
+                    while (w) {
+                        const int c = __clz(w);
+                        w ^= 0x80000000u >> c;
+                        int rs, cnt;
+                        const bool e = sc.step(base + c, rs, cnt);
+                        emit(e, rs, cnt);
+                    }
+                }
+            }
+        }
+    } else {
+    // FSR consumers: every lane walks its own pixel through the words at its
+    // own pace -- one event (or one word) per iteration -- so a lane with many
     // breaks does not hold the others back word by word; the ring bounds how
     // far lanes may drift apart.
     FsrWord cw;
@@ -103,17 +124,8 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
             ++wi;
             cw.load(rg[wi & (kRing - 1)][lane], wi * 32);
         }
-        if (cw.S) {
-            if constexpr (METHOD == kFSR) {
-                cw.iterate(sc, emit);
-            } else {
-                const int c = __clz(cw.S);
-                cw.S ^= 0x80000000u >> c;
-                int rs, cnt;
-                const bool e = sc.step(cw.base + c, rs, cnt);
-                emit(e, rs, cnt);
-            }
-        }
+        if (cw.S) cw.iterate(sc, emit);
+    }
     }
     if (valid) {
         int rs, cnt;
