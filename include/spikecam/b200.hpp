@@ -1,0 +1,163 @@
+// spikecam/b200.hpp -- C++ drop-in for the reconstruction surface of the
+// reference library (namespace spikecam, proj/include/spikecam/{core,
+// reconstruct,io}.hpp), implemented over the sm_100a C-ABI
+// (include/spikecam_b200.h).  Same names, signatures, value semantics and
+// exception classes as the reference, so its callers
+// (proj/tools/spikecam_main.cpp:174,271, proj/src/metrics.cpp:71, the tests)
+// compile against this header unchanged.  Every reconstruction runs on the
+// GPU; there is no CPU code path for it.
+//
+// Not provided: PixelReconState (the reference's per-frame CPU streaming
+// helper), the simulator, stability oracles, metrics and the PNG writer --
+// outside the accelerated path.
+#pragma once
+
+#include <cstdint>
+#include <filesystem>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace spikecam {
+
+// ---------------------------------------------------------------- types ----
+// W x H x T binary volume, frame-major, one byte per bit (core.hpp:15-49).
+class SpikeVolume {
+public:
+    SpikeVolume(int width, int height, int frames);
+    int width() const { return width_; }
+    int height() const { return height_; }
+    int frames() const { return frames_; }
+    bool at(int x, int y, int n) const;
+    void set(int x, int y, int n, bool v);
+    std::span<const uint8_t> raw() const { return bits_; }
+    std::span<uint8_t> raw_mutable() { return bits_; }
+    bool operator==(const SpikeVolume&) const = default;
+
+private:
+    size_t index(int x, int y, int n) const;
+    int width_, height_, frames_;
+    std::vector<uint8_t> bits_;
+};
+
+// Integer sequence with firing value e1 and optional resting value e2 (core.hpp:54-69).
+struct SpikeLikeStream {
+    std::vector<int> values;
+    int firing_value = 1;
+    std::optional<int> resting_value;
+    SpikeLikeStream() = default;
+    SpikeLikeStream(std::vector<int> vals, int e1, std::optional<int> e2);
+    static SpikeLikeStream from_values(std::vector<int> vals);
+    size_t size() const { return values.size(); }
+    std::vector<long> firing_positions() const;
+};
+
+struct IntervalStream {
+    std::vector<int> intervals;
+    IntervalStream() = default;
+    explicit IntervalStream(std::vector<int> ivals);
+    size_t size() const { return intervals.size(); }
+    bool empty() const { return intervals.empty(); }
+};
+
+// Half-open frame span of one stable run (core.hpp:85-96); degenerate = no interval.
+struct Segment {
+    long start_frame = 0;
+    long end_frame = 0;
+    IntervalStream intervals;
+    double intensity = 0.0;
+    Segment() = default;
+    Segment(long start, long end, IntervalStream ivals, double inten);
+    bool degenerate() const { return intervals.empty(); }
+    long duration() const { return end_frame - start_frame; }
+};
+
+struct IntensityImage {
+    int width = 0;
+    int height = 0;
+    std::vector<double> values;  // row-major, [0, 255]
+    IntensityImage() = default;
+    IntensityImage(int w, int h, double fill = 0.0);
+    double at(int x, int y) const { return values[static_cast<size_t>(y) * width + x]; }
+    double& at(int x, int y) { return values[static_cast<size_t>(y) * width + x]; }
+};
+
+SpikeLikeStream pixel_stream(const SpikeVolume& volume, int x, int y);
+
+// ------------------------------------------------------- reconstruction ----
+enum class Method { fsr, ssr, tfi, tfp };
+
+struct ReconMethod {
+    Method kind = Method::fsr;
+    int tfp_window = 32;
+    static ReconMethod parse(const std::string& name, int window = 32);
+    std::string name() const;
+};
+
+struct SegmentEvent {
+    long duration = 0;
+    double intensity = 0.0;
+    bool operator==(const SegmentEvent&) const = default;
+};
+
+std::vector<Segment> segment_fsr(const SpikeLikeStream& stream);
+std::vector<Segment> segment_ssr(const SpikeLikeStream& stream);
+double segment_intensity(const Segment& segment);
+std::vector<SegmentEvent> fsr_events(const SpikeLikeStream& stream);
+std::vector<double> reconstruct_pixel(const SpikeLikeStream& stream, ReconMethod method);
+
+// `workers` is accepted for signature compatibility: one call = one GPU.
+std::vector<IntensityImage> reconstruct(const SpikeVolume& volume, ReconMethod method,
+                                        int workers = 0);
+void reconstruct(const SpikeVolume& volume, ReconMethod method, int workers,
+                 std::vector<IntensityImage>& out);
+std::vector<IntensityImage> reconstruct_serial(const SpikeVolume& volume, ReconMethod method);
+
+// uint8 frames straight from the GPU (the CLI's per-frame output, quantize()
+// of io.cpp:78-81 applied on the device): frames[n][y*W + x].
+std::vector<std::vector<uint8_t>> reconstruct_u8(const SpikeVolume& volume, ReconMethod method);
+
+// ------------------------------------------------------------------- io ----
+struct io_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline constexpr uint32_t kDefaultFps = 20000;
+inline constexpr int kDefaultRawWidth = 400;
+inline constexpr int kDefaultRawHeight = 250;
+
+void write_spk(const SpikeVolume& volume, uint32_t fps, const std::filesystem::path& path);
+std::pair<SpikeVolume, uint32_t> read_spk(const std::filesystem::path& path);
+SpikeVolume read_raw(const std::filesystem::path& path, int width = kDefaultRawWidth,
+                     int height = kDefaultRawHeight, bool msb_first = false);
+
+enum class ImageFormat { pgm, png };
+// PGM only (PNG needs libpng, absent from this build): png -> io_error.
+void write_image(const IntensityImage& image, const std::filesystem::path& path,
+                 ImageFormat format);
+// P5 PGM back into [0, 255] values (read_image, io.cpp:230-234, PGM branch).
+IntensityImage read_image(const std::filesystem::path& path);
+
+// ------------------------------------------------ packed fast path (new) ----
+// The SPK1 payload kept bit-packed: no byte-per-bit SpikeVolume in between.
+// read_spk_packed + reconstruct_u8 is the CLI loop (spikecam_main.cpp:52,174-179)
+// with the volume going file -> GPU -> uint8 frames.
+struct PackedSpikes {
+    int width = 0;
+    int height = 0;
+    uint32_t fps = kDefaultFps;
+    uint32_t frames = 0;
+    std::vector<uint8_t> payload;  // frames * ceil(W*H/8) bytes, LSB-first
+};
+
+PackedSpikes read_spk_packed(const std::filesystem::path& path);
+PackedSpikes pack(const SpikeVolume& volume, uint32_t fps = kDefaultFps);
+// frames * W*H bytes, frame-major, the reference's quantize() of each value.
+std::vector<uint8_t> reconstruct_u8(const PackedSpikes& spikes, ReconMethod method);
+// frames * W*H doubles, frame-major, bit-identical to reconstruct().
+std::vector<double> reconstruct_f64(const PackedSpikes& spikes, ReconMethod method);
+
+}  // namespace spikecam

@@ -109,6 +109,12 @@ int spk_upload_planes(const spk_geom* g, const void* h_payload, size_t src_pitch
 int spk_reconstruct_host(const spk_geom* g, const void* h_payload, int method, int tfp_window,
                          int out_type, void* h_out, size_t out_pitch);
 
+/* Host boundary of segment_fsr / segment_ssr (proj/src/reconstruct.cpp:198-211):
+ * dense SPK1 payload in, per-pixel run lists out (layout as spk_segment;
+ * h_runs holds W*H*run_cap entries).  Synchronous. */
+int spk_segment_host(const spk_geom* g, const void* h_payload, int method, spk_run* h_runs,
+                     int64_t run_cap, uint32_t* h_counts, int32_t* h_last);
+
 /* ---- configuration / diagnostics ------------------------------------------ */
 /* run-list capacity per pixel used by spk_reconstruct_*: 0 = automatic
  * (max(64, T/32)).  Pixels that overflow it are recomputed exactly by a

@@ -40,6 +40,7 @@ SIGNATURES = {
     "spk_unpack_planes": (C.c_int, [_G, _P, _P, _P]),
     "spk_upload_planes": (C.c_int, [_G, _P, C.c_size_t, C.c_int, _P, _P]),
     "spk_reconstruct_host": (C.c_int, [_G, _P, C.c_int, C.c_int, C.c_int, _P, C.c_size_t]),
+    "spk_segment_host": (C.c_int, [_G, _P, C.c_int, _P, C.c_int64, _P, _P]),
     "spk_set_run_capacity": (C.c_int, [C.c_int64]),
     "spk_plane_pitch": (C.c_size_t, [C.c_int32, C.c_int32]),
     "spk_launch_count": (C.c_int64, [C.c_int]),

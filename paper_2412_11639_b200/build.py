@@ -15,6 +15,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libspikecam_b200.so"
+CPP_LIB = PKG / "libspikecam_cpp.so"
+CXX = "/usr/bin/g++"  # the system compiler (the image's CC/CXX env may point elsewhere)
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -56,5 +58,37 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_cpp(force: bool = False, verbose: bool = False) -> Path:
+    """C++ drop-in (include/spikecam/b200.hpp) over the C-ABI: g++ only, linked
+    against libspikecam_b200.so with an $ORIGIN rpath (no CUDA runtime of its own)."""
+    lib = build_library(force=force, verbose=verbose)
+    srcs = sorted((PKG / "cpp").glob("*.cpp"))
+    deps = srcs + [ROOT / "include" / "spikecam" / "b200.hpp", ROOT / "include" / "spikecam_b200.h", lib]
+    if not force and not _stale(CPP_LIB, deps):
+        return CPP_LIB
+    tmp = CPP_LIB.with_suffix(".so.tmp")
+    cmd = [CXX, "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", f"-I{ROOT / 'include'}",
+           "-o", str(tmp), *map(str, srcs), f"-L{PKG}", "-lspikecam_b200", "-Wl,-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    tmp.replace(CPP_LIB)
+    return CPP_LIB
+
+
+def build_cpp_program(src: Path, out: Path, verbose: bool = False) -> Path:
+    """A C++ program against the drop-in (tests/native/*.cpp)."""
+    lib = build_cpp(verbose=verbose)
+    if not _stale(out, [src, lib, ROOT / "include" / "spikecam" / "b200.hpp"]):
+        return out
+    cmd = [CXX, "-std=c++20", "-O2", "-Wall", f"-I{ROOT / 'include'}", "-o", str(out), str(src),
+           f"-L{PKG}", "-lspikecam_cpp", "-lspikecam_b200", f"-Wl,-rpath,{PKG}"]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    return out
+
+
 if __name__ == "__main__":
     print(build_library(force=True, verbose=True))
+    print(build_cpp(force=True, verbose=True))

@@ -1,0 +1,439 @@
+// spikecam_b200.cpp -- the C++ drop-in (include/spikecam/b200.hpp) over the
+// C-ABI of libspikecam_b200.so.  Reconstruction and segmentation are single
+// calls into the GPU library (spk_reconstruct_host / spk_segment_host); what
+// runs here is only the reference's container handling around them: value
+// checks of core.cpp, SpikeVolume bytes <-> SPK1 bit packing (io.cpp:52-76),
+// file headers (io.cpp:185-223) and turning run lists back into Segment
+// objects.  A missing or failing GPU surfaces as std::runtime_error.
+#include "spikecam/b200.hpp"
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <iterator>
+#include <set>
+
+#include "spikecam_b200.h"
+
+namespace spikecam {
+
+namespace {
+
+[[noreturn]] void raise(int rc) {
+    const std::string msg = spk_last_error();
+    if (rc == SPK_EINVAL) throw std::invalid_argument(msg);
+    if (rc == SPK_ENOMEM) throw std::bad_alloc();
+    throw std::runtime_error("spikecam_b200: " + msg);
+}
+
+inline void ck(int rc) {
+    if (rc != SPK_OK) raise(rc);
+}
+
+size_t plane_bytes(int w, int h) { return (static_cast<size_t>(w) * h + 7) / 8; }
+
+// byte b -> eight 0/1 bytes, bit i of b into byte i (LSB-first)
+const std::array<uint64_t, 256>& spread_table(bool msb_first) {
+    static const auto make = [](bool msb) {
+        std::array<uint64_t, 256> t{};
+        for (int b = 0; b < 256; ++b)
+            for (int i = 0; i < 8; ++i)
+                if ((b >> (msb ? 7 - i : i)) & 1) t[b] |= uint64_t{1} << (8 * i);
+        return t;
+    };
+    static const std::array<uint64_t, 256> lsb = make(false), msb = make(true);
+    return msb_first ? msb : lsb;
+}
+
+// eight bytes (any nonzero = spike) -> one LSB-first byte
+inline uint8_t gather8(uint64_t v) {
+    constexpr uint64_t k7f = 0x7f7f7f7f7f7f7f7fULL, k80 = 0x8080808080808080ULL;
+    const uint64_t nz = (((v & k7f) + k7f) | v) & k80;  // high bit of each nonzero byte
+    return static_cast<uint8_t>(((nz >> 7) * 0x0102040810204080ULL) >> 56);
+}
+
+// one frame of SpikeVolume bytes -> SPK1 plane (pack_frame, io.cpp:52-64)
+void pack_plane(const uint8_t* src, size_t npix, uint8_t* dst) {
+    const size_t full = npix / 8;
+    for (size_t j = 0; j < full; ++j) {
+        uint64_t v;
+        std::memcpy(&v, src + 8 * j, 8);
+        dst[j] = gather8(v);
+    }
+    if (npix % 8) {
+        uint8_t b = 0;
+        for (size_t p = full * 8; p < npix; ++p) b |= static_cast<uint8_t>((src[p] != 0) << (p % 8));
+        dst[full] = b;
+    }
+}
+
+// SPK1 plane -> SpikeVolume bytes (unpack_frame, io.cpp:66-76)
+void unpack_plane(const uint8_t* src, size_t npix, bool msb_first, uint8_t* dst) {
+    const auto& t = spread_table(msb_first);
+    const size_t full = npix / 8;
+    for (size_t j = 0; j < full; ++j) std::memcpy(dst + 8 * j, &t[src[j]], 8);
+    for (size_t p = full * 8; p < npix; ++p) {
+        const int shift = msb_first ? 7 - static_cast<int>(p % 8) : static_cast<int>(p % 8);
+        dst[p] = (src[p / 8] >> shift) & 1;
+    }
+}
+
+std::vector<uint8_t> read_file(const std::filesystem::path& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw io_error("cannot open " + path.string());
+    std::vector<uint8_t> data((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    if (in.bad()) throw io_error("read failure on " + path.string());
+    return data;
+}
+
+void write_file(const std::filesystem::path& path, const uint8_t* data, size_t n) {
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) throw io_error("cannot create " + path.string());
+    out.write(reinterpret_cast<const char*>(data), static_cast<std::streamsize>(n));
+    if (!out) throw io_error("write failure on " + path.string());
+}
+
+inline uint32_t le32(const uint8_t* p) {
+    return uint32_t{p[0]} | uint32_t{p[1]} << 8 | uint32_t{p[2]} << 16 | uint32_t{p[3]} << 24;
+}
+inline void put_le(uint8_t* p, uint32_t v, int n) {
+    for (int i = 0; i < n; ++i) p[i] = static_cast<uint8_t>(v >> (8 * i));
+}
+
+spk_geom geom(int w, int h, long frames) { return spk_geom{w, h, frames, 0}; }
+
+// one pixel stream as a 1x1 SPK1 payload (bit n of byte n/8)
+std::vector<uint8_t> stream_payload(const SpikeLikeStream& s) {
+    std::vector<uint8_t> pay(s.size(), 0);
+    for (size_t n = 0; n < s.size(); ++n) pay[n] = s.values[n] == s.firing_value ? 1 : 0;
+    return pay;  // 1 pixel -> one byte per plane, bit 0
+}
+
+template <typename T>
+std::vector<T> recon_host(const PackedSpikes& sp, ReconMethod m, int out_type) {
+    const size_t npix = static_cast<size_t>(sp.width) * sp.height;
+    std::vector<T> out(npix * sp.frames);
+    const spk_geom g = geom(sp.width, sp.height, sp.frames);
+    if (sp.payload.size() != plane_bytes(sp.width, sp.height) * sp.frames)
+        throw std::invalid_argument("PackedSpikes: payload size does not match the geometry");
+    ck(spk_reconstruct_host(&g, sp.payload.data(), static_cast<int>(m.kind), m.tfp_window, out_type,
+                            out.data(), npix));
+    return out;
+}
+
+void check_method(ReconMethod m) {
+    if (m.kind == Method::tfp && m.tfp_window < 1)
+        throw std::invalid_argument("tfp window must be >= 1");
+}
+
+// Segments of one stream from its GPU run list (build_segments semantics,
+// reconstruct.cpp:106-130): degenerate lead [0, first spike) when the first
+// spike is not frame 0, one segment per run, a degenerate tail from the last
+// spike carrying the last run's value; no spike -> one segment [0, T).
+std::vector<Segment> segments_of(const SpikeLikeStream& stream, Method kind) {
+    std::vector<Segment> segs;
+    const long T = static_cast<long>(stream.size());
+    if (T == 0) return segs;
+    const std::vector<long> spikes = stream.firing_positions();
+    const std::vector<uint8_t> pay = stream_payload(stream);
+    const spk_geom g = geom(1, 1, T);
+    const int64_t cap = std::max<long>(1, static_cast<long>(spikes.size()));
+    std::vector<spk_run> runs(static_cast<size_t>(cap));
+    uint32_t count = 0;
+    int32_t last = -1;
+    ck(spk_segment_host(&g, pay.data(), kind == Method::fsr ? SPK_FSR : SPK_SSR, runs.data(), cap,
+                        &count, &last));
+    if (spikes.empty()) {
+        segs.emplace_back(0, T, IntervalStream{}, 0.0);
+        return segs;
+    }
+    if (last != spikes.back() || count > static_cast<uint32_t>(cap))
+        throw std::runtime_error("spikecam_b200: inconsistent run list from the device");
+    if (spikes.front() > 0) segs.emplace_back(0, spikes.front(), IntervalStream{}, 0.0);
+    double carry = 0.0;
+    size_t a = 0;  // spike index of the current run's first spike
+    for (uint32_t k = 0; k < count; ++k) {
+        const size_t b = a + runs[k].intervals;
+        if (runs[k].intervals == 0 || b >= spikes.size() || spikes[a] != runs[k].start)
+            throw std::runtime_error("spikecam_b200: inconsistent run list from the device");
+        std::vector<int> iv(b - a);
+        for (size_t i = a; i < b; ++i) iv[i - a] = static_cast<int>(spikes[i + 1] - spikes[i]);
+        carry = 255.0 * static_cast<double>(b - a) / static_cast<double>(spikes[b] - spikes[a]);
+        segs.emplace_back(spikes[a], spikes[b], IntervalStream(std::move(iv)), carry);
+        a = b;
+    }
+    if (a != spikes.size() - 1)
+        throw std::runtime_error("spikecam_b200: run list does not cover the stream");
+    segs.emplace_back(spikes.back(), T, IntervalStream{}, carry);
+    return segs;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- types ----
+SpikeVolume::SpikeVolume(int width, int height, int frames)
+    : width_(width), height_(height), frames_(frames) {
+    if (width < 1 || height < 1 || frames < 0)
+        throw std::invalid_argument("SpikeVolume: width/height must be >= 1, frames >= 0");
+    bits_.assign(static_cast<size_t>(width) * height * frames, 0);
+}
+
+size_t SpikeVolume::index(int x, int y, int n) const {
+    if (x < 0 || x >= width_ || y < 0 || y >= height_ || n < 0 || n >= frames_)
+        throw std::out_of_range("SpikeVolume: index (" + std::to_string(x) + ", " +
+                                std::to_string(y) + ", " + std::to_string(n) + ") out of bounds");
+    return (static_cast<size_t>(n) * height_ + y) * width_ + x;
+}
+
+bool SpikeVolume::at(int x, int y, int n) const { return bits_[index(x, y, n)] != 0; }
+void SpikeVolume::set(int x, int y, int n, bool v) { bits_[index(x, y, n)] = v ? 1 : 0; }
+
+SpikeLikeStream::SpikeLikeStream(std::vector<int> vals, int e1, std::optional<int> e2)
+    : values(std::move(vals)), firing_value(e1), resting_value(e2) {
+    if (e2 && *e2 == e1)
+        throw std::invalid_argument("SpikeLikeStream: firing and resting values must differ");
+    for (int v : values)
+        if (v != e1 && !(e2 && v == *e2))
+            throw std::invalid_argument("SpikeLikeStream: element " + std::to_string(v) +
+                                        " is neither the firing nor the resting value");
+}
+
+SpikeLikeStream SpikeLikeStream::from_values(std::vector<int> vals) {
+    const std::set<int> seen(vals.begin(), vals.end());
+    if (seen.size() > 2) throw std::invalid_argument("SpikeLikeStream: more than two distinct values");
+    if (seen.empty()) return SpikeLikeStream({}, 1, 0);
+    std::optional<int> rest;
+    if (seen.size() == 2) rest = *seen.begin();
+    return SpikeLikeStream(std::move(vals), *seen.rbegin(), rest);
+}
+
+std::vector<long> SpikeLikeStream::firing_positions() const {
+    std::vector<long> pos;
+    for (size_t i = 0; i < values.size(); ++i)
+        if (values[i] == firing_value) pos.push_back(static_cast<long>(i));
+    return pos;
+}
+
+IntervalStream::IntervalStream(std::vector<int> ivals) : intervals(std::move(ivals)) {
+    for (int t : intervals)
+        if (t < 1) throw std::invalid_argument("IntervalStream: intervals must be >= 1");
+}
+
+Segment::Segment(long start, long end, IntervalStream ivals, double inten)
+    : start_frame(start), end_frame(end), intervals(std::move(ivals)), intensity(inten) {
+    if (start >= end) throw std::invalid_argument("Segment: start_frame must precede end_frame");
+    if (!(inten >= 0.0 && inten <= 255.0))
+        throw std::invalid_argument("Segment: intensity out of [0, 255]");
+}
+
+IntensityImage::IntensityImage(int w, int h, double fill) : width(w), height(h) {
+    if (w < 1 || h < 1) throw std::invalid_argument("IntensityImage: empty dimensions");
+    values.assign(static_cast<size_t>(w) * h, fill);
+}
+
+SpikeLikeStream pixel_stream(const SpikeVolume& volume, int x, int y) {
+    if (x < 0 || x >= volume.width() || y < 0 || y >= volume.height())
+        throw std::out_of_range("pixel_stream: coordinates out of bounds");
+    std::vector<int> vals(static_cast<size_t>(volume.frames()));
+    for (int n = 0; n < volume.frames(); ++n) vals[n] = volume.at(x, y, n) ? 1 : 0;
+    return SpikeLikeStream(std::move(vals), 1, 0);
+}
+
+// ------------------------------------------------------- reconstruction ----
+ReconMethod ReconMethod::parse(const std::string& name, int window) {
+    if (name == "fsr") return {Method::fsr};
+    if (name == "ssr") return {Method::ssr};
+    if (name == "tfi") return {Method::tfi};
+    if (name == "tfp") {
+        if (window < 1) throw std::invalid_argument("tfp window must be >= 1");
+        return {Method::tfp, window};
+    }
+    throw std::invalid_argument("unknown reconstruction method: " + name);
+}
+
+std::string ReconMethod::name() const {
+    switch (kind) {
+        case Method::fsr: return "fsr";
+        case Method::ssr: return "ssr";
+        case Method::tfi: return "tfi";
+        case Method::tfp: return "tfp-" + std::to_string(tfp_window);
+    }
+    return "?";
+}
+
+std::vector<Segment> segment_fsr(const SpikeLikeStream& stream) {
+    return segments_of(stream, Method::fsr);
+}
+
+std::vector<Segment> segment_ssr(const SpikeLikeStream& stream) {
+    return segments_of(stream, Method::ssr);
+}
+
+double segment_intensity(const Segment& segment) {
+    if (segment.degenerate())
+        throw std::invalid_argument("segment_intensity: degenerate segment has no interval");
+    long sum = 0;
+    for (int t : segment.intervals.intervals) sum += t;
+    return 255.0 * static_cast<double>(segment.intervals.size()) / static_cast<double>(sum);
+}
+
+std::vector<SegmentEvent> fsr_events(const SpikeLikeStream& stream) {
+    std::vector<SegmentEvent> ev;
+    for (const Segment& s : segment_fsr(stream)) ev.push_back({s.duration(), s.intensity});
+    return ev;
+}
+
+std::vector<double> reconstruct_pixel(const SpikeLikeStream& stream, ReconMethod method) {
+    check_method(method);
+    PackedSpikes sp;
+    sp.width = sp.height = 1;
+    sp.frames = static_cast<uint32_t>(stream.size());
+    sp.payload = stream_payload(stream);
+    return recon_host<double>(sp, method, SPK_OUT_F64);
+}
+
+void reconstruct(const SpikeVolume& volume, ReconMethod method, int workers,
+                 std::vector<IntensityImage>& out) {
+    (void)workers;  // one GPU per call; the result does not depend on it
+    check_method(method);
+    const int W = volume.width(), H = volume.height();
+    const size_t T = static_cast<size_t>(volume.frames());
+    if (out.size() != T || (T > 0 && (out[0].width != W || out[0].height != H)))
+        out.assign(T, IntensityImage(W, H));  // reuse rule of reconstruct.cpp:452-455
+    if (T == 0) return;
+    const std::vector<double> frames = reconstruct_f64(pack(volume), method);
+    const size_t npix = static_cast<size_t>(W) * H;
+    for (size_t n = 0; n < T; ++n)
+        std::copy_n(frames.begin() + n * npix, npix, out[n].values.begin());
+}
+
+std::vector<IntensityImage> reconstruct(const SpikeVolume& volume, ReconMethod method, int workers) {
+    std::vector<IntensityImage> out;
+    reconstruct(volume, method, workers, out);
+    return out;
+}
+
+std::vector<IntensityImage> reconstruct_serial(const SpikeVolume& volume, ReconMethod method) {
+    return reconstruct(volume, method, 1);
+}
+
+std::vector<std::vector<uint8_t>> reconstruct_u8(const SpikeVolume& volume, ReconMethod method) {
+    const std::vector<uint8_t> flat = reconstruct_u8(pack(volume), method);
+    const size_t npix = static_cast<size_t>(volume.width()) * volume.height();
+    std::vector<std::vector<uint8_t>> frames(static_cast<size_t>(volume.frames()));
+    for (size_t n = 0; n < frames.size(); ++n)
+        frames[n].assign(flat.begin() + n * npix, flat.begin() + (n + 1) * npix);
+    return frames;
+}
+
+std::vector<uint8_t> reconstruct_u8(const PackedSpikes& spikes, ReconMethod method) {
+    check_method(method);
+    return recon_host<uint8_t>(spikes, method, SPK_OUT_U8);
+}
+
+std::vector<double> reconstruct_f64(const PackedSpikes& spikes, ReconMethod method) {
+    check_method(method);
+    return recon_host<double>(spikes, method, SPK_OUT_F64);
+}
+
+PackedSpikes pack(const SpikeVolume& volume, uint32_t fps) {
+    PackedSpikes sp;
+    sp.width = volume.width();
+    sp.height = volume.height();
+    sp.fps = fps;
+    sp.frames = static_cast<uint32_t>(volume.frames());
+    const size_t npix = static_cast<size_t>(sp.width) * sp.height, fb = plane_bytes(sp.width, sp.height);
+    sp.payload.assign(fb * sp.frames, 0);
+    const uint8_t* raw = volume.raw().data();
+    for (size_t n = 0; n < sp.frames; ++n) pack_plane(raw + n * npix, npix, sp.payload.data() + n * fb);
+    return sp;
+}
+
+// ------------------------------------------------------------------- io ----
+PackedSpikes read_spk_packed(const std::filesystem::path& path) {
+    std::vector<uint8_t> data = read_file(path);
+    if (data.size() < 16 || std::memcmp(data.data(), "SPK1", 4) != 0)
+        throw io_error("bad SPK1 magic in " + path.string());
+    PackedSpikes sp;
+    sp.width = data[4] | data[5] << 8;
+    sp.height = data[6] | data[7] << 8;
+    sp.fps = le32(data.data() + 8);
+    sp.frames = le32(data.data() + 12);
+    if (sp.width < 1 || sp.height < 1) throw io_error("empty geometry in " + path.string());
+    const size_t expect = 16 + plane_bytes(sp.width, sp.height) * sp.frames;
+    if (data.size() != expect)
+        throw io_error("SPK1 length mismatch in " + path.string() + ": expected " +
+                       std::to_string(expect) + " bytes, got " + std::to_string(data.size()));
+    sp.payload.assign(data.begin() + 16, data.end());
+    return sp;
+}
+
+std::pair<SpikeVolume, uint32_t> read_spk(const std::filesystem::path& path) {
+    const PackedSpikes sp = read_spk_packed(path);
+    SpikeVolume v(sp.width, sp.height, static_cast<int>(sp.frames));
+    const size_t npix = static_cast<size_t>(sp.width) * sp.height, fb = plane_bytes(sp.width, sp.height);
+    for (size_t n = 0; n < sp.frames; ++n)
+        unpack_plane(sp.payload.data() + n * fb, npix, false, v.raw_mutable().data() + n * npix);
+    return {std::move(v), sp.fps};
+}
+
+SpikeVolume read_raw(const std::filesystem::path& path, int width, int height, bool msb_first) {
+    const std::vector<uint8_t> data = read_file(path);
+    const size_t fb = plane_bytes(width, height);
+    if (data.size() % fb != 0)
+        throw io_error("raw file " + path.string() + " (" + std::to_string(data.size()) +
+                       " bytes) is not a multiple of the " + std::to_string(fb) +
+                       "-byte frame size for " + std::to_string(width) + "x" +
+                       std::to_string(height) + "; check --width/--height");
+    const int frames = static_cast<int>(data.size() / fb);
+    SpikeVolume v(width, height, frames);
+    const size_t npix = static_cast<size_t>(width) * height;
+    for (int n = 0; n < frames; ++n)
+        unpack_plane(data.data() + n * fb, npix, msb_first, v.raw_mutable().data() + n * npix);
+    return v;
+}
+
+void write_spk(const SpikeVolume& volume, uint32_t fps, const std::filesystem::path& path) {
+    const PackedSpikes sp = pack(volume, fps);
+    std::vector<uint8_t> data(16 + sp.payload.size());
+    std::memcpy(data.data(), "SPK1", 4);
+    put_le(data.data() + 4, static_cast<uint32_t>(sp.width), 2);
+    put_le(data.data() + 6, static_cast<uint32_t>(sp.height), 2);
+    put_le(data.data() + 8, fps, 4);
+    put_le(data.data() + 12, sp.frames, 4);
+    std::copy(sp.payload.begin(), sp.payload.end(), data.begin() + 16);
+    write_file(path, data.data(), data.size());
+}
+
+void write_image(const IntensityImage& image, const std::filesystem::path& path, ImageFormat format) {
+    if (format != ImageFormat::pgm)
+        throw io_error("png output is not built into spikecam_b200: " + path.string());
+    const std::string head =
+        "P5\n" + std::to_string(image.width) + " " + std::to_string(image.height) + "\n255\n";
+    std::vector<uint8_t> data(head.begin(), head.end());
+    data.reserve(head.size() + image.values.size());
+    for (double v : image.values)  // quantize(), io.cpp:78-81
+        data.push_back(static_cast<uint8_t>(std::round(std::clamp(v, 0.0, 255.0))));
+    write_file(path, data.data(), data.size());
+}
+
+IntensityImage read_image(const std::filesystem::path& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw io_error("cannot open " + path.string());
+    std::string magic;
+    int w = 0, h = 0, maxval = 0;
+    in >> magic >> w >> h >> maxval;
+    if (magic != "P5" || maxval != 255 || w < 1 || h < 1)
+        throw io_error("not an 8-bit P5 PGM: " + path.string());
+    in.get();
+    std::vector<uint8_t> px(static_cast<size_t>(w) * h);
+    in.read(reinterpret_cast<char*>(px.data()), static_cast<std::streamsize>(px.size()));
+    if (!in) throw io_error("truncated PGM payload: " + path.string());
+    IntensityImage img(w, h);
+    std::copy(px.begin(), px.end(), img.values.begin());
+    return img;
+}
+
+}  // namespace spikecam

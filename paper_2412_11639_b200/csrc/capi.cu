@@ -529,6 +529,53 @@ int spk_reconstruct_host(const spk_geom* g, const void* h_payload, int method, i
     return SPK_OK;
 }
 
+int spk_segment_host(const spk_geom* g, const void* h_payload, int method, spk_run* h_runs,
+                     int64_t run_cap, uint32_t* h_counts, int32_t* h_last) {
+    spk_geom dg = *g;
+    dg.plane_pitch = spk_plane_pitch(g->width, g->height);
+    int rc = check_geom(&dg, true);
+    if (rc) return rc;
+    if (method != SPK_FSR && method != SPK_SSR)
+        return fail(SPK_EINVAL, "spk_segment: method must be fsr or ssr");
+    if (run_cap < 1 || run_cap > INT_MAX) return fail(SPK_EINVAL, "spk_segment: bad run_cap");
+    const size_t npix = (size_t)npix_of(g);
+    if (!h_counts || !h_last || (g->frames > 0 && (!h_payload || !h_runs)))
+        return fail(SPK_EINVAL, "spk: null host buffer");
+    if (g->frames == 0) {
+        std::fill(h_counts, h_counts + npix, 0u);
+        std::fill(h_last, h_last + npix, -1);
+        return SPK_OK;
+    }
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    cudaStream_t s;
+    SPK_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    rc = [&]() -> int {
+        Scratch planes(s), runs(s), counts(s), last(s);
+        SPK_CK(planes.alloc(dg.plane_pitch * (size_t)g->frames));
+        SPK_CK(runs.alloc(npix * (size_t)run_cap * sizeof(spk_run)));
+        SPK_CK(counts.alloc(npix * sizeof(uint32_t)));
+        SPK_CK(last.alloc(npix * sizeof(int32_t)));
+        int r = spk_upload_planes(&dg, h_payload, plane_bytes(g), 0, planes.p, s);
+        if (r) return r;
+        r = spk_segment(&dg, planes.p, method, static_cast<spk_run*>(runs.p), run_cap,
+                        static_cast<uint32_t*>(counts.p), static_cast<int32_t*>(last.p), s);
+        if (r) return r;
+        SPK_CK(cudaMemcpyAsync(h_runs, runs.p, npix * (size_t)run_cap * sizeof(spk_run),
+                               cudaMemcpyDeviceToHost, s));
+        SPK_CK(cudaMemcpyAsync(h_counts, counts.p, npix * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, s));
+        SPK_CK(cudaMemcpyAsync(h_last, last.p, npix * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        return SPK_OK;
+    }();
+    cudaError_t se = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (rc) return rc;
+    if (se != cudaSuccess) return cuda_fail(se, "cudaStreamSynchronize");
+    return SPK_OK;
+}
+
 int spk_set_run_capacity(int64_t per_pixel) {
     if (per_pixel < 0 || per_pixel > INT_MAX) return fail(SPK_EINVAL, "spk: bad run capacity");
     g_run_cap.store(per_pixel);

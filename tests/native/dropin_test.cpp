@@ -1,0 +1,298 @@
+// dropin_test.cpp -- exercises the C++ drop-in (include/spikecam/b200.hpp) the
+// way the reference's own callers do.  Driven by tests/test_dropin.py:
+//
+//   dropin_test selftest             host-only checks (no GPU needed)
+//   dropin_test gpucheck             self-consistency of the GPU-backed API
+//   dropin_test rows IN OUT          per-stream API on the golden streams
+//   dropin_test vol IN.spk OUTDIR    volume API on a golden SPK1 file
+//
+// `rows` / `vol` only dump results; the Python side compares them with the
+// reference's golden outputs (tests/golden/).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <functional>
+#include <random>
+#include <string>
+
+#include "spikecam/b200.hpp"
+
+using namespace spikecam;
+namespace fs = std::filesystem;
+
+static int g_fail = 0;
+#define EXPECT(cond)                                                       \
+    do {                                                                   \
+        if (!(cond)) {                                                     \
+            std::fprintf(stderr, "%s:%d: EXPECT(%s) failed\n", __FILE__,   \
+                         __LINE__, #cond);                                 \
+            ++g_fail;                                                      \
+        }                                                                  \
+    } while (0)
+
+template <typename E>
+static bool throws(const std::function<void()>& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+static SpikeVolume random_volume(int w, int h, int t, double p, unsigned seed) {
+    SpikeVolume v(w, h, t);
+    std::mt19937 rng(seed);
+    std::bernoulli_distribution b(p);
+    for (auto& x : v.raw_mutable()) x = b(rng) ? 1 : 0;
+    return v;
+}
+
+// ------------------------------------------------------------ selftest ----
+static void selftest(const fs::path& dir) {
+    // core value rules (core.cpp:9-75)
+    EXPECT(throws<std::invalid_argument>([] { SpikeVolume(0, 3, 4); }));
+    EXPECT(throws<std::invalid_argument>([] { SpikeVolume(3, 3, -1); }));
+    SpikeVolume v(5, 3, 4);
+    EXPECT(v.raw().size() == 60u);
+    v.set(4, 2, 3, true);
+    EXPECT(v.at(4, 2, 3) && !v.at(3, 2, 3));
+    EXPECT(v.raw()[3 * 15 + 2 * 5 + 4] == 1);
+    EXPECT(throws<std::out_of_range>([&] { v.at(5, 0, 0); }));
+    EXPECT(throws<std::out_of_range>([&] { v.set(0, 0, 4, true); }));
+    EXPECT(throws<std::out_of_range>([&] { pixel_stream(v, 0, 3); }));
+    EXPECT(pixel_stream(v, 4, 2).firing_positions() == std::vector<long>{3});
+    EXPECT(throws<std::invalid_argument>([] { SpikeLikeStream({1, 0, 2}, 1, 0); }));
+    EXPECT(throws<std::invalid_argument>([] { SpikeLikeStream({1, 1}, 1, 1); }));
+    EXPECT(throws<std::invalid_argument>([] { SpikeLikeStream::from_values({1, 2, 3}); }));
+    auto s = SpikeLikeStream::from_values({5, -1, 5});
+    EXPECT(s.firing_value == 5 && s.resting_value == -1);
+    EXPECT((s.firing_positions() == std::vector<long>{0, 2}));
+    EXPECT(throws<std::invalid_argument>([] { IntervalStream({2, 0}); }));
+    EXPECT(throws<std::invalid_argument>([] { Segment(3, 3, {}, 1.0); }));
+    EXPECT(throws<std::invalid_argument>([] { Segment(0, 3, {}, 256.0); }));
+    EXPECT(throws<std::invalid_argument>([] { IntensityImage(0, 1); }));
+    EXPECT(throws<std::invalid_argument>([] { segment_intensity(Segment(0, 4, {}, 0.0)); }));
+    EXPECT(segment_intensity(Segment(0, 10, IntervalStream({3, 3, 4}), 0.0)) == 255.0 * 3 / 10);
+
+    // ReconMethod (reconstruct.cpp:177-196)
+    EXPECT(ReconMethod::parse("ssr").kind == Method::ssr);
+    EXPECT(ReconMethod::parse("tfp", 7).name() == "tfp-7");
+    EXPECT(ReconMethod::parse("fsr").name() == "fsr");
+    EXPECT(throws<std::invalid_argument>([] { ReconMethod::parse("tfp", 0); }));
+    EXPECT(throws<std::invalid_argument>([] { ReconMethod::parse("nope"); }));
+
+    // SPK1 round trip, odd pixel count (pad bits), and the header layout
+    const SpikeVolume a = random_volume(13, 7, 37, 0.3, 5);
+    write_spk(a, 1234, dir / "a.spk");
+    auto [b, fps] = read_spk(dir / "a.spk");
+    EXPECT(fps == 1234u && b == a);
+    EXPECT(fs::file_size(dir / "a.spk") == 16u + 12u * 37u);
+    const PackedSpikes pk = read_spk_packed(dir / "a.spk");
+    EXPECT(pk.width == 13 && pk.height == 7 && pk.frames == 37u && pk.payload == pack(a).payload);
+    {  // headerless dump, LSB and MSB bit order
+        std::ofstream o(dir / "a.raw", std::ios::binary);
+        o.write(reinterpret_cast<const char*>(pk.payload.data()), (std::streamsize)pk.payload.size());
+    }
+    EXPECT(read_raw(dir / "a.raw", 13, 7) == a);
+    const SpikeVolume m = read_raw(dir / "a.raw", 13, 7, true);
+    for (int n = 0; n < 37; ++n)
+        for (int p = 0; p < 91; ++p) {
+            const int q = (p & ~7) | (7 - (p & 7));  // bit reversed within its byte
+            if (q < 91) EXPECT(m.at(p % 13, p / 13, n) == a.at(q % 13, q / 13, n));
+        }
+    EXPECT(throws<io_error>([&] { read_raw(dir / "a.raw", 10, 10); }));
+    EXPECT(throws<io_error>([&] { read_spk(dir / "missing.spk"); }));
+    {
+        std::ofstream o(dir / "bad.spk", std::ios::binary);
+        o << "SPK2xxxxxxxxxxxx";
+    }
+    EXPECT(throws<io_error>([&] { read_spk(dir / "bad.spk"); }));
+    {  // truncated payload
+        auto bytes = std::vector<char>(16 + 5);
+        std::ifstream i(dir / "a.spk", std::ios::binary);
+        i.read(bytes.data(), (std::streamsize)bytes.size());
+        std::ofstream o(dir / "short.spk", std::ios::binary);
+        o.write(bytes.data(), (std::streamsize)bytes.size());
+    }
+    EXPECT(throws<io_error>([&] { read_spk(dir / "short.spk"); }));
+
+    // PGM: quantize() rounding (io.cpp:78-81) and read back
+    IntensityImage img(4, 2);
+    img.values = {0.0, 127.5, 127.49999, 254.5, 255.0, 0.5, -3.0, 300.0};
+    write_image(img, dir / "q.pgm", ImageFormat::pgm);
+    const IntensityImage r = read_image(dir / "q.pgm");
+    EXPECT(r.width == 4 && r.height == 2);
+    EXPECT((r.values == std::vector<double>{0, 128, 127, 255, 255, 1, 0, 255}));
+    EXPECT(throws<io_error>([&] { write_image(img, dir / "q.png", ImageFormat::png); }));
+}
+
+// ------------------------------------------------------------ gpucheck ----
+static bool same_bits(double x, double y) { return std::memcmp(&x, &y, sizeof x) == 0; }
+
+static void gpucheck() {
+    // worked example of the paper / reconstruct.hpp:30-35: intervals 3,3,4,3 | 7,6,7
+    std::vector<int> vals(40, 0);
+    for (int f : {0, 3, 6, 10, 13, 20, 26, 33}) vals[f] = 1;
+    const SpikeLikeStream ex(vals, 1, 0);
+    const auto segs = segment_fsr(ex);
+    EXPECT(segs.size() == 3u);
+    if (segs.size() == 3u) {
+        EXPECT(segs[0].start_frame == 0 && segs[0].end_frame == 13 && segs[0].intervals.size() == 4u);
+        EXPECT(segs[1].start_frame == 13 && segs[1].end_frame == 33 && segs[1].intervals.size() == 3u);
+        EXPECT((segs[1].intervals.intervals == std::vector<int>{7, 6, 7}));
+        EXPECT(segs[2].degenerate() && segs[2].end_frame == 40);
+        EXPECT(same_bits(segs[0].intensity, 255.0 * 4 / 13));
+        EXPECT(same_bits(segs[2].intensity, 255.0 * 3 / 20));
+        EXPECT(same_bits(segment_intensity(segs[1]), segs[1].intensity));
+    }
+    const auto ev = fsr_events(ex);
+    EXPECT(ev.size() == 3u && ev[0].duration == 13 && ev[1].duration == 20 && ev[2].duration == 7);
+    EXPECT(segment_fsr(SpikeLikeStream({}, 1, 0)).empty());
+    const auto silent = segment_fsr(SpikeLikeStream(std::vector<int>(9, 0), 1, 0));
+    EXPECT(silent.size() == 1u && silent[0].end_frame == 9 && silent[0].intensity == 0.0);
+    // firing value other than 1 (SpikeLikeStream e1/e2)
+    std::vector<int> alt(vals.size());
+    for (size_t i = 0; i < vals.size(); ++i) alt[i] = vals[i] ? 7 : -2;
+    const auto pix_alt = reconstruct_pixel(SpikeLikeStream(alt, 7, -2), ReconMethod::parse("fsr"));
+    EXPECT(pix_alt == reconstruct_pixel(ex, ReconMethod::parse("fsr")));
+
+    // volume API: identical for any worker count and buffer reuse
+    // (test_reconstruct.cpp:250-267 property), per-pixel form == volume column
+    const SpikeVolume vol = random_volume(11, 6, 300, 0.35, 9);
+    for (const char* name : {"fsr", "ssr", "tfi", "tfp"}) {
+        const ReconMethod m = ReconMethod::parse(name, 5);
+        const auto base = reconstruct_serial(vol, m);
+        EXPECT(base.size() == 300u && base[0].width == 11 && base[0].height == 6);
+        for (int w : {0, 1, 3, 64}) {
+            const auto o = reconstruct(vol, m, w);
+            bool eq = o.size() == base.size();
+            for (size_t n = 0; eq && n < o.size(); ++n)
+                eq = std::memcmp(o[n].values.data(), base[n].values.data(), 66 * sizeof(double)) == 0;
+            EXPECT(eq);
+        }
+        std::vector<IntensityImage> reuse(300, IntensityImage(11, 6, -1.0));
+        const double* keep = reuse[0].values.data();
+        reconstruct(vol, m, 2, reuse);
+        EXPECT(reuse[0].values.data() == keep);  // same geometry -> buffers reused
+        EXPECT(reuse[299].values == base[299].values);
+        for (int p : {0, 17, 65}) {
+            const auto col = reconstruct_pixel(pixel_stream(vol, p % 11, p / 11), m);
+            bool eq = col.size() == 300u;
+            for (int n = 0; eq && n < 300; ++n) eq = same_bits(col[n], base[n].at(p % 11, p / 11));
+            EXPECT(eq);
+        }
+        // uint8 frames == quantize(values)
+        const auto u8 = reconstruct_u8(vol, m);
+        bool eq = u8.size() == 300u;
+        for (size_t n = 0; eq && n < 300; ++n)
+            for (size_t i = 0; i < 66; ++i)
+                eq &= u8[n][i] == (uint8_t)std::round(std::clamp(base[n].values[i], 0.0, 255.0));
+        EXPECT(eq);
+    }
+    // SSR refines FSR: every SSR segment lies inside one FSR segment
+    for (int p = 0; p < 66; ++p) {
+        const auto st = pixel_stream(vol, p % 11, p / 11);
+        const auto f = segment_fsr(st), s = segment_ssr(st);
+        EXPECT(s.size() >= f.size());
+        size_t j = 0;
+        for (const auto& seg : s) {
+            while (j < f.size() && f[j].end_frame <= seg.start_frame) ++j;
+            EXPECT(j < f.size() && f[j].start_frame <= seg.start_frame && seg.end_frame <= f[j].end_frame);
+        }
+    }
+    // errors surface as the reference's exceptions
+    EXPECT(throws<std::invalid_argument>([&] { reconstruct(vol, ReconMethod{Method::tfp, 0}); }));
+    EXPECT(reconstruct(SpikeVolume(3, 2, 0), ReconMethod{}).empty());
+}
+
+// ---------------------------------------------------------------- rows ----
+template <typename T>
+static void put(std::ofstream& o, T v) {
+    o.write(reinterpret_cast<const char*>(&v), sizeof v);
+}
+
+static void rows(const fs::path& in, const fs::path& out) {
+    std::ifstream i(in, std::ios::binary);
+    std::ofstream o(out, std::ios::binary);
+    uint32_t ncase = 0;
+    i.read(reinterpret_cast<char*>(&ncase), 4);
+    for (uint32_t c = 0; c < ncase; ++c) {
+        uint32_t t = 0;
+        i.read(reinterpret_cast<char*>(&t), 4);
+        std::vector<uint8_t> b(t);
+        i.read(reinterpret_cast<char*>(b.data()), t);
+        const SpikeLikeStream st(std::vector<int>(b.begin(), b.end()), 1, 0);
+        for (auto* fn : {&segment_fsr, &segment_ssr}) {
+            const auto segs = (*fn)(st);
+            put<uint32_t>(o, (uint32_t)segs.size());
+            for (const auto& s : segs) {
+                put<int64_t>(o, s.start_frame);
+                put<int64_t>(o, s.end_frame);
+                put<int64_t>(o, (int64_t)s.intervals.size());
+                put<double>(o, s.intensity);
+            }
+        }
+        const std::pair<const char*, int> variants[] = {{"fsr", 32}, {"ssr", 32}, {"tfi", 32},
+                                                        {"tfp", 32}, {"tfp", 7},  {"tfp", 1}};
+        for (auto [name, win] : variants) {
+            const auto pix = reconstruct_pixel(st, ReconMethod::parse(name, win));
+            o.write(reinterpret_cast<const char*>(pix.data()), (std::streamsize)(pix.size() * 8));
+        }
+        const auto ev = fsr_events(st);
+        put<uint32_t>(o, (uint32_t)ev.size());
+        for (const auto& e : ev) {
+            put<int64_t>(o, e.duration);
+            put<double>(o, e.intensity);
+        }
+    }
+}
+
+// ----------------------------------------------------------------- vol ----
+static void vol(const fs::path& spk, const fs::path& dir) {
+    auto [v, fps] = read_spk(spk);
+    (void)fps;
+    const PackedSpikes pk = read_spk_packed(spk);
+    const std::pair<const char*, int> variants[] = {{"fsr", 32}, {"ssr", 32}, {"tfi", 32},
+                                                    {"tfp", 32}, {"tfp", 16}, {"tfp", 3}};
+    for (auto [name, win] : variants) {
+        const ReconMethod m = ReconMethod::parse(name, win);
+        const std::string tag = std::string(name) + (std::string(name) == "tfp" ? std::to_string(win) : "");
+        const auto imgs = reconstruct(v, m);  // SpikeVolume -> IntensityImage path
+        std::ofstream f(dir / (tag + ".f64"), std::ios::binary);
+        for (const auto& im : imgs)
+            f.write(reinterpret_cast<const char*>(im.values.data()), (std::streamsize)(im.values.size() * 8));
+        const auto u8 = reconstruct_u8(pk, m);  // packed file -> uint8 frames path
+        std::ofstream g(dir / (tag + ".u8"), std::ios::binary);
+        g.write(reinterpret_cast<const char*>(u8.data()), (std::streamsize)u8.size());
+        if (imgs.size() > 1)
+            write_image(imgs[imgs.size() / 2], dir / (tag + "_mid.pgm"), ImageFormat::pgm);
+    }
+}
+
+int main(int argc, char** argv) {
+    const std::string mode = argc > 1 ? argv[1] : "";
+    try {
+        if (mode == "selftest" && argc == 3) {
+            selftest(argv[2]);
+        } else if (mode == "gpucheck") {
+            gpucheck();
+        } else if (mode == "rows" && argc == 4) {
+            rows(argv[2], argv[3]);
+        } else if (mode == "vol" && argc == 4) {
+            vol(argv[2], argv[3]);
+        } else {
+            std::fprintf(stderr, "usage: dropin_test selftest DIR | gpucheck | rows IN OUT | vol SPK DIR\n");
+            return 2;
+        }
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "uncaught exception: %s\n", e.what());
+        return 1;
+    }
+    if (g_fail) std::fprintf(stderr, "%d check(s) failed\n", g_fail);
+    return g_fail ? 1 : 0;
+}
