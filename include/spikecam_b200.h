@@ -24,6 +24,9 @@
  *                          (proj/src/io.cpp:185-223) into the pitched device layout
  *   spk_reconstruct_host   the host-buffer boundary of reconstruct(): host SPK1
  *                          payload in, host frames out
+ *   spk_segment_host       segment_fsr / segment_ssr on a host payload
+ *   spk_records[_host]     --emit-records: segment_* -> encode_events -> write_spkr
+ *                          (proj/tools/spikecam_main.cpp:146-172) as one SPKR image
  *
  * Error behaviour mirrors the reference's exceptions: SPK_EINVAL where the
  * reference throws std::invalid_argument (bad method / window / geometry,
@@ -114,6 +117,24 @@ int spk_reconstruct_host(const spk_geom* g, const void* h_payload, int method, i
  * h_runs holds W*H*run_cap entries).  Synchronous. */
 int spk_segment_host(const spk_geom* g, const void* h_payload, int method, spk_run* h_runs,
                      int64_t run_cap, uint32_t* h_counts, int32_t* h_last);
+
+/* ---- segment records (SPKR) ------------------------------------------------ */
+/* The CLI's --emit-records output (proj/tools/spikecam_main.cpp:146-172):
+ * every pixel's FSR / SSR segments (lead, runs, tail) encoded as 16-bit
+ * words (duration << 8 | lround(intensity), durations > 255 split;
+ * proj/src/codec.cpp:8-19), laid out as the complete SPKR file image
+ * (proj/src/io.cpp:240-255: "SPKR", u16 W, u16 H, u32 fps, u32 frames, then
+ * per pixel a u32 word count and its words, little endian).
+ * spk_records allocates *d_image from the device pool (stream-ordered on
+ * `stream`; release with spk_free_device) and synchronises `stream` once to
+ * learn the size.  W, H <= 65535. */
+int spk_records(const spk_geom* g, const void* d_planes, int method, uint32_t fps, void** d_image,
+                uint64_t* image_bytes, void* stream);
+/* host payload in, malloc'd host image out (release with spk_free_host) */
+int spk_records_host(const spk_geom* g, const void* h_payload, int method, uint32_t fps,
+                     void** h_image, uint64_t* image_bytes);
+int spk_free_device(void* d_ptr, void* stream);
+void spk_free_host(void* h_ptr);
 
 /* ---- configuration / diagnostics ------------------------------------------ */
 /* run-list capacity per pixel used by spk_reconstruct_*: 0 = automatic

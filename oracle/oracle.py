@@ -116,6 +116,39 @@ class Oracle:
             raise ValueError("encode: bad duration/intensity")
         return w[:n]
 
+    def pixel_records(self, bits: np.ndarray, method: int) -> np.ndarray:
+        """encode_events of one pixel's segments (spikecam_main.cpp:146-172):
+        lead [0, s0) at 0, each run at 255*N/span, tail [s_last, T) carrying
+        the last run's value (build_segments, reconstruct.cpp:107-130)."""
+        bits = np.ascontiguousarray(bits, dtype=np.uint8)
+        t = bits.size
+        if t == 0:
+            return np.zeros(0, np.uint16)
+        spikes = np.flatnonzero(bits)
+        segs = []
+        if spikes.size == 0:
+            segs.append((t, 0.0))
+        else:
+            if spikes[0] > 0:
+                segs.append((int(spikes[0]), 0.0))
+            carry = 0.0
+            for a, b, n in zip(*self.runs(bits, method)):
+                carry = 255.0 * float(n) / float(b - a)
+                segs.append((int(b - a), carry))
+            segs.append((int(t - spikes[-1]), carry))
+        return np.concatenate([self.encode(d, v) for d, v in segs])
+
+    def records(self, planes: np.ndarray, w: int, h: int, t: int, pitch: int, method: int,
+                fps: int = 20000) -> bytes:
+        """SPKR file image (write_spkr, io.cpp:240-255) of a packed volume."""
+        bits = self.unpack(planes, w, h, t, pitch)
+        out = [b"SPKR", np.array([w, h], "<u2").tobytes(), np.array([fps, t], "<u4").tobytes()]
+        for p in range(w * h):
+            words = self.pixel_records(bits[:, p], method) if t else np.zeros(0, np.uint16)
+            out.append(np.array([words.size], "<u4").tobytes())
+            out.append(words.astype("<u2").tobytes())
+        return b"".join(out)
+
     # volumes (planes: [T, pitch] uint8, LSB-first)
     def reconstruct(self, planes: np.ndarray, w: int, h: int, t: int, pitch: int, method: int,
                     window: int = 32, dtype=np.uint8, pix_begin: int = 0,
@@ -174,6 +207,9 @@ class Reference:
         h.ref_write_pgm.argtypes = [_P, C.c_int, C.c_int, C.c_char_p]
         h.ref_encode_events.restype = _L
         h.ref_encode_events.argtypes = [_P, _P, _L, _P, _L]
+        h.ref_emit_records.restype = _L
+        h.ref_emit_records.argtypes = [_P, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_uint32, C.c_char_p]
         self.h = h
 
     def _err(self):
@@ -273,6 +309,12 @@ class Reference:
         if n < 0:
             raise ValueError(self._err())
         return words[:n]
+
+    def emit_records(self, planes, pitch, w, h, t, method, fps, path):
+        """The CLI's --emit-records output (SPKR file) for a packed volume."""
+        planes = np.ascontiguousarray(planes, dtype=np.uint8)
+        if self.h.ref_emit_records(_ptr(planes), pitch, w, h, t, method, fps, str(path).encode()) < 0:
+            raise ValueError(self._err())
 
 
 def ref_available() -> bool:

@@ -269,4 +269,34 @@ long ref_encode_events(const long* duration, const double* intensity, long nev,
     });
 }
 
+// The CLI's --emit-records loop (proj/tools/spikecam_main.cpp:146-172) on a
+// packed volume: per pixel fsr_events / segment_ssr -> encode_events, then
+// write_spkr to `path`.
+long ref_emit_records(const uint8_t* planes, size_t pitch, int w, int h, int t, int method,
+                      uint32_t fps, const char* path) {
+    return guarded([&]() -> long {
+        const SpikeVolume volume = volume_of(planes, pitch, w, h, t);
+        RecordVolume rv;
+        rv.width = w;
+        rv.height = h;
+        rv.fps = fps;
+        rv.frame_count = static_cast<uint32_t>(t);
+        rv.words.resize(static_cast<size_t>(w) * h);
+        for (int y = 0; y < h; ++y) {
+            for (int x = 0; x < w; ++x) {
+                const SpikeLikeStream stream = pixel_stream(volume, x, y);
+                std::vector<SegmentEvent> events;
+                if (method == 0) {
+                    events = fsr_events(stream);
+                } else {
+                    for (const Segment& sg : segment_ssr(stream)) events.push_back({sg.duration(), sg.intensity});
+                }
+                rv.pixel(x, y) = encode_events(events);
+            }
+        }
+        write_spkr(rv, path);
+        return 0;
+    });
+}
+
 }  // extern "C"

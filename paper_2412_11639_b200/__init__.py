@@ -22,6 +22,7 @@ from .recon import (  # noqa: F401
     synth,
     write_spk,
 )
+from .records import RecordVolume, decode, read_spkr, records, records_host, write_spkr  # noqa: F401
 from ._capi import LIB_PATH, SpikecamError  # noqa: F401
 
 __version__ = "0.1.0"

@@ -12,6 +12,7 @@
 #include <atomic>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "spk_common.cuh"
@@ -158,17 +159,18 @@ int launch_segment(int method, const SegArgs& a, cudaStream_t s) {
     return SPK_OK;
 }
 
-// exclusive scan of n uint32 counts (three small launches)
-int launch_scan(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_t s) {
+// exclusive scan of n uint32 counts into T (three small launches)
+template <typename T>
+int launch_scan(const uint32_t* in, T* out, int64_t n, cudaStream_t s) {
     const int64_t nb = (n + kScanBlock - 1) / kScanBlock;
     Scratch sums(s);
-    SPK_CK(sums.alloc((size_t)nb * sizeof(uint32_t)));
-    uint32_t* sp = static_cast<uint32_t*>(sums.p);
-    k_scan_blocks<<<(unsigned)nb, kScanBlock, 0, s>>>(in, out, sp, n);
+    SPK_CK(sums.alloc((size_t)nb * sizeof(T)));
+    T* sp = static_cast<T*>(sums.p);
+    k_scan_blocks<T><<<(unsigned)nb, kScanBlock, 0, s>>>(in, out, sp, n);
     SPK_LAUNCHED("k_scan_blocks");
-    k_scan_sums<<<1, kScanBlock, 0, s>>>(sp, nb);
+    k_scan_sums<T><<<1, kScanBlock, 0, s>>>(sp, nb);
     SPK_LAUNCHED("k_scan_sums");
-    k_scan_add<<<(unsigned)nb, kScanBlock, 0, s>>>(out, sp, n);
+    k_scan_add<T><<<(unsigned)nb, kScanBlock, 0, s>>>(out, sp, n);
     SPK_LAUNCHED("k_scan_add");
     return SPK_OK;
 }
@@ -575,6 +577,135 @@ int spk_segment_host(const spk_geom* g, const void* h_payload, int method, spk_r
     if (se != cudaSuccess) return cuda_fail(se, "cudaStreamSynchronize");
     return SPK_OK;
 }
+
+int spk_records(const spk_geom* g, const void* d_planes, int method, uint32_t fps, void** d_image,
+                uint64_t* image_bytes, void* stream) {
+    int rc = check_geom(g, true);
+    if (rc) return rc;
+    if (method != SPK_FSR && method != SPK_SSR)
+        return fail(SPK_EINVAL, "--emit-records needs method fsr or ssr");
+    if (g->width > 65535 || g->height > 65535)
+        return fail(SPK_EINVAL, "spk_records: SPKR geometry is 16-bit (W, H <= 65535)");
+    if (!d_image || !image_bytes || (g->frames > 0 && !d_planes))
+        return fail(SPK_EINVAL, "spk: null buffer");
+    *d_image = nullptr;
+    *image_bytes = 0;
+    const int64_t npix = npix_of(g);
+    cudaStream_t s = as_stream(stream);
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    const int cap = run_capacity(g->frames);
+    Scratch runs(s), counts(s), last(s), wc(s), offs(s);
+    SPK_CK(runs.alloc((size_t)npix * cap * sizeof(spk_run)));
+    SPK_CK(counts.alloc((size_t)npix * sizeof(uint32_t)));
+    SPK_CK(last.alloc((size_t)npix * sizeof(int32_t)));
+    SPK_CK(wc.alloc((size_t)npix * sizeof(uint32_t)));
+    SPK_CK(offs.alloc((size_t)npix * sizeof(unsigned long long)));
+    RecArgs r;
+    r.seg.planes = d_planes;
+    r.seg.pitch = g->plane_pitch;
+    r.seg.npix = npix;
+    r.seg.frames = (int)g->frames;
+    r.seg.cap = cap;
+    r.seg.nchunks = (int)((g->frames + kChunk - 1) / kChunk);
+    r.seg.runs = static_cast<spk_run*>(runs.p);
+    r.seg.counts = static_cast<uint32_t*>(counts.p);
+    r.seg.last = static_cast<int32_t*>(last.p);
+    r.wc = static_cast<uint32_t*>(wc.p);
+    r.offs = static_cast<unsigned long long*>(offs.p);
+    r.img = nullptr;
+    r.width = g->width;
+    r.height = g->height;
+    r.fps = fps;
+    if (g->frames > 0) {
+        if ((rc = launch_segment(method, r.seg, s))) return rc;
+    } else {
+        SPK_CK(cudaMemsetAsync(r.seg.counts, 0, (size_t)npix * sizeof(uint32_t), s));
+        SPK_CK(cudaMemsetAsync(r.seg.last, 0xff, (size_t)npix * sizeof(int32_t), s));
+    }
+    const unsigned blocks = (unsigned)((npix + 127) / 128);
+    if (method == SPK_FSR)
+        k_rec_count<kFSR><<<blocks, 128, 0, s>>>(r);
+    else
+        k_rec_count<kSSR><<<blocks, 128, 0, s>>>(r);
+    SPK_LAUNCHED("k_rec_count");
+    if ((rc = launch_scan(r.wc, static_cast<unsigned long long*>(offs.p), npix, s))) return rc;
+    // image size = header + per-pixel counts + all words (one small readback)
+    unsigned long long tail[2] = {0, 0};
+    uint32_t tail_wc = 0;
+    SPK_CK(cudaMemcpyAsync(&tail[0], r.offs + (npix - 1), sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, s));
+    SPK_CK(cudaMemcpyAsync(&tail_wc, r.wc + (npix - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    SPK_CK(cudaStreamSynchronize(s));
+    const uint64_t words = tail[0] + tail_wc;
+    const uint64_t bytes = 16 + 4 * (uint64_t)npix + 2 * words;
+    void* img = nullptr;
+    SPK_CK(cudaMallocAsync(&img, bytes, s));
+    r.img = static_cast<uint8_t*>(img);
+    if (method == SPK_FSR)
+        k_rec_write<kFSR><<<blocks, 128, 0, s>>>(r);
+    else
+        k_rec_write<kSSR><<<blocks, 128, 0, s>>>(r);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        cudaFreeAsync(img, s);
+        return cuda_fail(e, "k_rec_write");
+    }
+    *d_image = img;
+    *image_bytes = bytes;
+    return SPK_OK;
+}
+
+int spk_records_host(const spk_geom* g, const void* h_payload, int method, uint32_t fps,
+                     void** h_image, uint64_t* image_bytes) {
+    spk_geom dg = *g;
+    dg.plane_pitch = spk_plane_pitch(g->width, g->height);
+    int rc = check_geom(&dg, true);
+    if (rc) return rc;
+    if (!h_image || !image_bytes || (g->frames > 0 && !h_payload))
+        return fail(SPK_EINVAL, "spk: null host buffer");
+    *h_image = nullptr;
+    *image_bytes = 0;
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    cudaStream_t s;
+    SPK_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    void* host = nullptr;
+    rc = [&]() -> int {
+        Scratch planes(s), img(s);
+        SPK_CK(planes.alloc(dg.plane_pitch * (size_t)std::max<int64_t>(1, g->frames)));
+        int r = spk_upload_planes(&dg, h_payload, plane_bytes(g), 0, planes.p, s);
+        if (r) return r;
+        uint64_t bytes = 0;
+        r = spk_records(&dg, planes.p, method, fps, &img.p, &bytes, s);
+        if (r) return r;
+        host = std::malloc(bytes);
+        if (!host) return fail(SPK_ENOMEM, "spk_records_host: host allocation failed");
+        SPK_CK(cudaMemcpyAsync(host, img.p, bytes, cudaMemcpyDeviceToHost, s));
+        *image_bytes = bytes;
+        return SPK_OK;
+    }();
+    cudaError_t se = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (!rc && se != cudaSuccess) rc = cuda_fail(se, "cudaStreamSynchronize");
+    if (rc) {
+        std::free(host);
+        *image_bytes = 0;
+        return rc;
+    }
+    *h_image = host;
+    return SPK_OK;
+}
+
+int spk_free_device(void* d_ptr, void* stream) {
+    if (d_ptr) SPK_CK(cudaFreeAsync(d_ptr, as_stream(stream)));
+    return SPK_OK;
+}
+
+void spk_free_host(void* h_ptr) { std::free(h_ptr); }
 
 int spk_set_run_capacity(int64_t per_pixel) {
     if (per_pixel < 0 || per_pixel > INT_MAX) return fail(SPK_EINVAL, "spk: bad run capacity");

@@ -355,26 +355,27 @@ template __global__ void k_expand<double>(ExpArgs);
 // ----------------------------------------------------------------- scan --
 // Exclusive prefix sum of uint32 counts (three launches: block scans, scan
 // of block sums, add-back).
-__global__ void __launch_bounds__(kScanBlock) k_scan_blocks(const uint32_t* in, uint32_t* out,
-                                                            uint32_t* sums, int64_t n) {
-    __shared__ uint32_t ws[kScanBlock / 32];
+template <typename T>
+__global__ void __launch_bounds__(kScanBlock) k_scan_blocks(const uint32_t* in, T* out, T* sums,
+                                                            int64_t n) {
+    __shared__ T ws[kScanBlock / 32];
     const int64_t i = (int64_t)blockIdx.x * kScanBlock + threadIdx.x;
-    const uint32_t x = i < n ? in[i] : 0u;
+    const T x = i < n ? (T)in[i] : T(0);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t incl = x;
+    T incl = x;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, incl, d);
+        const T y = __shfl_up_sync(kFull, incl, d);
         if (lane >= d) incl += y;
     }
     if (lane == 31) ws[w] = incl;
     __syncthreads();
     if (w == 0) {
-        const uint32_t s = ws[lane];
-        uint32_t si = s;
+        const T s = ws[lane];
+        T si = s;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t y = __shfl_up_sync(kFull, si, d);
+            const T y = __shfl_up_sync(kFull, si, d);
             if (lane >= d) si += y;
         }
         ws[lane] = si - s;
@@ -384,35 +385,36 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_blocks(const uint32_t* in, 
     if (i < n) out[i] = incl - x + ws[w];
 }
 
-__global__ void __launch_bounds__(kScanBlock) k_scan_sums(uint32_t* sums, int64_t nb) {
-    __shared__ uint32_t ws[kScanBlock / 32];
-    __shared__ uint32_t carry;
-    if (threadIdx.x == 0) carry = 0;
+template <typename T>
+__global__ void __launch_bounds__(kScanBlock) k_scan_sums(T* sums, int64_t nb) {
+    __shared__ T ws[kScanBlock / 32];
+    __shared__ T carry;
+    if (threadIdx.x == 0) carry = T(0);
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int64_t base = 0; base < nb; base += kScanBlock) {
         const int64_t i = base + threadIdx.x;
-        const uint32_t x = i < nb ? sums[i] : 0u;
-        uint32_t incl = x;
+        const T x = i < nb ? sums[i] : T(0);
+        T incl = x;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t y = __shfl_up_sync(kFull, incl, d);
+            const T y = __shfl_up_sync(kFull, incl, d);
             if (lane >= d) incl += y;
         }
         if (lane == 31) ws[w] = incl;
         __syncthreads();
         if (w == 0) {
-            const uint32_t s = ws[lane];
-            uint32_t si = s;
+            const T s = ws[lane];
+            T si = s;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(kFull, si, d);
+                const T y = __shfl_up_sync(kFull, si, d);
                 if (lane >= d) si += y;
             }
             ws[lane] = si - s;
         }
         __syncthreads();
-        const uint32_t c0 = carry;
+        const T c0 = carry;
         if (i < nb) sums[i] = c0 + incl - x + ws[w];
         __syncthreads();
         if (threadIdx.x == kScanBlock - 1) carry = c0 + incl + ws[w];
@@ -420,10 +422,19 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_sums(uint32_t* sums, int64_
     }
 }
 
-__global__ void __launch_bounds__(kScanBlock) k_scan_add(uint32_t* out, const uint32_t* sums,
-                                                         int64_t n) {
+template <typename T>
+__global__ void __launch_bounds__(kScanBlock) k_scan_add(T* out, const T* sums, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * kScanBlock + threadIdx.x;
     if (i < n) out[i] += sums[blockIdx.x];
 }
+
+template __global__ void k_scan_blocks<uint32_t>(const uint32_t*, uint32_t*, uint32_t*, int64_t);
+template __global__ void k_scan_sums<uint32_t>(uint32_t*, int64_t);
+template __global__ void k_scan_add<uint32_t>(uint32_t*, const uint32_t*, int64_t);
+template __global__ void k_scan_blocks<unsigned long long>(const uint32_t*, unsigned long long*,
+                                                           unsigned long long*, int64_t);
+template __global__ void k_scan_sums<unsigned long long>(unsigned long long*, int64_t);
+template __global__ void k_scan_add<unsigned long long>(unsigned long long*, const unsigned long long*,
+                                                        int64_t);
 
 }  // namespace spk

@@ -114,8 +114,22 @@ struct CausalArgs {
     int lut_n;         // entries in the shared-memory value table
 };
 
+// SPKR emission from K2's run lists (records.cu)
+struct RecArgs {
+    SegArgs seg;                  // runs / counts / last (+ planes for overflowed pixels)
+    uint32_t* wc;                 // words per pixel (k_rec_count)
+    const unsigned long long* offs;  // exclusive prefix of wc (k_rec_write)
+    uint8_t* img;                 // SPKR file image (k_rec_write)
+    int width, height;
+    uint32_t fps;
+};
+
 template <int METHOD>
 __global__ void k_segment(SegArgs a);
+template <int METHOD>
+__global__ void k_rec_count(RecArgs a);
+template <int METHOD>
+__global__ void k_rec_write(RecArgs a);
 template <int METHOD, typename OUT>
 __global__ void k_fixup(SegArgs a, OUT* out, size_t out_pitch);
 template <int GP>
@@ -125,9 +139,14 @@ __global__ void k_fin_scatter(FinArgs a);
 template <typename OUT>
 __global__ void k_expand(ExpArgs a);
 size_t expand_smem_bytes(int out_size);  // dynamic shared memory of k_expand<OUT>
-__global__ void k_scan_blocks(const uint32_t* in, uint32_t* out, uint32_t* sums, int64_t n);
-__global__ void k_scan_sums(uint32_t* sums, int64_t nb);
-__global__ void k_scan_add(uint32_t* out, const uint32_t* sums, int64_t n);
+// exclusive scan of uint32 counts into T (uint32_t, or unsigned long long
+// where totals may pass 2^32)
+template <typename T>
+__global__ void k_scan_blocks(const uint32_t* in, T* out, T* sums, int64_t n);
+template <typename T>
+__global__ void k_scan_sums(T* sums, int64_t nb);
+template <typename T>
+__global__ void k_scan_add(T* out, const T* sums, int64_t n);
 constexpr int kScanBlock = 1024;
 template <int METHOD, typename OUT>
 __global__ void k_causal(CausalArgs a);

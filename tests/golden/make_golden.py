@@ -147,6 +147,43 @@ def save_volume(name, bits, w, h, methods):
     print(f"vol_{name}.npz", w, h, t)
 
 
+def save_records():
+    """SPKR images of the golden volumes from the reference's --emit-records
+    loop (proj/tools/spikecam_main.cpp:146-172 -> write_spkr), plus a
+    long-duration case (> 255-frame segments split into several words)."""
+    import tempfile
+    data = {}
+    vols = {}
+    for name in ("par12x9", "bar64x48", "noise40x25", "odd9x1", "odd13x7"):
+        g = np.load(OUT / f"vol_{name}.npz")
+        vols[name] = (g["planes"], *(int(x) for x in g["geom"]))
+    # sparse pixels: silent, single spike, ISI > 255, runs longer than 255 frames
+    rng = np.random.default_rng(83)
+    w, h, t = 7, 3, 2600
+    bits = np.zeros((t, w * h), np.uint8)
+    for p in range(w * h):
+        kind = p % 5
+        if kind == 1:
+            bits[int(rng.integers(0, t)), p] = 1
+        elif kind == 2:
+            bits[int(rng.integers(0, 300))::int(rng.integers(256, 700)), p] = 1
+        elif kind == 3:
+            bits[int(rng.integers(0, 5))::int(rng.integers(2, 9)), p] = 1
+        elif kind == 4:
+            bits[:, p] = (rng.random(t) < 0.02).astype(np.uint8)
+    vols["sparse7x3"] = (pack(bits, w, h), w, h, t)
+    data["sparse7x3/planes"] = vols["sparse7x3"][0]
+    data["sparse7x3/geom"] = np.array([w, h, t], np.int64)
+    with tempfile.TemporaryDirectory() as d:
+        for name, (planes, w, h, t) in vols.items():
+            for m, tag in ((0, "fsr"), (1, "ssr")):
+                f = Path(d) / f"{name}_{tag}.spkr"
+                REF.emit_records(planes, planes.shape[1], w, h, t, m, 20000, f)
+                data[f"{name}/{tag}"] = np.fromfile(f, np.uint8)
+    np.savez_compressed(OUT / "records.npz", **data)
+    print("records.npz:", len(vols), "volumes")
+
+
 ALL = [(0, "fsr", 32), (1, "ssr", 32), (2, "tfi", 32), (3, "tfp32", 32), (3, "tfp16", 16),
        (3, "tfp3", 3)]
 
@@ -184,7 +221,11 @@ def main():
     np.savez_compressed(OUT / "formats.npz", spk_golden=gold, spk_pad=pad, quant_in=vals,
                         quant_out=pgm)
     print("formats.npz")
+    save_records()
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["records"]:
+        save_records()
+    else:
+        main()
