@@ -159,13 +159,14 @@ template __global__ void k_fin_scatter<double>(FinArgs);
 
 // -------------------------------------------------------------- K3 expand --
 // Per-warp shared memory: for each frame of the sub-tile and each lane, the
-// pending values of its P pixels (D) and a byte mask of the pending pixels
-// (B), bank-interleaved by lane.
+// pending values of its P pixels (D, P values) and a bit mask of the pending
+// pixels (B, one 32-bit word: bit i = pixel i changes at this frame).  Only
+// the masks are read for every frame; D cells are read when a mask is set.
 template <typename OUT>
 struct ExpSmem {
     static constexpr int P = Geo<OUT>::P;
     static constexpr int DE = P * (int)sizeof(OUT);  // D cell bytes
-    static constexpr int BE = P;                       // B cell bytes
+    static constexpr int BE = 4;                       // B cell bytes
     static constexpr int per_warp = kSub * 32 * (DE + BE);
 };
 
@@ -173,6 +174,17 @@ size_t expand_smem_bytes(int out_size) {
     return out_size == 1 ? (size_t)ExpSmem<uint8_t>::per_warp * Geo<uint8_t>::WARPS
          : out_size == 4 ? (size_t)ExpSmem<float>::per_warp * Geo<float>::WARPS
                          : (size_t)ExpSmem<double>::per_warp * Geo<double>::WARPS;
+}
+
+// Mask bit of pixel i of a lane: for uint8 output (4 pixels per 32-bit word)
+// bit 8*(i&3) + (i>>2), so word w's byte mask is ((m >> w) & 0x01010101)*255;
+// otherwise bit i.
+template <typename OUT>
+__device__ __forceinline__ uint32_t pend_bit(int i) {
+    if constexpr (sizeof(OUT) == 1)
+        return 1u << (8 * (i & 3) + (i >> 2));
+    else
+        return 1u << i;
 }
 
 template <typename OUT>
@@ -186,7 +198,7 @@ __global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     unsigned char* D = sm + (size_t)warp * G::per_warp;
-    unsigned char* B = D + kSub * 32 * G::DE;
+    uint32_t* B = reinterpret_cast<uint32_t*>(D + kSub * 32 * G::DE);
 
     const int g = blockIdx.x * Geo<OUT>::WARPS + warp;
     const int c = a.chunk0 + (int)blockIdx.y;
@@ -232,10 +244,7 @@ __global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
     const uint32_t cnt_lo = a.bins[b0 + lane], cnt_hi = a.bins[b0 + 32 + lane];
     const Change<OUT>* st = reinterpret_cast<const Change<OUT>*>(a.stream);
 #pragma unroll
-    for (int f = 0; f < kSub; ++f)
-#pragma unroll
-        for (int k = 0; k < P / 8; ++k)
-            reinterpret_cast<uint2*>(B + (f * 32 + lane) * P)[k] = make_uint2(0u, 0u);
+    for (int f = 0; f < kSub; ++f) B[f * 32 + lane] = 0u;
 
     const size_t step = a.pitch * sizeof(OUT);
     char* ptr = reinterpret_cast<char*>(a.out) + ((size_t)f0 * a.pitch + (size_t)p0) * sizeof(OUT);
@@ -273,7 +282,7 @@ __global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
             reinterpret_cast<uint32_t*>(dcell)[i] = ch.bits;
         else
             reinterpret_cast<double*>(dcell)[i] = ch.v;
-        B[(fs * 32 + own) * P + i] = 0xffu;
+        atomicOr(&B[fs * 32 + own], pend_bit<OUT>(i));
     };
 
     for (int sub = 0; sub < kBins; ++sub) {
@@ -296,30 +305,27 @@ __global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
         const int nf = min(kSub, f1 - t0);
 #pragma unroll 4
         for (int fs = 0; fs < nf; ++fs) {
-            unsigned char* dcell = D + (fs * 32 + lane) * G::DE;
-            unsigned char* bcell = B + (fs * 32 + lane) * P;
-            if constexpr (sizeof(OUT) == 1) {
-                const uint4 dv = *reinterpret_cast<const uint4*>(dcell);
-                const uint4 bm = *reinterpret_cast<const uint4*>(bcell);
-                *reinterpret_cast<uint4*>(bcell) = make_uint4(0u, 0u, 0u, 0u);
-                words[0] = (words[0] & ~bm.x) | (dv.x & bm.x);
-                words[1] = (words[1] & ~bm.y) | (dv.y & bm.y);
-                words[2] = (words[2] & ~bm.z) | (dv.z & bm.z);
-                words[3] = (words[3] & ~bm.w) | (dv.w & bm.w);
-            } else {
-                const uint2 bm = *reinterpret_cast<const uint2*>(bcell);
-                if (bm.x | bm.y) {
-                    *reinterpret_cast<uint2*>(bcell) = make_uint2(0u, 0u);
-                    const uint32_t* dw = reinterpret_cast<const uint32_t*>(dcell);
+            const uint32_t bm = B[fs * 32 + lane];
+            if constexpr (sizeof(OUT) == 1) {  // branch-free: a clear mask keeps every byte
+                B[fs * 32 + lane] = 0u;
+                const uint4 dv = *reinterpret_cast<const uint4*>(D + (fs * 32 + lane) * G::DE);
+                const uint32_t m0 = (bm & 0x01010101u) * 0xffu, m1 = ((bm >> 1) & 0x01010101u) * 0xffu;
+                const uint32_t m2 = ((bm >> 2) & 0x01010101u) * 0xffu, m3 = ((bm >> 3) & 0x01010101u) * 0xffu;
+                words[0] = (words[0] & ~m0) | (dv.x & m0);
+                words[1] = (words[1] & ~m1) | (dv.y & m1);
+                words[2] = (words[2] & ~m2) | (dv.z & m2);
+                words[3] = (words[3] & ~m3) | (dv.w & m3);
+            } else if (bm) {
+                B[fs * 32 + lane] = 0u;
+                const uint32_t* dw = reinterpret_cast<const uint32_t*>(D + (fs * 32 + lane) * G::DE);
 #pragma unroll
-                    for (int i = 0; i < P; ++i) {
-                        const bool take = ((i < 4 ? bm.x : bm.y) >> ((i & 3) * 8)) & 1u;
-                        if constexpr (sizeof(OUT) == 4) {
-                            words[i] = take ? dw[i] : words[i];
-                        } else {
-                            words[2 * i] = take ? dw[2 * i] : words[2 * i];
-                            words[2 * i + 1] = take ? dw[2 * i + 1] : words[2 * i + 1];
-                        }
+                for (int i = 0; i < P; ++i) {
+                    const bool take = (bm >> i) & 1u;
+                    if constexpr (sizeof(OUT) == 4) {
+                        words[i] = take ? dw[i] : words[i];
+                    } else {
+                        words[2 * i] = take ? dw[2 * i] : words[2 * i];
+                        words[2 * i + 1] = take ? dw[2 * i + 1] : words[2 * i + 1];
                     }
                 }
             }

@@ -56,9 +56,14 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     Scan<METHOD> sc;
     sc.init();
     int nrun = 0;
-    // runs beyond the capacity are counted (overflow -> k_fixup) but not stored
+    // runs beyond the capacity are counted (overflow -> k_fixup) but not stored.
+    // The stored pair lives in its own registers (written only on an emit), so
+    // the automaton's next update does not wait for the store to read them.
+    int o_rs = 0, o_cnt = 0;
     auto emit = [&](bool e, int rs, int cnt) {
-        st_run_if(e & (nrun <= capm1), rp + min(nrun, capm1), rs, cnt);
+        o_rs = e ? rs : o_rs;
+        o_cnt = e ? cnt : o_cnt;
+        st_run_if(e & (nrun <= capm1), rp + min(nrun, capm1), o_rs, o_cnt);
         nrun += (int)e;
     };
 
@@ -107,24 +112,28 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         }
     } else {
     // FSR consumers: every lane walks its own pixel through the words at its
-    // own pace -- one event (or one word) per iteration -- so a lane with many
-    // breaks does not hold the others back word by word; the ring bounds how
-    // far lanes may drift apart.
-    FsrWord cw;
-    cw.S = 0;
-    int wi = -1;  // current word of this lane
+    // own pace -- a window of four words per iteration, stopping at the first
+    // event (fsr_batch4) -- so a lane with many breaks does not hold the others
+    // back word by word; the ring bounds how far lanes may drift apart.
+    int wi = 0;    // first word of this lane's window
+    int cpos = 0;  // frames of word wi already consumed
     for (;;) {
-        const bool need = cw.S == 0 && wi + 1 < ngroups;
-        const bool waiting = need && wi + 1 >= produced;
-        const int lowest = (int)__reduce_min_sync(kFull, (unsigned)(need ? wi + 1 : (cw.S ? wi : 0x7fffffff)));
-        if (__any_sync(kFull, waiting) && produced < ngroups && produced + kBatch <= lowest + kRing)
-            produce();
-        if (!__any_sync(kFull, cw.S != 0 || wi + 1 < ngroups)) break;
-        if (cw.S == 0 && wi + 1 < produced) {
-            ++wi;
-            cw.load(rg[wi & (kRing - 1)][lane], wi * 32);
+        const bool more = wi < ngroups;
+        const bool ready = min(wi + 4, ngroups) <= produced;
+        // refill only when a lane is starved, and only into slots no lane can
+        // still read (lowest = the earliest window start)
+        if (__any_sync(kFull, more & !ready)) {
+            const int lowest = (int)__reduce_min_sync(kFull, (unsigned)(more ? wi : 0x7fffffff));
+            if (produced < ngroups && produced + kBatch <= lowest + kRing) produce();
         }
-        if (cw.S) cw.iterate(sc, emit);
+        if (!__any_sync(kFull, more)) break;
+        if (more & (min(wi + 4, ngroups) <= produced)) {
+            const uint32_t w0 = rg[wi & (kRing - 1)][lane];
+            const uint32_t w1 = wi + 1 < ngroups ? rg[(wi + 1) & (kRing - 1)][lane] : 0u;
+            const uint32_t w2 = wi + 2 < ngroups ? rg[(wi + 2) & (kRing - 1)][lane] : 0u;
+            const uint32_t w3 = wi + 3 < ngroups ? rg[(wi + 3) & (kRing - 1)][lane] : 0u;
+            wi += fsr_batch4(sc, w0, w1, w2, w3, wi * 32, cpos, emit);
+        }
     }
     }
     if (valid) {

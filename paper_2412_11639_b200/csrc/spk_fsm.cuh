@@ -330,56 +330,47 @@ SPK_HD uint32_t bit_shr_clamp(uint32_t x, uint32_t, uint32_t s) {
 
 // FSR over one 32-frame word (bit 31 = first frame), accepting spikes in
 // bulk.  While the open run's pair is [lo, lo+hw], a spike is in the run iff
-// its gap to the previous spike lies in the pair; bit-parallel over the word:
-//   * a spike has a predecessor at distance lo or lo+hw:  Q = S>>lo | S>>(lo+1)
-//   * no spike has another within lo-1 before it:          C = S & smear(S, lo-1)
-//   * the word's first spike is checked against `last` directly.
-// Everything before the first violating spike is accepted at once (cnt +=
-// popc, last = latest accepted); the violating spike -- a pair completion or
-// a break -- goes through the exact per-spike automaton, then the bulk test
-// resumes with the updated pair.  A word costs one iteration per event
-// instead of one per spike.  FsrWord holds one word; iterate() does one bulk
-// test plus at most one event, so a caller can interleave words freely.
+// its gap to the previous spike lies in the pair.  Bit-parallel over the word,
+// the FIRST violating spike is the first one flagged by
+//   * no spike exactly lo (or, hw = 1, lo+1) frames earlier:  ~(S>>lo | S>>(lo+1))
+//   * a spike exactly 1 frame earlier while lo >= 2:          S & S>>1
+//   * for the word's first spike, its gap to `last` directly.
+// Proof sketch: a flagged spike is a violation (its real predecessor is at a
+// flagged distance).  Conversely let c be the first violation, p its real
+// predecessor.  A gap c-p > lo+hw leaves frames c-lo, c-lo-hw empty -> flagged.
+// A gap c-p < lo escapes the first test only through a spike k at c-lo or
+// c-lo-1 before p; every accepted gap (and the gap that opened the current
+// state) is >= lo, so p-k >= lo, forcing c-p = 1 and c-k = lo+1 -- caught by
+// the second test.  Everything before the first flagged spike is accepted at
+// once (cnt += popc, last = latest accepted); the flagged spike -- a pair
+// completion or a break -- goes through the exact per-spike automaton, then
+// the bulk test resumes with the updated pair.  A word costs one iteration per
+// event instead of one per spike.  FsrWord holds one word; iterate() does one
+// bulk test plus at most one event, so a caller can interleave words freely.
 struct FsrWord {
-    uint32_t So, S;                      // spikes of the word / not yet consumed
-    uint32_t R1, R2, R4, R8, R16, R32;   // So smeared by 1..2^k frames
-    uint32_t fb;                         // the word's first spike
-    int f, base;                         // its offset, the word's first frame
+    uint32_t So, S;  // spikes of the word / not yet consumed
+    uint32_t G1;     // spikes with a spike one frame earlier
+    uint32_t fb;     // the word's first spike
+    int f, base;     // its offset, the word's first frame
 
     SPK_HD void load(uint32_t w, int b) {
         So = S = w;
         base = b;
-        R1 = So >> 1;
-        R2 = R1 | (R1 >> 1);
-        R4 = R2 | (R2 >> 2);
-        R8 = R4 | (R4 >> 4);
-        R16 = R8 | (R8 >> 8);
-        R32 = R16 | (R16 >> 16);
+        G1 = So & (So >> 1);
         f = bit_clz(So | 1u);
         fb = So ? (0x80000000u >> f) : 0u;
     }
 
     template <class SC, class EMIT>
     SPK_HD void iterate(SC& sc, EMIT&& emit) {
-        // ---- bulk: violations among the remaining spikes (selects only)
+        // ---- bulk: the first violation among the remaining spikes (selects only)
         const int lo = sc.lo;
         const uint32_t hw = sc.hw;
-        const int L = lo - 1;  // gaps < lo are too short: smear S by 1..L
-        uint32_t Rk = R1;
-        Rk = bit_sel(L >= 2, R2, Rk);
-        Rk = bit_sel(L >= 4, R4, Rk);
-        Rk = bit_sel(L >= 8, R8, Rk);
-        Rk = bit_sel(L >= 16, R16, Rk);
-        const uint32_t Lc = (uint32_t)(L < 1 ? 1 : (L > 31 ? 31 : L));
-        const uint32_t pk = 0x80000000u >> bit_clz(Lc);  // largest power of two <= Lc
-        uint32_t M = Rk | (Rk >> (Lc - pk));
-        M = bit_sel(L >= 32, R32, M);
-        M = bit_sel(L <= 0, 0u, M);
         const uint32_t Q = bit_shr_clamp(So, 0u, (uint32_t)lo) |
                            bit_sel(hw != 0u, bit_shr_clamp(So, 0u, (uint32_t)lo + 1u), 0u);
         const int d0 = base + f - sc.last;
         const bool bad0 = ((S & fb) != 0u) & ((uint32_t)(d0 - lo) > hw);
-        const uint32_t V = (S & M) | (S & ~Q & ~fb) | bit_sel(bad0, fb, 0u);
+        const uint32_t V = (S & ~(Q | fb)) | bit_sel(lo >= 2, S & G1, 0u) | bit_sel(bad0, fb, 0u);
         const uint32_t p = V ? (uint32_t)bit_clz(V) : 32u;
         const uint32_t A = S & ~bit_shr_clamp(0xffffffffu, 0u, p);
         sc.cnt += bit_popc(A);
@@ -394,6 +385,69 @@ struct FsrWord {
         emit(e, rs, cnt);
     }
 };
+
+// FSR over a window of four consecutive words (frames base0 .. base0+127; the
+// first `cpos` frames of word 0 already consumed).  The FsrWord test is run on
+// all four words at once -- independent given the open run's pair, so they
+// overlap in the pipeline -- with each word's first remaining spike checked
+// against the last spike before it (in an earlier word of the window, or
+// sc.last).  The first word holding a violation decides: everything before
+// the violating spike is accepted in bulk and the spike itself goes through
+// the exact automaton.  Returns the number of words fully consumed (4 when no
+// word of the window violates) and leaves `cpos` = frames consumed in the new
+// first word.  Words past the end of the stream must be passed as 0.
+template <class SC, class EMIT>
+SPK_HD int fsr_batch4(SC& sc, uint32_t W0, uint32_t W1, uint32_t W2, uint32_t W3, int base0,
+                      int& cpos, EMIT&& emit) {
+    const int lo = sc.lo;
+    const uint32_t hw = sc.hw;
+    const bool two = lo >= 2;
+    const uint32_t r0 = W0 & bit_shr_clamp(0xffffffffu, 0u, (uint32_t)cpos);
+    int pv = sc.last;  // last spike before the word under test
+    int p0v, p1v, p2v, p3v;
+    uint32_t V0, V1, V2, V3;
+    auto test = [&](uint32_t w, uint32_t r, int base, int& prev_out, uint32_t& V) {
+        prev_out = pv;
+        const uint32_t Q = bit_shr_clamp(w, 0u, (uint32_t)lo) |
+                           bit_sel(hw != 0u, bit_shr_clamp(w, 0u, (uint32_t)lo + 1u), 0u);
+        const uint32_t G1 = w & (w >> 1);
+        const int f = bit_clz(r | 1u);
+        const uint32_t fb = r ? (0x80000000u >> f) : 0u;
+        const bool bad0 = (r != 0u) & ((uint32_t)(base + f - pv - lo) > hw);
+        V = (r & ~(Q | fb)) | bit_sel(two, r & G1, 0u) | bit_sel(bad0, fb, 0u);
+        pv = r ? base + 32 - bit_ffs(r) : pv;
+    };
+    test(W0, r0, base0, p0v, V0);
+    test(W1, W1, base0 + 32, p1v, V1);
+    test(W2, W2, base0 + 64, p2v, V2);
+    test(W3, W3, base0 + 96, p3v, V3);
+    const uint32_t c0 = (uint32_t)bit_popc(r0), c1 = (uint32_t)bit_popc(W1);
+    const uint32_t c2 = (uint32_t)bit_popc(W2), c3 = (uint32_t)bit_popc(W3);
+    const uint32_t nz = (uint32_t)(V0 != 0u) | (uint32_t)(V1 != 0u) << 1 |
+                        (uint32_t)(V2 != 0u) << 2 | (uint32_t)(V3 != 0u) << 3 | 16u;
+    // first violating word; with none, word 3 is taken whole (Vk = 0 -> p = 32)
+    const int k = bit_ffs(nz) - 1;
+    const bool ev = k < 4;
+    const int kk = ev ? k : 3;
+    const bool s0 = kk == 0, s1 = kk == 1, s2 = kk == 2;
+    const uint32_t Vk = bit_sel(s0, V0, bit_sel(s1, V1, bit_sel(s2, V2, V3)));
+    const uint32_t rk = bit_sel(s0, r0, bit_sel(s1, W1, bit_sel(s2, W2, W3)));
+    const int prevk = (int)bit_sel(s0, (uint32_t)p0v,
+                                   bit_sel(s1, (uint32_t)p1v, bit_sel(s2, (uint32_t)p2v, (uint32_t)p3v)));
+    const uint32_t before = bit_sel(kk > 0, c0, 0u) + bit_sel(kk > 1, c1, 0u) + bit_sel(kk > 2, c2, 0u);
+    const int basek = base0 + 32 * kk;
+    const int p = bit_clz(Vk);
+    const uint32_t A = rk & ~bit_shr_clamp(0xffffffffu, 0u, (uint32_t)p);
+    sc.cnt += (int)(before + (uint32_t)bit_popc(A));
+    sc.last = A ? basek + 32 - bit_ffs(A) : prevk;
+    cpos = ev ? p + 1 : 0;
+    if (ev) {  // the violating spike through the exact automaton
+        int rs, cnt;
+        const bool e = sc.step(basek + p, rs, cnt);
+        emit(e, rs, cnt);
+    }
+    return ev ? kk : 4;
+}
 
 // `emit(pred, rs, cnt)` stores a closed run when pred is true.
 template <class SC, class EMIT>

@@ -1,0 +1,96 @@
+// write_ceiling.cu -- HBM write-only ceiling probe (reference point for K3):
+// grid-stride 16-B stores, 32-B (v8) stores, and cudaMemsetAsync over 4 GB.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o write_ceiling write_ceiling.cu
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void w16(uint4* p, size_t n, uint32_t v) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = make_uint4(v, v, v, v);
+}
+
+// row-tiled like K3: warp writes 512 B of a row per frame, 16 frames per tile
+__global__ void wrows(char* p, size_t pitch, int rows, int groups, uint32_t v) {
+    const int lane = threadIdx.x & 31;
+    const int g = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int c = blockIdx.y;
+    if (g >= groups) return;
+    char* q = p + (size_t)c * 1024 * pitch + (size_t)g * 512 + lane * 16;
+    for (int f = 0; f < 1024 && c * 1024 + f < rows; ++f)
+        *reinterpret_cast<uint4*>(q + (size_t)f * pitch) = make_uint4(v, v, v, f);
+}
+
+// warp writes SEG bytes of each row (lane: SEG/32 bytes as 16-B stores), 1024 rows
+template <int SEG>
+__global__ void wseg(char* p, size_t pitch, int rows, int groups, uint32_t v) {
+    const int lane = threadIdx.x & 31;
+    const int g = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int c = blockIdx.y;
+    if (g >= groups) return;
+    char* q = p + (size_t)c * 1024 * pitch + (size_t)g * SEG;
+    for (int f = 0; f < 1024 && c * 1024 + f < rows; ++f) {
+#pragma unroll
+        for (int k = 0; k < SEG / 512; ++k)
+            *reinterpret_cast<uint4*>(q + (size_t)f * pitch + k * 512 + lane * 16) = make_uint4(v, v, v, f);
+    }
+}
+
+template <int SEG>
+void run_seg(char* d, cudaEvent_t a, cudaEvent_t b, int wpb) {
+    const int groups = 100000 / SEG;
+    dim3 grid((groups + wpb - 1) / wpb, 40);
+    wseg<SEG><<<grid, wpb * 32>>>(d, 100000, 40000, groups, 1);
+    cudaEventRecord(a);
+    for (int r = 0; r < 10; ++r) wseg<SEG><<<grid, wpb * 32>>>(d, 100000, 40000, groups, r);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    const double bytes = (double)groups * SEG * 40000;
+    printf("wseg %5d B/row, %d warps/block: %.3f ms  %.0f GB/s\n", SEG, wpb, ms / 10, bytes / (ms / 10) / 1e6);
+}
+
+int main() {
+    const size_t bytes = 40000ull * 100000ull;
+    char* d;
+    cudaMalloc(&d, bytes);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float ms;
+    for (int blocks : {148 * 4, 148 * 8, 148 * 16, 148 * 32}) {
+        w16<<<blocks, 512>>>((uint4*)d, bytes / 16, 1);
+        cudaEventRecord(a);
+        for (int r = 0; r < 10; ++r) w16<<<blocks, 512>>>((uint4*)d, bytes / 16, r);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        printf("w16 grid %5d x 512: %.3f ms  %.0f GB/s\n", blocks, ms / 10, bytes / (ms / 10) / 1e6);
+    }
+    cudaMemsetAsync(d, 1, bytes);
+    cudaEventRecord(a);
+    for (int r = 0; r < 10; ++r) cudaMemsetAsync(d, r, bytes);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    printf("memset: %.3f ms  %.0f GB/s\n", ms / 10, bytes / (ms / 10) / 1e6);
+    for (int wpb : {4, 8}) {
+        dim3 grid((196 + wpb - 1) / wpb, 40);
+        wrows<<<grid, wpb * 32>>>(d, 100000, 40000, 196, 1);
+        cudaEventRecord(a);
+        for (int r = 0; r < 10; ++r) wrows<<<grid, wpb * 32>>>(d, 100000, 40000, 196, r);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        printf("wrows (K3 pattern, %d warps/block): %.3f ms  %.0f GB/s\n", wpb, ms / 10, bytes / (ms / 10) / 1e6);
+    }
+    for (int wpb : {2, 4}) {
+        run_seg<512>(d, a, b, wpb);
+        run_seg<1024>(d, a, b, wpb);
+        run_seg<2048>(d, a, b, wpb);
+        run_seg<4096>(d, a, b, wpb);
+    }
+    printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}

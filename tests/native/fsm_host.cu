@@ -3,6 +3,7 @@
 // header the sm_100a kernels use, driven frame by frame on the CPU and
 // compared with the oracle in tests/test_fsm_host.py.  Test code only.
 #include <cstdint>
+#include <vector>
 
 #include "../../paper_2412_11639_b200/csrc/spk_fsm.cuh"
 #include "../../paper_2412_11639_b200/csrc/spk_common.cuh"
@@ -131,6 +132,41 @@ extern "C" long word_runs(const uint8_t* bits, long frames, int method, long* st
         spk::Scan<spk::kSSR> sc;
         go(sc, false);
     }
+    for (long k = 0; k < n && k < cap; ++k) end[k] = (k + 1 < n) ? start[k + 1] : last;
+    return n;
+}
+
+// The FSR 4-word window driver of the segment kernel (fsr_batch4).
+extern "C" long batch_runs(const uint8_t* bits, long frames, int method, long* start, long* end,
+                           long* cnt, long cap) {
+    if (method != 0) return word_runs(bits, frames, method, start, end, cnt, cap);
+    long n = 0, last = -1;
+    auto put = [&](bool e, int rs, int c) {
+        if (e) {
+            if (n < cap) {
+                start[n] = rs;
+                cnt[n] = c;
+            }
+            ++n;
+        }
+    };
+    const long ngroups = (frames + 31) / 32;
+    std::vector<uint32_t> words(ngroups + 4, 0u);
+    for (long f = 0; f < frames; ++f)
+        if (bits[f]) {
+            words[f / 32] |= 0x80000000u >> (f % 32);
+            last = f;
+        }
+    spk::Scan<spk::kFSR> sc;
+    sc.init();
+    long wi = 0;
+    int cpos = 0;
+    while (wi < ngroups)
+        wi += spk::fsr_batch4(sc, words[wi], words[wi + 1], words[wi + 2], words[wi + 3],
+                              (int)(wi * 32), cpos, put);
+    int rs, c;
+    const bool e = sc.tail(rs, c);
+    put(e, rs, c);
     for (long k = 0; k < n && k < cap; ++k) end[k] = (k + 1 < n) ? start[k + 1] : last;
     return n;
 }

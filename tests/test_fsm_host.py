@@ -33,6 +33,8 @@ def fsm():
     h.scan_runs.argtypes = h.fsm_runs.argtypes
     h.word_runs.restype = C.c_long
     h.word_runs.argtypes = h.fsm_runs.argtypes
+    h.batch_runs.restype = C.c_long
+    h.batch_runs.argtypes = h.fsm_runs.argtypes
 
     def make(fn):
         def run(bits, m):
@@ -42,7 +44,8 @@ def fsm():
                    c.ctypes.data, cap)
             return s[:n], e[:n], c[:n]
         return run
-    return {"fsm": make(h.fsm_runs), "scan": make(h.scan_runs), "word": make(h.word_runs)}
+    return {"fsm": make(h.fsm_runs), "scan": make(h.scan_runs), "word": make(h.word_runs),
+            "batch": make(h.batch_runs)}
 
 
 def if_stream(rng, t, segs, flips):
@@ -58,7 +61,7 @@ def if_stream(rng, t, segs, flips):
     return b ^ (rng.random(t) < flips).astype(np.uint8)
 
 
-@pytest.mark.parametrize("kind", ["fsm", "scan", "word"])
+@pytest.mark.parametrize("kind", ["fsm", "scan", "word", "batch"])
 @pytest.mark.parametrize("family", ["noise", "if", "if_noisy", "if_rare_flips"])
 def test_fsm_matches_oracle(fsm, oracle, family, kind):
     run = fsm[kind]
@@ -75,7 +78,7 @@ def test_fsm_matches_oracle(fsm, oracle, family, kind):
             assert all(np.array_equal(x, y) for x, y in zip(got, want)), (family, m, t)
 
 
-@pytest.mark.parametrize("kind", ["fsm", "scan", "word"])
+@pytest.mark.parametrize("kind", ["fsm", "scan", "word", "batch"])
 def test_fsm_golden_rows(fsm, golden_dir, kind):
     z = np.load(golden_dir / "rows.npz")
     for name in sorted({k.split("/")[0] for k in z.files}):
