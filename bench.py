@@ -259,28 +259,29 @@ def main():
         return ms, launches
 
     def kernel_times(method, steps):
-        """mean per-kernel device time (CUDA events on the launch stream)"""
+        """mean per-phase device time (CUDA events on the launch stream):
+        K2 segment, K2b/scan/K2c finalize, K3 expand, fixup"""
         import ctypes as C
-        fs, fe, ff = C.c_float(), C.c_float(), C.c_float()
-        seg, exp = [], []
+        v = [C.c_float() for _ in range(4)]
+        acc = [[] for _ in range(4)]
         lib.spk_set_timing(1)
         for _ in range(steps):
             step(method)
-            capi.check(lib.spk_last_timing(C.byref(fs), C.byref(fe), C.byref(ff)))
-            seg.append(fs.value)
-            exp.append(fe.value)
+            capi.check(lib.spk_last_timing(*(C.byref(x) for x in v)))
+            for a, x in zip(acc, v):
+                a.append(x.value)
         lib.spk_set_timing(0)
-        return float(np.mean(seg)), float(np.mean(exp))
+        return [float(np.mean(a)) for a in acc]
 
     sampler = ClockSampler(local)
     with sampler:
         ms, launches = timed(args.method, args.steps, args.warmup)
     clocks = sampler.report()
-    seg_ms, exp_ms = kernel_times(args.method, max(3, min(20, args.steps)))
+    phases = kernel_times(args.method, max(3, min(20, args.steps)))
     other = "ssr" if args.method == "fsr" else "fsr"
     k2 = max(5, args.steps // 5)
     ms2, _ = timed(other, k2, 3)
-    seg2, exp2 = kernel_times(other, max(3, min(20, k2)))
+    phases2 = kernel_times(other, max(3, min(20, k2)))
 
     peak, peak_kind = peaks()
     pxf = W * H * frames
@@ -288,15 +289,18 @@ def main():
     fps = world * frames / (ms_step * 1e-3)
     gpxf = world * pxf / (ms_step * 1e-3) / 1e9
 
-    def roofline(seg, exp, ms_step):
-        # dominant kernel: algorithmic bytes per launch / its mean duration
+    def roofline(ph, ms_step):
+        """Dominant kernel (largest share of the step): algorithmic bytes per
+        launch / its mean CUDA-event duration.  K2 (segment) reads 0.125 B/px-frame
+        and is issue-bound (integer ALU; profiles/), K3 (expand) writes 1 B/px-frame
+        and is HBM-write-bound; both fractions are reported."""
+        seg, fin, exp, fix = ph
+        k2_gbs = pxf * 0.125 / (seg * 1e-3) / 1e9
+        k3_gbs = pxf * 1.0 / (exp * 1e-3) / 1e9
         if exp >= seg:
-            kern, alg = "k_expand", pxf * 1.0
-            dur = exp
+            kern, achieved, dur = "k_expand", k3_gbs, exp
         else:
-            kern, alg = "k_segment", pxf * 0.125
-            dur = seg
-        achieved = alg / (dur * 1e-3) / 1e9
+            kern, achieved, dur = "k_segment", k2_gbs, seg
         traffic = None
         tf = ROOT / "profiles" / f"traffic_{kern}_{args.method}.json"
         if tf.exists():
@@ -304,8 +308,12 @@ def main():
         return {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_kind": peak_kind, "kernel_ms": dur,
+                "kernel_note": ("k_segment is issue-bound (integer ALU), not HBM-bound: its "
+                                "HBM fraction is low by construction" if kern == "k_segment" else
+                                "HBM write-bound"),
                 "step_frac": pxf * BYTES_PER_PXF / (ms_step * 1e-3) / 1e9 / peak,
-                "segment_ms": seg, "expand_ms": exp}
+                "phases_ms": {"segment": seg, "finalize": fin, "expand": exp, "fixup": fix},
+                "expand_hbm_gbs": k3_gbs, "expand_hbm_frac": k3_gbs / peak}
 
     line = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
@@ -317,12 +325,12 @@ def main():
                    "l2": "no flush: 0.5 GB in + 4 GB out per step > 126 MB L2",
                    "vs_baseline_ref": "FPGA 20,000 FPS (BASELINE.md, PAPER.md:199)"},
         "gpx_frames_per_s": gpxf,
-        "roofline": roofline(seg_ms, exp_ms, ms_step),
+        "roofline": roofline(phases, ms_step),
         "gpu_launches": int(launches),
         "clocks": clocks,
         other: {"value": world * frames / (ms2 / k2 * 1e-3),
                 "ms_per_step": ms2 / k2,
-                "roofline": roofline(seg2, exp2, ms2 / k2)},
+                "roofline": roofline(phases2, ms2 / k2)},
     }
 
     # end to end through the C-ABI host boundary (pinned host buffers)

@@ -147,11 +147,12 @@ size_t spk_plane_pitch(int32_t width, int32_t height);
 int64_t spk_launch_count(int reset);
 /* Per-phase device timing of this thread's next spk_reconstruct_* calls:
  * when enabled, CUDA events are recorded on the call's stream around the
- * segment (K2), expand (K3) and fixup kernels (or the single TFI/TFP kernel,
- * reported as `expand`).  spk_last_timing waits for the last call's events and
- * returns milliseconds (negative if a phase did not run). */
+ * segment kernel (K2), the run finalisation (K2b, scan, K2c), the expand
+ * kernel (K3) and the overflow fixup (TFI/TFP: the single kernel is reported
+ * as `expand`).  spk_last_timing waits for the last call's events and returns
+ * milliseconds (negative if a phase did not run). */
 int spk_set_timing(int enable);
-int spk_last_timing(float* segment_ms, float* expand_ms, float* fixup_ms);
+int spk_last_timing(float* segment_ms, float* finalize_ms, float* expand_ms, float* fixup_ms);
 const char* spk_last_error(void);
 int spk_version(void);
 

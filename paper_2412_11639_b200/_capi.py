@@ -49,7 +49,7 @@ SIGNATURES = {
     "spk_plane_pitch": (C.c_size_t, [C.c_int32, C.c_int32]),
     "spk_launch_count": (C.c_int64, [C.c_int]),
     "spk_set_timing": (C.c_int, [C.c_int]),
-    "spk_last_timing": (C.c_int, [_P, _P, _P]),
+    "spk_last_timing": (C.c_int, [_P, _P, _P, _P]),
     "spk_last_error": (C.c_char_p, []),
     "spk_version": (C.c_int, []),
     "spk_synth": (C.c_int, [C.c_int, C.c_uint64, _G, C.c_int64, C.c_double, _P, _P]),

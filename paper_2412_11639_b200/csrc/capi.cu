@@ -26,10 +26,11 @@ namespace {
 thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
 thread_local bool g_timing = false;
-thread_local cudaEvent_t g_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+thread_local cudaEvent_t g_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 thread_local int g_ev_used = 0;  // events recorded by the last call
 
-// phase marker k (0..3) on stream s when timing is enabled
+// phase marker k (0..4) on stream s when timing is enabled: 0 before K2,
+// 1 after K2, 2 after K2b/scan/K2c, 3 after K3, 4 after the fixup
 int mark(int k, cudaStream_t s) {
     if (!g_timing) return SPK_OK;
     if (!g_ev[k]) {
@@ -204,6 +205,7 @@ template <typename OUT>
 int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pitch,
                   cudaStream_t s) {
     constexpr int GP = 32 * Geo<OUT>::P;
+    mark(1, s);
     FinArgs f;
     f.runs = sa.runs;
     f.counts = sa.counts;
@@ -227,7 +229,7 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     f.cursor = static_cast<uint32_t*>(w.cursor.p);
     k_fin_scatter<OUT><<<(unsigned)((sa.npix + 255) / 256), 256, 0, s>>>(f);
     SPK_LAUNCHED("k_fin_scatter");
-    mark(1, s);
+    mark(2, s);
 
     ExpArgs e;
     e.tblv = w.tblv.p;
@@ -312,8 +314,9 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
     if (method == SPK_TFI || method == SPK_TFP) {
         mark(0, s);
         mark(1, s);
-        rc = launch_causal<OUT>(g, planes, method, window, out, out_pitch, s);
         mark(2, s);
+        rc = launch_causal<OUT>(g, planes, method, window, out, out_pitch, s);
+        mark(3, s);
         return rc;
     }
 
@@ -345,9 +348,9 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
         mark(0, s);
         if ((rc = launch_segment(method, a, s))) return rc;
         if ((rc = launch_expand<OUT>(a, w, out, out_pitch, s))) return rc;
-        mark(2, s);
-        rc = launch_fixup<OUT>(method, a, out, out_pitch, s);
         mark(3, s);
+        rc = launch_fixup<OUT>(method, a, out, out_pitch, s);
+        mark(4, s);
         return rc;
     }
     cudaStream_t aux;
@@ -724,8 +727,8 @@ int spk_set_timing(int enable) {
     return SPK_OK;
 }
 
-int spk_last_timing(float* segment_ms, float* expand_ms, float* fixup_ms) {
-    float* outs[3] = {segment_ms, expand_ms, fixup_ms};
+int spk_last_timing(float* segment_ms, float* finalize_ms, float* expand_ms, float* fixup_ms) {
+    float* outs[4] = {segment_ms, finalize_ms, expand_ms, fixup_ms};
     for (float* o : outs)
         if (o) *o = -1.f;
     if (g_ev_used < 2) return fail(SPK_EINVAL, "spk_last_timing: no timed call");
