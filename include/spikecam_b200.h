@@ -81,6 +81,39 @@ typedef struct spk_run {
     uint32_t intervals;
 } spk_run;
 
+/* Time shards (exact stitching of independently scanned frame ranges):
+ * per pixel, how the true automaton -- re-run from the true state at the
+ * shard start -- met the speculative one (started fresh at the shard start).
+ * npre >= 0: synced after `npre` true runs closed; the speculative run that
+ * started at rs_spec is the true run that started at rs_true, holding `delta`
+ * more intervals.  npre = -2: never synced, but every true run of the shard
+ * is in the prefix list; npre = -1: needs the full re-scan. */
+typedef struct spk_sync {
+    int32_t rs_true;
+    int32_t rs_spec;
+    int32_t delta;
+    int32_t npre;
+} spk_sync;
+
+/* Close of the run(s) that cross a shard boundary, relative to the shard the
+ * record belongs to.  Run A is the run covering the boundary (the run open
+ * there, or the run that will start at the last spike before it).
+ * a_state: 0 = no such run; 1 = it closes at a_end with a_intervals intervals
+ * in total; 2 (entry records only) = it runs on past the next boundary -- take
+ * the next record's A.  When A closes at the last spike before the boundary,
+ * run B starts there: b_kind 1 = b_intervals / b_end known, 2 = B runs on past
+ * the next boundary (the next record's A), 0 = no such run. */
+typedef struct spk_close {
+    int32_t a_state;
+    int32_t a_intervals;
+    int32_t a_end;
+    int32_t b_kind;
+    int32_t b_intervals;
+    int32_t b_end;
+    int32_t pad0;
+    int32_t pad1;
+} spk_close;
+
 /* ---- device-resident path (asynchronous on `stream`) -------------------- */
 int spk_reconstruct_u8(const spk_geom* g, const void* d_planes, int method, int tfp_window,
                        uint8_t* d_out, size_t out_pitch, void* stream);
@@ -94,6 +127,58 @@ int spk_reconstruct_f64(const spk_geom* g, const void* d_planes, int method, int
  * truncated), its last spike frame in d_last[p] (-1 if none). */
 int spk_segment(const spk_geom* g, const void* d_planes, int method, spk_run* d_runs,
                 int64_t run_cap, uint32_t* d_counts, int32_t* d_last, void* stream);
+
+/* spk_segment with the automaton state carried across time shards: d_state_in
+ * (nullable = stream start) is the state at frame 0 of these planes, d_state_out
+ * (nullable) receives the state after the last frame.  State = 14 int32
+ * fields per pixel, field-major (d_state[f * W*H + p]), frames relative to the
+ * first plane (earlier spikes negative); see spk_shard_* below. */
+int spk_segment_state(const spk_geom* g, const void* d_planes, int method, spk_run* d_runs,
+                      int64_t run_cap, uint32_t* d_counts, int32_t* d_last,
+                      const int32_t* d_state_in, int32_t* d_state_out, void* stream);
+
+/* ---- time shards: exact reconstruction of one long stream cut in frame
+ * ranges (BASELINE configs[4]).  Shard r is scanned on its own
+ * (spk_segment_state from a fresh state: the speculative runs); then, in shard
+ * order, spk_shard_resolve re-runs the start of shard r from the true entry
+ * state until it agrees with the speculative automaton and spk_shard_junction
+ * produces the true exit state (the next shard's entry) and whether the run
+ * open at the entry closes inside the shard; spk_shard_close_chain carries the
+ * close of boundary-crossing runs back; spk_shard_stitch writes each shard's
+ * true run list, which spk_expand_runs_* turns into that shard's frames.
+ * g->frames is the shard length throughout; state layout as spk_segment_state. */
+/* the automaton state at the start of a stream (entry of the first shard) */
+int spk_state_fresh(int64_t npix, int32_t* d_state, void* stream);
+int spk_shard_resolve(const spk_geom* g, const void* d_planes, int method, const int32_t* d_entry,
+                      spk_run* d_prefix, int32_t prefix_cap, spk_sync* d_sync, int32_t* d_tstate,
+                      void* stream);
+int spk_shard_junction(const spk_geom* g, int method, const int32_t* d_entry, const spk_sync* d_sync,
+                       const spk_run* d_prefix, int32_t prefix_cap, const int32_t* d_tstate,
+                       const spk_run* d_spec, int64_t spec_cap, const uint32_t* d_spec_counts,
+                       const int32_t* d_spec_state, const spk_run* d_fb, const uint32_t* d_fb_counts,
+                       const int32_t* d_fb_state, int32_t* d_exit_state, spk_close* d_entry_close,
+                       spk_close* d_tail_close, void* stream);
+int spk_shard_close_chain(int64_t npix, const spk_close* d_entry_close_next,
+                          const spk_close* d_close_next, int32_t shard_len, spk_close* d_close,
+                          void* stream);
+int spk_shard_stitch(const spk_geom* g, int method, const int32_t* d_entry, const spk_sync* d_sync,
+                     const spk_run* d_prefix, int32_t prefix_cap, const int32_t* d_tstate,
+                     const spk_run* d_spec, int64_t spec_cap, const uint32_t* d_spec_counts,
+                     const int32_t* d_spec_state, const spk_run* d_fb, const uint32_t* d_fb_counts,
+                     const int32_t* d_fb_state, const spk_close* d_close, spk_run* d_region,
+                     int64_t region_cap, uint32_t* d_region_counts, int32_t* d_region_last,
+                     void* stream);
+/* Frames of one shard from its stitched run list (run starts may precede the
+ * shard: such a run's change is placed at frame 0; values use the true span). */
+int spk_expand_runs_u8(const spk_geom* g, const spk_run* d_runs, int64_t run_cap,
+                       const uint32_t* d_counts, const int32_t* d_last, uint8_t* d_out,
+                       size_t out_pitch, void* stream);
+int spk_expand_runs_f32(const spk_geom* g, const spk_run* d_runs, int64_t run_cap,
+                        const uint32_t* d_counts, const int32_t* d_last, float* d_out,
+                        size_t out_pitch, void* stream);
+int spk_expand_runs_f64(const spk_geom* g, const spk_run* d_runs, int64_t run_cap,
+                        const uint32_t* d_counts, const int32_t* d_last, double* d_out,
+                        size_t out_pitch, void* stream);
 
 /* one byte per bit (frame-major n*W*H + p, nonzero = spike) <-> planes */
 int spk_pack_bytes(const spk_geom* g, const uint8_t* d_bytes, void* d_planes, void* stream);

@@ -45,6 +45,17 @@ SIGNATURES = {
     "spk_records_host": (C.c_int, [_G, _P, C.c_int, C.c_uint32, _P, _P]),
     "spk_free_device": (C.c_int, [_P, _P]),
     "spk_free_host": (None, [_P]),
+    "spk_segment_state": (C.c_int, [_G, _P, C.c_int, _P, C.c_int64, _P, _P, _P, _P, _P]),
+    "spk_state_fresh": (C.c_int, [C.c_int64, _P, _P]),
+    "spk_shard_resolve": (C.c_int, [_G, _P, C.c_int, _P, _P, C.c_int32, _P, _P, _P]),
+    "spk_shard_junction": (C.c_int, [_G, C.c_int, _P, _P, _P, C.c_int32, _P, _P, C.c_int64, _P, _P,
+                                     _P, _P, _P, _P, _P, _P, _P]),
+    "spk_shard_close_chain": (C.c_int, [C.c_int64, _P, _P, C.c_int32, _P, _P]),
+    "spk_shard_stitch": (C.c_int, [_G, C.c_int, _P, _P, _P, C.c_int32, _P, _P, C.c_int64, _P, _P, _P,
+                                   _P, _P, _P, _P, C.c_int64, _P, _P, _P]),
+    "spk_expand_runs_u8": (C.c_int, [_G, _P, C.c_int64, _P, _P, _P, C.c_size_t, _P]),
+    "spk_expand_runs_f32": (C.c_int, [_G, _P, C.c_int64, _P, _P, _P, C.c_size_t, _P]),
+    "spk_expand_runs_f64": (C.c_int, [_G, _P, C.c_int64, _P, _P, _P, C.c_size_t, _P]),
     "spk_set_run_capacity": (C.c_int, [C.c_int64]),
     "spk_plane_pitch": (C.c_size_t, [C.c_int32, C.c_int32]),
     "spk_launch_count": (C.c_int64, [C.c_int]),

@@ -383,9 +383,54 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
     return SPK_OK;
 }
 
+template <typename OUT>
+int expand_runs_impl(const spk_geom* g, const spk_run* runs, int64_t cap, const uint32_t* counts,
+                     const int32_t* last, OUT* out, size_t out_pitch, void* stream) {
+    int rc = check_geom(g, false);
+    if (rc) return rc;
+    const int64_t npix = npix_of(g);
+    if (g->frames == 0) return SPK_OK;
+    if (cap < 1 || cap > INT_MAX) return fail(SPK_EINVAL, "spk_expand_runs: bad run_cap");
+    if (!runs || !counts || !last || !out) return fail(SPK_EINVAL, "spk: null device buffer");
+    if (out_pitch < (size_t)npix) return fail(SPK_EINVAL, "spk: out_pitch must be >= W*H");
+    cudaStream_t s = as_stream(stream);
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    SegArgs a;
+    a.planes = nullptr;
+    a.pitch = 0;
+    a.npix = npix;
+    a.frames = (int)g->frames;
+    a.cap = (int)cap;
+    a.nchunks = (int)((g->frames + kChunk - 1) / kChunk);
+    a.runs = const_cast<spk_run*>(runs);
+    a.counts = const_cast<uint32_t*>(counts);
+    a.last = const_cast<int32_t*>(last);
+    ExpandWork<OUT> w(s);
+    if ((rc = prepare_expand<OUT>(a, w, s))) return rc;
+    return launch_expand<OUT>(a, w, out, out_pitch, s);
+}
+
 }  // namespace
 
 extern "C" {
+
+int spk_expand_runs_u8(const spk_geom* g, const spk_run* d_runs, int64_t run_cap,
+                       const uint32_t* d_counts, const int32_t* d_last, uint8_t* d_out,
+                       size_t out_pitch, void* stream) {
+    return expand_runs_impl<uint8_t>(g, d_runs, run_cap, d_counts, d_last, d_out, out_pitch, stream);
+}
+int spk_expand_runs_f32(const spk_geom* g, const spk_run* d_runs, int64_t run_cap,
+                        const uint32_t* d_counts, const int32_t* d_last, float* d_out,
+                        size_t out_pitch, void* stream) {
+    return expand_runs_impl<float>(g, d_runs, run_cap, d_counts, d_last, d_out, out_pitch, stream);
+}
+int spk_expand_runs_f64(const spk_geom* g, const spk_run* d_runs, int64_t run_cap,
+                        const uint32_t* d_counts, const int32_t* d_last, double* d_out,
+                        size_t out_pitch, void* stream) {
+    return expand_runs_impl<double>(g, d_runs, run_cap, d_counts, d_last, d_out, out_pitch, stream);
+}
 
 int spk_reconstruct_u8(const spk_geom* g, const void* d_planes, int method, int tfp_window,
                        uint8_t* d_out, size_t out_pitch, void* stream) {
@@ -432,6 +477,170 @@ int spk_segment(const spk_geom* g, const void* d_planes, int method, spk_run* d_
     a.counts = d_counts;
     a.last = d_last;
     return launch_segment(method, a, s);
+}
+
+int spk_segment_state(const spk_geom* g, const void* d_planes, int method, spk_run* d_runs,
+                      int64_t run_cap, uint32_t* d_counts, int32_t* d_last,
+                      const int32_t* d_state_in, int32_t* d_state_out, void* stream) {
+    int rc = check_geom(g, true);
+    if (rc) return rc;
+    if (method != SPK_FSR && method != SPK_SSR)
+        return fail(SPK_EINVAL, "spk_segment: method must be fsr or ssr");
+    if (run_cap < 1 || run_cap > INT_MAX) return fail(SPK_EINVAL, "spk_segment: bad run_cap");
+    if (!d_runs || !d_counts || !d_last || (g->frames > 0 && !d_planes))
+        return fail(SPK_EINVAL, "spk: null device buffer");
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    SegArgs a;
+    a.planes = d_planes;
+    a.pitch = g->plane_pitch;
+    a.npix = npix_of(g);
+    a.frames = (int)g->frames;
+    a.cap = (int)run_cap;
+    a.nchunks = (int)((g->frames + kChunk - 1) / kChunk);
+    a.runs = d_runs;
+    a.counts = d_counts;
+    a.last = d_last;
+    a.state_in = d_state_in;
+    a.state_out = d_state_out;
+    return launch_segment(method, a, as_stream(stream));
+}
+
+namespace {
+
+ShardArgs shard_args(const spk_geom* g, const void* planes, const int32_t* entry, const spk_sync* sync,
+                     const spk_run* prefix, int32_t pcap, const int32_t* tstate) {
+    ShardArgs a{};
+    a.planes = planes;
+    a.pitch = g->plane_pitch;
+    a.npix = npix_of(g);
+    a.frames = (int)g->frames;
+    a.entry = entry;
+    a.prefix = const_cast<spk_run*>(prefix);
+    a.pcap = pcap;
+    a.sync = const_cast<spk_sync*>(sync);
+    a.tstate = const_cast<int32_t*>(tstate);
+    return a;
+}
+
+int check_shard(const spk_geom* g, int method, int32_t pcap) {
+    int rc = check_geom(g, false);
+    if (rc) return rc;
+    if (method != SPK_FSR && method != SPK_SSR)
+        return fail(SPK_EINVAL, "spk_shard: method must be fsr or ssr");
+    if (pcap < 1) return fail(SPK_EINVAL, "spk_shard: prefix_cap must be >= 1");
+    return SPK_OK;
+}
+
+}  // namespace
+
+int spk_shard_resolve(const spk_geom* g, const void* d_planes, int method, const int32_t* d_entry,
+                      spk_run* d_prefix, int32_t prefix_cap, spk_sync* d_sync, int32_t* d_tstate,
+                      void* stream) {
+    int rc = check_shard(g, method, prefix_cap);
+    if (rc) return rc;
+    if ((rc = check_geom(g, true))) return rc;
+    if (!d_entry || !d_prefix || !d_sync || !d_tstate || (g->frames > 0 && !d_planes))
+        return fail(SPK_EINVAL, "spk: null device buffer");
+    ShardArgs a = shard_args(g, d_planes, d_entry, d_sync, d_prefix, prefix_cap, d_tstate);
+    const int64_t threads = (a.npix + 31) / 32 * 32;
+    const unsigned blocks = (unsigned)((threads + 63) / 64);
+    cudaStream_t s = as_stream(stream);
+    if (method == SPK_FSR)
+        k_resolve<kFSR><<<blocks, 64, 0, s>>>(a);
+    else
+        k_resolve<kSSR><<<blocks, 64, 0, s>>>(a);
+    SPK_LAUNCHED("k_resolve");
+    return SPK_OK;
+}
+
+int spk_shard_junction(const spk_geom* g, int method, const int32_t* d_entry, const spk_sync* d_sync,
+                       const spk_run* d_prefix, int32_t prefix_cap, const int32_t* d_tstate,
+                       const spk_run* d_spec, int64_t spec_cap, const uint32_t* d_spec_counts,
+                       const int32_t* d_spec_state, const spk_run* d_fb, const uint32_t* d_fb_counts,
+                       const int32_t* d_fb_state, int32_t* d_exit_state, spk_close* d_entry_close,
+                       spk_close* d_tail_close, void* stream) {
+    int rc = check_shard(g, method, prefix_cap);
+    if (rc) return rc;
+    if (spec_cap < 1 || spec_cap > INT_MAX) return fail(SPK_EINVAL, "spk_shard: bad spec_cap");
+    if (!d_entry || !d_sync || !d_prefix || !d_tstate || !d_spec || !d_spec_counts || !d_spec_state ||
+        !d_exit_state || !d_entry_close || !d_tail_close)
+        return fail(SPK_EINVAL, "spk: null device buffer");
+    ShardArgs a = shard_args(g, nullptr, d_entry, d_sync, d_prefix, prefix_cap, d_tstate);
+    a.spec = d_spec;
+    a.scap = (int)spec_cap;
+    a.scount = d_spec_counts;
+    a.sstate = d_spec_state;
+    a.fb = d_fb;
+    a.fbcount = d_fb_counts;
+    a.fbstate = d_fb_state;
+    a.exit_state = d_exit_state;
+    a.entry_close = d_entry_close;
+    a.tail_close = d_tail_close;
+    const unsigned blocks = (unsigned)((a.npix + 127) / 128);
+    cudaStream_t s = as_stream(stream);
+    if (method == SPK_FSR)
+        k_junction<kFSR><<<blocks, 128, 0, s>>>(a);
+    else
+        k_junction<kSSR><<<blocks, 128, 0, s>>>(a);
+    SPK_LAUNCHED("k_junction");
+    return SPK_OK;
+}
+
+int spk_state_fresh(int64_t npix, int32_t* d_state, void* stream) {
+    if (npix < 1 || !d_state) return fail(SPK_EINVAL, "spk_state_fresh: bad arguments");
+    k_state_fresh<<<(unsigned)((npix + 255) / 256), 256, 0, as_stream(stream)>>>(d_state, npix);
+    SPK_LAUNCHED("k_state_fresh");
+    return SPK_OK;
+}
+
+int spk_shard_close_chain(int64_t npix, const spk_close* d_entry_close_next,
+                          const spk_close* d_close_next, int32_t shard_len, spk_close* d_close,
+                          void* stream) {
+    if (npix < 1 || !d_entry_close_next || !d_close_next || !d_close)
+        return fail(SPK_EINVAL, "spk_shard_close_chain: bad arguments");
+    k_close_chain<<<(unsigned)((npix + 255) / 256), 256, 0, as_stream(stream)>>>(
+        d_entry_close_next, d_close_next, shard_len, npix, d_close);
+    SPK_LAUNCHED("k_close_chain");
+    return SPK_OK;
+}
+
+int spk_shard_stitch(const spk_geom* g, int method, const int32_t* d_entry, const spk_sync* d_sync,
+                     const spk_run* d_prefix, int32_t prefix_cap, const int32_t* d_tstate,
+                     const spk_run* d_spec, int64_t spec_cap, const uint32_t* d_spec_counts,
+                     const int32_t* d_spec_state, const spk_run* d_fb, const uint32_t* d_fb_counts,
+                     const int32_t* d_fb_state, const spk_close* d_close, spk_run* d_region,
+                     int64_t region_cap, uint32_t* d_region_counts, int32_t* d_region_last,
+                     void* stream) {
+    int rc = check_shard(g, method, prefix_cap);
+    if (rc) return rc;
+    if (spec_cap < 1 || spec_cap > INT_MAX || region_cap < 1 || region_cap > INT_MAX)
+        return fail(SPK_EINVAL, "spk_shard: bad capacity");
+    if (!d_entry || !d_sync || !d_prefix || !d_tstate || !d_spec || !d_spec_counts || !d_spec_state ||
+        !d_close || !d_region || !d_region_counts || !d_region_last)
+        return fail(SPK_EINVAL, "spk: null device buffer");
+    ShardArgs a = shard_args(g, nullptr, d_entry, d_sync, d_prefix, prefix_cap, d_tstate);
+    a.spec = d_spec;
+    a.scap = (int)spec_cap;
+    a.scount = d_spec_counts;
+    a.sstate = d_spec_state;
+    a.fb = d_fb;
+    a.fbcount = d_fb_counts;
+    a.fbstate = d_fb_state;
+    a.close = d_close;
+    a.region = d_region;
+    a.rcap = (int)region_cap;
+    a.rcount = d_region_counts;
+    a.rlast = d_region_last;
+    const unsigned blocks = (unsigned)((a.npix + 127) / 128);
+    cudaStream_t s = as_stream(stream);
+    if (method == SPK_FSR)
+        k_stitch<kFSR><<<blocks, 128, 0, s>>>(a);
+    else
+        k_stitch<kSSR><<<blocks, 128, 0, s>>>(a);
+    SPK_LAUNCHED("k_stitch");
+    return SPK_OK;
 }
 
 int spk_pack_bytes(const spk_geom* g, const uint8_t* d_bytes, void* d_planes, void* stream) {

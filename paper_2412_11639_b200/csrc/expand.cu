@@ -67,7 +67,8 @@ __global__ void __launch_bounds__(kFinWarps * 32, 2) k_fin_bins(FinArgs a) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int k = b + 32 * u + lane;
-                sv[u] = k < n ? rp[k].start : 0xffffffffu;
+                // a run started before frame 0 (time shards) changes the value at frame 0
+                sv[u] = k < n ? (uint32_t)max((int)rp[k].start, 0) : 0xffffffffu;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -119,7 +120,7 @@ __global__ void __launch_bounds__(256) k_fin_scatter(FinArgs a) {
 #pragma unroll
         for (int j = 0; j < B; ++j) {
             if (k0 + j < n) {
-                const int st = (int)r[j].start;
+                const int st = max((int)r[j].start, 0);  // see K2b: starts before frame 0
                 const int c = st >> kChunkLog2;
                 const int bi = (st & (kChunk - 1)) / kSub;
                 pos[j] = atomicAdd(&a.cursor[((int64_t)c * a.ngroups + g) * kBins + bi], 1u);
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(256) k_fin_scatter(FinArgs a) {
 #pragma unroll
         for (int j = 0; j < B; ++j) {
             if (k0 + j < n) {
-                const int st = (int)r[j].start;
+                const int st = max((int)r[j].start, 0);
                 const uint32_t fo = (uint32_t)(st & (kChunk - 1));
                 const OUT val = over ? OUT(0) : OutVal<OUT>::run(r[j].intervals, r[j + 1].start - r[j].start);
                 Change<OUT> ch;
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(256) k_fin_scatter(FinArgs a) {
                 }
                 stp[pos[j]] = ch;
                 if (!over) {  // chunk starts in [start, next start); the last run covers the tail
-                    const int64_t hi = k0 + j + 1 < n ? (int64_t)r[j + 1].start : total_frames;
+                    const int64_t hi = k0 + j + 1 < n ? (int64_t)(int)r[j + 1].start : total_frames;
                     for (int64_t cc = ((int64_t)st + kChunk - 1) >> kChunkLog2; cc <= (hi - 1) >> kChunkLog2; ++cc)
                         tb[cc * a.npix + p] = val;
                 }

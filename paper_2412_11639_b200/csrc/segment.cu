@@ -55,6 +55,10 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
 
     Scan<METHOD> sc;
     sc.init();
+    if (a.state_in != nullptr && valid) {  // time shard: continue from a carried state
+        sc.restore(a.state_in, a.npix, p);
+        sc.nrun = 0;
+    }
     int nrun = 0;
     // runs beyond the capacity are counted (overflow -> k_fixup) but not stored.
     // The stored pair lives in its own registers (written only on an emit), so
@@ -137,6 +141,7 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     }
     }
     if (valid) {
+        if (a.state_out != nullptr) sc.save(a.state_out, a.npix, p);
         int rs, cnt;
         const bool e = sc.tail(rs, cnt);
         emit(e, rs, cnt);

@@ -291,6 +291,54 @@ struct Scan {
         out_cnt = cnt;
         return lo < kLim;
     }
+
+    // ---- state carried across time shards (SoA: field f of pixel p at
+    // st[f * stride + p]; frames relative to the shard's first frame)
+    static constexpr int kFields = 14;
+    SPK_HD void save(int32_t* st, int64_t stride, int64_t p) const {
+        const int32_t v[kFields] = {last, lo, rs, cnt, nrun, (int32_t)hw, ii, sub0,
+                                    l0, l1, g0, g1, (int32_t)h0, (int32_t)h1};
+        for (int f = 0; f < kFields; ++f) st[f * stride + p] = v[f];
+    }
+    SPK_HD void restore(const int32_t* st, int64_t stride, int64_t p) {
+        last = st[0 * stride + p];
+        lo = st[1 * stride + p];
+        rs = st[2 * stride + p];
+        cnt = st[3 * stride + p];
+        nrun = st[4 * stride + p];
+        hw = (uint32_t)st[5 * stride + p];
+        ii = st[6 * stride + p];
+        sub0 = st[7 * stride + p];
+        l0 = st[8 * stride + p];
+        l1 = st[9 * stride + p];
+        g0 = st[10 * stride + p];
+        g1 = st[11 * stride + p];
+        h0 = (uint32_t)st[12 * stride + p];
+        h1 = (uint32_t)st[13 * stride + p];
+    }
+
+    // Same future: from here on both automata take identical decisions on any
+    // spike sequence (only the open run's bookkeeping rs / cnt may differ).
+    // Requires an interval in both (rs is the open run's start only then).
+    // FSR: the pair and the last spike; SSR also each parity slot's state,
+    // relative to the interval index: empty (stale), or (gap base, gap pair).
+    SPK_HD bool same_future(const Scan& o) const {
+        if ((lo >= kLim) | (o.lo >= kLim)) return false;
+        if ((lo != o.lo) | (hw != o.hw) | (last != o.last)) return false;
+        if (METHOD == kSSR) {
+            auto slot_eq = [&](int la, int ga, uint32_t ha, int lb, int gb, uint32_t hb) {
+                const bool sa = la < sub0, sb = lb < o.sub0;
+                if (sa != sb) return false;
+                if (sa) return true;
+                if (ii - la != o.ii - lb) return false;
+                const bool na = ga >= kLim, nb = gb >= kLim;
+                if (na != nb) return false;
+                return na || ((ga == gb) & (ha == hb));
+            };
+            return slot_eq(l0, g0, h0, o.l0, o.g0, o.h0) && slot_eq(l1, g1, h1, o.l1, o.g1, o.h1);
+        }
+        return true;
+    }
 };
 
 // ---- bit helpers usable on host and device (the host build backs the CPU tests)

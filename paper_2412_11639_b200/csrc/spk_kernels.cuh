@@ -10,6 +10,8 @@
 namespace spk {
 
 using spk_run_t = ::spk_run;
+using spk_sync_t = ::spk_sync;
+using spk_close_t = ::spk_close;
 
 constexpr int kSegThreads = 64;  // 2 warps: fine-grained blocks balance 148 SMs
 constexpr int kBatch = 8;        // 32-frame groups per prefetch batch
@@ -26,6 +28,38 @@ struct SegArgs {
     spk_run_t* runs;
     uint32_t* counts;
     int32_t* last;
+    const int32_t* state_in = nullptr;  // time shards: automaton state at frame 0
+    int32_t* state_out = nullptr;       //              state after the last frame
+};
+
+// ---- time shards (shard.cu): exact stitching of independently scanned
+// frame ranges, see DESIGN.md "Time sharding".
+struct ShardArgs {
+    const void* planes;  // this shard's planes (frame 0 = shard start)
+    size_t pitch;
+    int64_t npix;
+    int frames;                 // shard length
+    const int32_t* entry;       // true automaton state at the shard start
+    spk_run_t* prefix;          // true runs closed before the sync point
+    int pcap;
+    spk_sync_t* sync;
+    int32_t* tstate;            // true end state when the scan ran through the shard
+    // junction / stitch
+    const spk_run_t* spec;      // speculative run list (fresh at the shard start)
+    int scap;
+    const uint32_t* scount;
+    const int32_t* sstate;      // speculative end state
+    const spk_run_t* fb;        // fallback: full re-scan from `entry` (or null)
+    const uint32_t* fbcount;
+    const int32_t* fbstate;
+    int32_t* exit_state;        // true end state, frames relative to the next shard
+    spk_close_t* entry_close;   // does the run open at the shard start close here?
+    spk_close_t* tail_close;    // the run open at the end, closed at the stream end
+    const spk_close_t* close;   // close of the run open at the end (from the right)
+    spk_run_t* region;          // stitched true runs intersecting the shard
+    int rcap;
+    uint32_t* rcount;
+    int32_t* rlast;             // end of the last region run (may lie past the shard)
 };
 
 // Geometry of the expand stage per output type: a warp owns a group of
@@ -126,6 +160,15 @@ struct RecArgs {
 
 template <int METHOD>
 __global__ void k_segment(SegArgs a);
+template <int METHOD>
+__global__ void k_resolve(ShardArgs a);
+template <int METHOD>
+__global__ void k_junction(ShardArgs a);
+__global__ void k_state_fresh(int32_t* st, int64_t npix);
+__global__ void k_close_chain(const spk_close_t* entry_next, const spk_close_t* close_next,
+                              int shard_len, int64_t npix, spk_close_t* close);
+template <int METHOD>
+__global__ void k_stitch(ShardArgs a);
 template <int METHOD>
 __global__ void k_rec_count(RecArgs a);
 template <int METHOD>

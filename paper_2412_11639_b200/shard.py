@@ -22,7 +22,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from .recon import PackedVolume, reconstruct
+from .recon import Method, PackedVolume, reconstruct
 
 BAND_ALIGN = 128
 
@@ -101,3 +101,217 @@ def reconstruct_sharded(volume: PackedVolume, method="fsr", group=None,
         return p0, p1, local[:, : p1 - p0]
     full = gather_bands(local, volume.npix, group)
     return full.view(volume.frames, volume.height, volume.width)
+
+
+# ------------------------------------------------------------ time shards --
+# One long stream cut in frame ranges (BASELINE configs[4]): exact, see
+# csrc/shard.cu and DESIGN.md "Time sharding".  `TimeShard` holds one shard's
+# device buffers; the driver below runs all shards of a volume in one process
+# (one GPU); reconstruct_time_sharded_dist runs one shard per rank.
+
+STATE_FIELDS = 14
+SYNC_DT = 4   # spk_sync: 4 x int32
+CLOSE_DT = 8  # spk_close: 8 x int32
+
+
+def _ptr(t):
+    return t.data_ptr() if t is not None else None
+
+
+class TimeShard:
+    """Frames [f0, f1) of a volume: speculative scan, then resolve / junction /
+    stitch / expand through the C-ABI (all asynchronous on `stream`)."""
+
+    def __init__(self, volume: PackedVolume, f0: int, f1: int, method, prefix_cap: int = 64,
+                 stream=None):
+        from .recon import _method, _stream
+        from . import _capi as capi
+        self.capi, self.lib = capi, capi.lib()
+        m = _method(method)
+        if m.kind not in (Method.fsr, Method.ssr):
+            raise ValueError("time sharding applies to fsr / ssr")
+        self.kind = int(m.kind)
+        self.vol = volume
+        self.f0, self.f1 = f0, f1
+        self.frames = f1 - f0
+        self.npix = volume.npix
+        self.dev = volume.planes.device
+        self.planes = volume.planes[f0:f1]
+        self.stream = _stream(stream)
+        self.pcap = int(prefix_cap)
+        self.g = capi.geom(volume.width, volume.height, self.frames, volume.pitch)
+        i32 = dict(dtype=torch.int32, device=self.dev)
+        self.prefix = torch.empty((self.npix, self.pcap, 2), **i32)
+        self.sync = torch.empty((self.npix, SYNC_DT), **i32)
+        self.tstate = torch.empty((STATE_FIELDS, self.npix), **i32)
+        self.exit_state = torch.empty((STATE_FIELDS, self.npix), **i32)
+        self.entry_close = torch.empty((self.npix, CLOSE_DT), **i32)
+        self.tail_close = torch.empty((self.npix, CLOSE_DT), **i32)
+        self.fb = self.fb_counts = self.fb_state = None
+
+    def _segment(self, state_in):
+        """runs of this shard from `state_in` (None = fresh), capacity grown
+        until no pixel overflows"""
+        cap = max(64, self.frames // 32)
+        i32 = dict(dtype=torch.int32, device=self.dev)
+        while True:
+            runs = torch.empty((self.npix, cap, 2), **i32)
+            counts = torch.empty((self.npix,), **i32)
+            last = torch.empty((self.npix,), **i32)
+            state = torch.empty((STATE_FIELDS, self.npix), **i32)
+            self.capi.check(self.lib.spk_segment_state(
+                self.g, _ptr(self.planes) if self.frames else None, self.kind, _ptr(runs), cap,
+                _ptr(counts), _ptr(last), _ptr(state_in), _ptr(state), self.stream))
+            need = int(counts.max().item()) if self.npix else 0
+            if need <= cap:
+                return runs, counts, last, state, cap
+            cap = need
+
+    def speculate(self):
+        self.spec, self.spec_counts, _, self.spec_state, self.scap = self._segment(None)
+
+    def fresh_entry(self) -> torch.Tensor:
+        """entry state of the first shard (start of the stream)"""
+        return fresh_state(self.npix, self.dev, self.stream)
+
+    def resolve(self, entry: torch.Tensor):
+        """true entry state -> sync records, exit state, entry / tail closes"""
+        self.entry = entry
+        self.capi.check(self.lib.spk_shard_resolve(
+            self.g, _ptr(self.planes) if self.frames else None, self.kind, _ptr(entry),
+            _ptr(self.prefix), self.pcap, _ptr(self.sync), _ptr(self.tstate), self.stream))
+        if bool((self.sync[:, 3] == -1).any().item()):  # a prefix overflowed: full re-scan
+            self.fb, self.fb_counts, _, self.fb_state, fbcap = self._segment(entry)
+            if fbcap != self.scap:  # keep one capacity for both lists
+                pad = torch.empty((self.npix, max(fbcap, self.scap), 2), dtype=torch.int32,
+                                  device=self.dev)
+                if fbcap < self.scap:
+                    pad[:, :fbcap] = self.fb
+                    self.fb = pad
+                else:
+                    pad[:, :self.scap] = self.spec
+                    self.spec = pad
+                    self.scap = fbcap
+        self.capi.check(self.lib.spk_shard_junction(
+            self.g, self.kind, _ptr(entry), _ptr(self.sync), _ptr(self.prefix), self.pcap,
+            _ptr(self.tstate), _ptr(self.spec), self.scap, _ptr(self.spec_counts),
+            _ptr(self.spec_state), _ptr(self.fb), _ptr(self.fb_counts), _ptr(self.fb_state),
+            _ptr(self.exit_state), _ptr(self.entry_close), _ptr(self.tail_close), self.stream))
+        return self.exit_state
+
+    def close_from_next(self, entry_close_next, close_next):
+        close = torch.empty((self.npix, CLOSE_DT), dtype=torch.int32, device=self.dev)
+        self.capi.check(self.lib.spk_shard_close_chain(
+            self.npix, _ptr(entry_close_next), _ptr(close_next), self.frames, _ptr(close),
+            self.stream))
+        return close
+
+    def stitch(self, close: torch.Tensor):
+        rcap = self.scap + self.pcap + 1
+        i32 = dict(dtype=torch.int32, device=self.dev)
+        self.region = torch.empty((self.npix, rcap, 2), **i32)
+        self.region_counts = torch.empty((self.npix,), **i32)
+        self.region_last = torch.empty((self.npix,), **i32)
+        self.rcap = rcap
+        self.capi.check(self.lib.spk_shard_stitch(
+            self.g, self.kind, _ptr(self.entry), _ptr(self.sync), _ptr(self.prefix), self.pcap,
+            _ptr(self.tstate), _ptr(self.spec), self.scap, _ptr(self.spec_counts),
+            _ptr(self.spec_state), _ptr(self.fb), _ptr(self.fb_counts), _ptr(self.fb_state),
+            _ptr(close), _ptr(self.region), rcap, _ptr(self.region_counts),
+            _ptr(self.region_last), self.stream))
+
+    def expand(self, out: torch.Tensor):
+        """this shard's frames into `out` ([frames, >= W*H], row-major)"""
+        fn = {torch.uint8: "spk_expand_runs_u8", torch.float32: "spk_expand_runs_f32",
+              torch.float64: "spk_expand_runs_f64"}[out.dtype]
+        g = self.capi.geom(self.vol.width, self.vol.height, self.frames, 0)
+        self.capi.check(getattr(self.lib, fn)(
+            g, _ptr(self.region), self.rcap, _ptr(self.region_counts), _ptr(self.region_last),
+            _ptr(out), out.stride(0), self.stream))
+
+
+def fresh_state(npix: int, device, stream=None) -> torch.Tensor:
+    from .recon import _stream
+    from . import _capi as capi
+    st = torch.empty((STATE_FIELDS, npix), dtype=torch.int32, device=device)
+    capi.check(capi.lib().spk_state_fresh(npix, st.data_ptr(), _stream(stream)))
+    return st
+
+
+def time_bounds(frames: int, nshards: int) -> list[int]:
+    """[0 = a_0 < a_1 < ... < a_K = frames], shard lengths multiples of 32 frames"""
+    words = (frames + 31) // 32
+    b = [min(frames, (words * r // nshards) * 32) for r in range(nshards + 1)]
+    b[-1] = frames
+    return sorted(set(b))
+
+
+def reconstruct_time_sharded(volume: PackedVolume, method="fsr", nshards: int = 2,
+                             bounds: list[int] | None = None, dtype: torch.dtype = torch.uint8,
+                             prefix_cap: int = 64, out: torch.Tensor | None = None, stream=None):
+    """reconstruct() of one volume cut into time shards processed independently
+    (one GPU, all shards in this process); bit-identical to reconstruct()."""
+    bounds = bounds or time_bounds(volume.frames, nshards)
+    if bounds[0] != 0 or bounds[-1] != volume.frames or any(b1 <= b0 for b0, b1 in zip(bounds, bounds[1:])):
+        raise ValueError("bounds must increase strictly from 0 to the frame count")
+    if out is None:
+        out = torch.empty((volume.frames, volume.npix), dtype=dtype, device=volume.planes.device)
+    with torch.cuda.device(volume.planes.device):
+        shards = [TimeShard(volume, b0, b1, method, prefix_cap, stream)
+                  for b0, b1 in zip(bounds, bounds[1:])]
+        for sh in shards:                      # independent: the speculative scans
+            sh.speculate()
+        entry = fresh_state(volume.npix, volume.planes.device, stream)
+        for sh in shards:                      # forward: true entry states
+            entry = sh.resolve(entry)
+        close = shards[-1].tail_close          # backward: closes of crossing runs
+        closes = [None] * len(shards)
+        closes[-1] = close
+        for r in range(len(shards) - 2, -1, -1):
+            closes[r] = shards[r].close_from_next(shards[r + 1].entry_close, closes[r + 1])
+        for sh, c in zip(shards, closes):      # independent: stitch + frames
+            sh.stitch(c)
+            sh.expand(out[sh.f0:sh.f1])
+    return out.view(volume.frames, volume.height, volume.width)
+
+
+def reconstruct_time_sharded_dist(shard: PackedVolume, method="fsr", group=None,
+                                  dtype: torch.dtype = torch.uint8, prefix_cap: int = 64,
+                                  out: torch.Tensor | None = None, stream=None,
+                                  shard_type=TimeShard):
+    """One time shard per rank (rank r holds frames [a_r, a_{r+1}) of the
+    stream as `shard`, ranks in time order): returns this rank's frames,
+    identical to the same frames of a single-pass reconstruct().
+
+    Data path: none; the only exchange is O(W*H) per boundary -- the true
+    automaton state forward (rank r -> r+1, 56 B/px) and the close records of
+    boundary-crossing runs backward (rank r+1 -> r, 2 x 32 B/px)."""
+    rank, world = _group_info(group)
+    peer = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
+    if out is None:
+        out = torch.empty((shard.frames, shard.npix), dtype=dtype, device=shard.planes.device)
+    sh = shard_type(shard, 0, shard.frames, method, prefix_cap, stream)
+    sh.speculate()                              # independent on every rank
+    if rank == 0:
+        entry = sh.fresh_entry()
+    else:                                       # forward: true entry state
+        entry = torch.empty((STATE_FIELDS, shard.npix), dtype=torch.int32,
+                            device=shard.planes.device)
+        dist.recv(entry, src=peer(rank - 1), group=group)
+    exit_state = sh.resolve(entry)
+    if rank + 1 < world:
+        dist.send(exit_state, dst=peer(rank + 1), group=group)
+    if rank + 1 == world:                       # backward: closes of crossing runs
+        close = sh.tail_close
+    else:
+        ec_next = torch.empty((shard.npix, CLOSE_DT), dtype=torch.int32, device=shard.planes.device)
+        close_next = torch.empty_like(ec_next)
+        dist.recv(ec_next, src=peer(rank + 1), group=group)
+        dist.recv(close_next, src=peer(rank + 1), group=group)
+        close = sh.close_from_next(ec_next, close_next)
+    if rank > 0:
+        dist.send(sh.entry_close, dst=peer(rank - 1), group=group)
+        dist.send(close, dst=peer(rank - 1), group=group)
+    sh.stitch(close)                            # independent: stitch + frames
+    sh.expand(out)
+    return out

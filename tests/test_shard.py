@@ -133,3 +133,71 @@ def test_bands_assemble_to_single_gpu(oracle, geom, method):
             assert torch.equal(full, ref), (world, dtype)
         one = reconstruct_sharded(vol, method, dtype=dtype)  # no process group: world 1
         assert torch.equal(one.reshape(t, -1), ref)
+
+
+# ---- time shards across ranks: the exchange schedule (gloo, CPU) ----------
+class _FakeTimeShard:
+    """Stands in for TimeShard's device work so the rank-to-rank protocol can
+    run on CPU: every tensor a rank produces encodes who made it."""
+
+    def __init__(self, vol, f0, f1, method, pcap, stream):
+        self.npix = vol.npix
+        self.rank = dist.get_rank()
+        self.tail_close = torch.full((self.npix, 8), 1000 + self.rank, dtype=torch.int32)
+        self.entry_close = torch.full((self.npix, 8), 2000 + self.rank, dtype=torch.int32)
+
+    def speculate(self):
+        pass
+
+    def fresh_entry(self):
+        return torch.zeros((14, self.npix), dtype=torch.int32)
+
+    def resolve(self, entry):
+        self.entry = entry.clone()
+        return entry + (self.rank + 1)  # exit state = entry state "advanced" by this shard
+
+    def close_from_next(self, ec_next, close_next):
+        return ec_next * 10000 + close_next
+
+    def stitch(self, close):
+        self.close = close.clone()
+
+    def expand(self, out):
+        out[0, :] = self.entry[0, 0]
+        out[1, :] = self.close[0, 0] % 1000003
+
+
+def _timeshard_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2412_11639_b200.shard import reconstruct_time_sharded_dist
+        vol = PackedVolume(4, 2, 5, torch.zeros((5, 16), dtype=torch.uint8))
+        out = torch.zeros((5, 8), dtype=torch.int64)
+        reconstruct_time_sharded_dist(vol, "fsr", out=out, shard_type=_FakeTimeShard)
+        q.put((rank, int(out[0, 0]), int(out[1, 0])))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_time_shard_exchange_gloo_world3():
+    """forward: rank r's entry = exit of rank r-1 (state advanced by every
+    earlier shard); backward: rank r's close combines rank r+1's entry close and
+    close record, recursively from the last rank's tail close."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_timeshard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    got = {r: (e, c) for r, e, c in (q.get(timeout=5) for _ in range(world))}
+    closes = {world - 1: 1000 + world - 1}
+    for r in range(world - 2, -1, -1):
+        closes[r] = (2000 + r + 1) * 10000 + closes[r + 1]
+    for r in range(world):
+        assert got[r][0] == sum(i + 1 for i in range(r)), (r, got[r])
+        assert got[r][1] == closes[r] % 1000003, (r, got[r])
