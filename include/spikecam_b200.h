@@ -150,8 +150,9 @@ int spk_segment_state(const spk_geom* g, const void* d_planes, int method, spk_r
 /* the automaton state at the start of a stream (entry of the first shard) */
 int spk_state_fresh(int64_t npix, int32_t* d_state, void* stream);
 int spk_shard_resolve(const spk_geom* g, const void* d_planes, int method, const int32_t* d_entry,
-                      spk_run* d_prefix, int32_t prefix_cap, spk_sync* d_sync, int32_t* d_tstate,
-                      void* stream);
+                      const spk_run* d_spec, int64_t spec_cap, const uint32_t* d_spec_counts,
+                      const int32_t* d_spec_state, spk_run* d_prefix, int32_t prefix_cap,
+                      spk_sync* d_sync, int32_t* d_tstate, void* stream);
 int spk_shard_junction(const spk_geom* g, int method, const int32_t* d_entry, const spk_sync* d_sync,
                        const spk_run* d_prefix, int32_t prefix_cap, const int32_t* d_tstate,
                        const spk_run* d_spec, int64_t spec_cap, const uint32_t* d_spec_counts,

@@ -47,7 +47,8 @@ SIGNATURES = {
     "spk_free_host": (None, [_P]),
     "spk_segment_state": (C.c_int, [_G, _P, C.c_int, _P, C.c_int64, _P, _P, _P, _P, _P]),
     "spk_state_fresh": (C.c_int, [C.c_int64, _P, _P]),
-    "spk_shard_resolve": (C.c_int, [_G, _P, C.c_int, _P, _P, C.c_int32, _P, _P, _P]),
+    "spk_shard_resolve": (C.c_int, [_G, _P, C.c_int, _P, _P, C.c_int64, _P, _P, _P, C.c_int32, _P,
+                                    _P, _P]),
     "spk_shard_junction": (C.c_int, [_G, C.c_int, _P, _P, _P, C.c_int32, _P, _P, C.c_int64, _P, _P,
                                      _P, _P, _P, _P, _P, _P, _P]),
     "spk_shard_close_chain": (C.c_int, [C.c_int64, _P, _P, C.c_int32, _P, _P]),

@@ -152,10 +152,14 @@ int launch_segment(int method, const SegArgs& a, cudaStream_t s) {
     const int64_t nwords = (a.npix + 31) / 32;
     const int64_t threads = nwords * 32;
     const unsigned blocks = (unsigned)((threads + kSegThreads - 1) / kSegThreads);
-    if (method == SPK_FSR)
-        k_segment<kFSR><<<blocks, kSegThreads, 0, s>>>(a);
-    else
-        k_segment<kSSR><<<blocks, kSegThreads, 0, s>>>(a);
+    const size_t smem = (size_t)kSegWarps * kRing * 32 * sizeof(uint32_t);  // the warps' rings
+    auto go = [&](auto kern) -> int {
+        SPK_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<blocks, kSegThreads, smem, s>>>(a);
+        return SPK_OK;
+    };
+    int rc = method == SPK_FSR ? go(k_segment<kFSR>) : go(k_segment<kSSR>);
+    if (rc) return rc;
     SPK_LAUNCHED("k_segment");
     return SPK_OK;
 }
@@ -536,14 +540,21 @@ int check_shard(const spk_geom* g, int method, int32_t pcap) {
 }  // namespace
 
 int spk_shard_resolve(const spk_geom* g, const void* d_planes, int method, const int32_t* d_entry,
-                      spk_run* d_prefix, int32_t prefix_cap, spk_sync* d_sync, int32_t* d_tstate,
-                      void* stream) {
+                      const spk_run* d_spec, int64_t spec_cap, const uint32_t* d_spec_counts,
+                      const int32_t* d_spec_state, spk_run* d_prefix, int32_t prefix_cap,
+                      spk_sync* d_sync, int32_t* d_tstate, void* stream) {
     int rc = check_shard(g, method, prefix_cap);
     if (rc) return rc;
     if ((rc = check_geom(g, true))) return rc;
     if (!d_entry || !d_prefix || !d_sync || !d_tstate || (g->frames > 0 && !d_planes))
         return fail(SPK_EINVAL, "spk: null device buffer");
+    if (!d_spec || !d_spec_counts || !d_spec_state || spec_cap < 1 || spec_cap > INT_MAX)
+        return fail(SPK_EINVAL, "spk_shard_resolve: bad speculative lists");
     ShardArgs a = shard_args(g, d_planes, d_entry, d_sync, d_prefix, prefix_cap, d_tstate);
+    a.spec = d_spec;
+    a.scap = (int)spec_cap;
+    a.scount = d_spec_counts;
+    a.sstate = d_spec_state;
     const int64_t threads = (a.npix + 31) / 32 * 32;
     const unsigned blocks = (unsigned)((threads + 63) / 64);
     cudaStream_t s = as_stream(stream);

@@ -36,11 +36,29 @@ __device__ __forceinline__ void st_run_if(bool pred, spk_run_t* addr, int rs, in
 template <int METHOD>
 __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     // transposed words of each warp: ring of kRing 32-frame words per lane
-    __shared__ uint32_t ring[kSegThreads / 32][kRing][32];
+    extern __shared__ uint32_t seg_smem[];
+    __shared__ int prog[kSegWarps];  // per warp: earliest group still to be read
     const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
     const int64_t word = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (threadIdx.x < kSegWarps) {
+        const int64_t w = (int64_t)blockIdx.x * kSegWarps + threadIdx.x;
+        prog[threadIdx.x] = w * 32 < a.npix ? 0 : 0x7fffffff;  // warps without pixels never hold others back
+    }
+    __syncthreads();
     if (word * 32 >= a.npix) return;  // warp-uniform
-    uint32_t(*rg)[32] = ring[threadIdx.x >> 5];
+    uint32_t(*rg)[32] = reinterpret_cast<uint32_t(*)[32]>(seg_smem + (size_t)wid * kRing * 32);
+    volatile int* vprog = prog;
+    // stay within kDrift groups of the block's slowest warp (L2 sector sharing)
+    auto throttle = [&](int front) {
+        for (;;) {
+            int mn = 0x7fffffff;
+#pragma unroll
+            for (int i = 0; i < kSegWarps; ++i) mn = min(mn, vprog[i]);
+            if (front - mn <= kDrift) break;
+            __nanosleep(256);
+        }
+    };
     const int64_t p = word * 32 + lane;
     const bool valid = p < a.npix;
     const int frames = a.frames;
@@ -79,13 +97,17 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         nxt[j] = f < frames ? __ldg(reinterpret_cast<const uint32_t*>(col + (size_t)f * pitch)) : 0u;
     }
     int produced = 0;  // groups transposed into the ring
-    auto produce = [&]() {
+    // `lowest`: this warp's earliest group still to be read (published for the
+    // other warps of the block), then the next batch's loads wait for them
+    auto produce = [&](int lowest) {
+        if (lane == 0) vprog[wid] = lowest;
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
             const uint32_t w = transpose32(nxt[j], lane);
             rg[(produced + j) & (kRing - 1)][lane] = valid ? w : 0u;
         }
         produced += kBatch;
+        throttle(produced);
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
             const int f = (produced + j) * 32 + rev;
@@ -98,7 +120,7 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         // SSR: spike by spike, the warp in lockstep over words (the per-spike
         // step is long enough that independent progress does not pay off)
         for (int g0 = 0; g0 < ngroups; g0 += kBatch) {
-            produce();
+            produce(g0);
 #pragma unroll
             for (int j = 0; j < kBatch; ++j) {
                 if (g0 + j < ngroups) {
@@ -128,7 +150,7 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         // still read (lowest = the earliest window start)
         if (__any_sync(kFull, more & !ready)) {
             const int lowest = (int)__reduce_min_sync(kFull, (unsigned)(more ? wi : 0x7fffffff));
-            if (produced < ngroups && produced + kBatch <= lowest + kRing) produce();
+            if (produced < ngroups && produced + kBatch <= lowest + kRing) produce(lowest);
         }
         if (!__any_sync(kFull, more)) break;
         if (more & (min(wi + 4, ngroups) <= produced)) {
@@ -140,6 +162,7 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         }
     }
     }
+    if (lane == 0) vprog[wid] = 0x7fffffff;  // done: never hold the others back
     if (valid) {
         if (a.state_out != nullptr) sc.save(a.state_out, a.npix, p);
         int rs, cnt;

@@ -29,6 +29,54 @@
 
 namespace spk {
 
+namespace {
+
+// FSR shortcut: when the speculative scan had no break in the whole shard, the
+// shard's intervals all lie in its final pair, so the true automaton never
+// breaks either iff E's pair, the boundary-crossing interval and that pair fit
+// one pair {x, x+1} -- then its end state follows without a scan.  (Pixels
+// whose speculative pair never completes in a long shard would otherwise keep
+// their warp scanning to the shard end.)
+__device__ bool fsr_no_break(const ShardArgs& a, int64_t p, const Scan<kFSR>& E, Scan<kFSR>& X) {
+    if (a.scount[p] > 1u) return false;  // the speculative scan broke in the shard
+    Scan<kFSR> S;
+    S.restore(a.sstate, a.npix, p);
+    if (S.last == kNoSpike) {  // no spike in the shard
+        X = E;
+        return true;
+    }
+    if (E.last == kNoSpike) {  // nothing before: the true scan is the speculative one
+        X = S;
+        return true;
+    }
+    const bool hasS = S.lo < kLim;  // >= 2 spikes in the shard
+    const int f1 = hasS ? (int)a.spec[p * a.scap].start : S.last;
+    const int t0 = f1 - E.last;
+    int lo = t0, hi = t0;
+    if (E.lo < kLim) {
+        lo = min(lo, E.lo);
+        hi = max(hi, E.lo + (int)E.hw);
+    }
+    if (hasS) {
+        lo = min(lo, S.lo);
+        hi = max(hi, S.lo + (int)S.hw);
+    }
+    if (hi - lo > 1) return false;
+    X = E;
+    X.lo = lo;
+    X.hw = (uint32_t)(hi - lo);
+    if (E.lo >= kLim) {  // E held a lone spike: the run starts there
+        X.rs = E.last;
+        X.cnt = 1 + (hasS ? S.cnt : 0);
+    } else {
+        X.cnt = E.cnt + 1 + (hasS ? S.cnt : 0);
+    }
+    X.last = S.last;
+    return true;
+}
+
+}  // namespace
+
 // Thread per pixel in warp lockstep over 32-frame words: lanes load the
 // transposed words as K2 does and walk their spikes with both automata until
 // every lane of the warp has synced (or the shard ends).
@@ -54,16 +102,34 @@ __global__ void __launch_bounds__(64) k_resolve(ShardArgs a) {
     int m = 0;
     bool done = !valid;
     spk_sync_t out{0, 0, 0, -1};
+    if constexpr (METHOD == kFSR) {
+        Scan<kFSR> X;
+        if (valid && a.scount != nullptr && fsr_no_break(a, p, T, X)) {
+            T = X;  // reported below as "never synced, no closed run"
+            done = true;
+        }
+    }
     for (int g = 0; g < ngroups; ++g) {
         if (__all_sync(kFull, done)) break;
         const int f = g * 32 + rev;
         uint32_t w = f < a.frames ? __ldg(reinterpret_cast<const uint32_t*>(col + (size_t)f * a.pitch)) : 0u;
         w = transpose32(w, lane);
         if (done) continue;
+        const int base = g * 32;
+        const uint32_t wo = w;
         while (w) {
+            if constexpr (METHOD == kFSR) {
+                // both automata accept in bulk up to the next event of either
+                const uint32_t V = fsr_flags(T, wo, w, base) | fsr_flags(S, wo, w, base);
+                const uint32_t A = w & ~bit_shr_clamp(0xffffffffu, 0u, V ? (uint32_t)__clz(V) : 32u);
+                fsr_accept(T, A, base);
+                fsr_accept(S, A, base);
+                w &= ~A;
+                if (!w) break;
+            }
             const int c = __clz(w);
             w ^= 0x80000000u >> c;
-            const int n = g * 32 + c;
+            const int n = base + c;
             int rs, cnt;
             if (T.step(n, rs, cnt)) {
                 if (m < a.pcap) pre[m] = spk_run_t{(uint32_t)rs, (uint32_t)cnt};

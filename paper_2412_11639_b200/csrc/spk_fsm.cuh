@@ -497,6 +497,29 @@ SPK_HD int fsr_batch4(SC& sc, uint32_t W0, uint32_t W1, uint32_t W2, uint32_t W3
     return ev ? kk : 4;
 }
 
+// FSR: the remaining spikes S of word So (first frame in bit 31, frames
+// base..base+31) that the automaton would flag -- its next event is the first
+// one; everything before it is accepted as-is (fsr_accept).  Same test as
+// FsrWord::iterate.
+template <class SC>
+SPK_HD uint32_t fsr_flags(const SC& sc, uint32_t So, uint32_t S, int base) {
+    const int lo = sc.lo;
+    const uint32_t hw = sc.hw;
+    const uint32_t Q = bit_shr_clamp(So, 0u, (uint32_t)lo) |
+                       bit_sel(hw != 0u, bit_shr_clamp(So, 0u, (uint32_t)lo + 1u), 0u);
+    const uint32_t G1 = So & (So >> 1);
+    const int f = bit_clz(So | 1u);
+    const uint32_t fb = So ? (0x80000000u >> f) : 0u;
+    const bool bad0 = ((S & fb) != 0u) & ((uint32_t)(base + f - sc.last - lo) > hw);
+    return (S & ~(Q | fb)) | bit_sel(lo >= 2, S & G1, 0u) | bit_sel(bad0, fb, 0u);
+}
+
+template <class SC>
+SPK_HD void fsr_accept(SC& sc, uint32_t A, int base) {
+    sc.cnt += bit_popc(A);
+    sc.last = A ? base + 32 - bit_ffs(A) : sc.last;
+}
+
 // `emit(pred, rs, cnt)` stores a closed run when pred is true.
 template <class SC, class EMIT>
 SPK_HD void fsr_word(SC& sc, uint32_t S, int base, EMIT&& emit) {

@@ -13,7 +13,13 @@ using spk_run_t = ::spk_run;
 using spk_sync_t = ::spk_sync;
 using spk_close_t = ::spk_close;
 
-constexpr int kSegThreads = 64;  // 2 warps: fine-grained blocks balance 148 SMs
+// K2 block = 8 warps = 256 pixels = one 32-byte sector of every plane row;
+// the warps share each sector through L2, so they are kept within kDrift
+// groups of each other (otherwise every 4-byte load pulls its own sector from
+// DRAM on long streams)
+constexpr int kSegThreads = 256;
+constexpr int kSegWarps = kSegThreads / 32;
+constexpr int kDrift = 96;       // max groups a warp may produce ahead of its block's slowest
 constexpr int kBatch = 8;        // 32-frame groups per prefetch batch
 constexpr int kRing = 64;        // transposed words buffered per lane (lane drift bound)
 constexpr int kCausalWarps = 2;  // warps per TFI/TFP block

@@ -152,7 +152,7 @@ class TimeShard:
     def _segment(self, state_in):
         """runs of this shard from `state_in` (None = fresh), capacity grown
         until no pixel overflows"""
-        cap = max(64, self.frames // 32)
+        cap = max(64, self.frames // 64)  # grown below if any pixel needs more
         i32 = dict(dtype=torch.int32, device=self.dev)
         while True:
             runs = torch.empty((self.npix, cap, 2), **i32)
@@ -179,6 +179,7 @@ class TimeShard:
         self.entry = entry
         self.capi.check(self.lib.spk_shard_resolve(
             self.g, _ptr(self.planes) if self.frames else None, self.kind, _ptr(entry),
+            _ptr(self.spec), self.scap, _ptr(self.spec_counts), _ptr(self.spec_state),
             _ptr(self.prefix), self.pcap, _ptr(self.sync), _ptr(self.tstate), self.stream))
         if bool((self.sync[:, 3] == -1).any().item()):  # a prefix overflowed: full re-scan
             self.fb, self.fb_counts, _, self.fb_state, fbcap = self._segment(entry)
