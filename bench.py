@@ -35,6 +35,7 @@ W, H, T = 400, 250, 40000
 FPGA_FPS = 20000.0  # FSR/SSR on the XCVU9P FPGA, 400x250
 BYTES_PER_PXF = 1.125  # 1 packed input bit + 1 uint8 output byte
 CPU_SAMPLE_FRAMES = 2000
+LONG_T = 1_000_000  # BASELINE configs[4]: one long stream, extreme dynamic range
 
 
 def peaks():
@@ -206,6 +207,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--frames", type=int, default=T)
+    ap.add_argument("--no-long", action="store_true", help="skip the configs[4] long-stream leg")
+    ap.add_argument("--long-frames", type=int, default=LONG_T)
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -367,11 +370,78 @@ def main():
                                 "kind": kind,
                                 "sample": f"frames [0,{tcpu}) of the same stream, reference "
                                           f"bench() median of 3, {cores} workers"}
+    if not args.no_long:
+        del vol, out
+        if not args.no_e2e:
+            del payload, hout
+        torch.cuda.empty_cache()
+        line["long_stream"] = long_stream(args, rank, world, dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def long_stream(args, rank, world, dev):
+    """BASELINE configs[4]: one 400x250 stream of LONG_T frames, time-sharded
+    across the ranks (rank r holds and outputs frames [a_r, a_r+1); exact
+    boundary resolution, csrc/shard.cu) -- strong scaling.  On one GPU the
+    single-pass time and the 8-shard time (protocol overhead) are reported,
+    and the two outputs are compared through per-frame checksums."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_11639_b200 as spk
+    from paper_2412_11639_b200.shard import (reconstruct_time_sharded,
+                                             reconstruct_time_sharded_dist, time_bounds)
+    T5 = args.long_frames
+    b = time_bounds(T5, world)
+    f0, f1 = b[rank], b[rank + 1]
+    vol = spk.synth("range", 0, W, H, f1 - f0, frame0=f0, device=dev)
+    out = torch.empty((f1 - f0, W * H), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, steps=5, warmup=3):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    def sums():
+        return torch.cat([out[i:i + 4096].to(torch.int32).sum(dim=1)
+                          for i in range(0, out.shape[0], 4096)])
+
+    res = {"workload": f"configs[4] range 400x250x{T5}", "method": args.method,
+           "unit": "frames/s", "scaling": "strong", "frames": T5}
+    if world > 1:
+        ms = timed(lambda: reconstruct_time_sharded_dist(vol, args.method, out=out))
+        res.update(value=T5 / (ms * 1e-3), ms_per_step=ms,
+                   parallelism=f"time shards x{world} (exact boundary resolution)")
+    else:
+        ms = timed(lambda: spk.reconstruct(vol, args.method, out=out))
+        ref = sums()
+        ms8 = timed(lambda: reconstruct_time_sharded(vol, args.method, nshards=8, out=out), 3, 3)
+        res.update(value=T5 / (ms * 1e-3), ms_per_step=ms, parallelism="single pass",
+                   time_sharded_8_on_1gpu_ms=ms8,
+                   time_sharded_equal=bool(torch.equal(sums(), ref)))
+    pxf = W * H * T5
+    res["step_frac"] = pxf * BYTES_PER_PXF / (ms * 1e-3) / 1e9 / peaks()[0]
+    return res
 
 
 if __name__ == "__main__":
