@@ -130,7 +130,7 @@ int spk_segment(const spk_geom* g, const void* d_planes, int method, spk_run* d_
 
 /* spk_segment with the automaton state carried across time shards: d_state_in
  * (nullable = stream start) is the state at frame 0 of these planes, d_state_out
- * (nullable) receives the state after the last frame.  State = 14 int32
+ * (nullable) receives the state after the last frame.  State = 17 int32
  * fields per pixel, field-major (d_state[f * W*H + p]), frames relative to the
  * first plane (earlier spikes negative); see spk_shard_* below. */
 int spk_segment_state(const spk_geom* g, const void* d_planes, int method, spk_run* d_runs,

@@ -117,23 +117,74 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     };
 
     if constexpr (METHOD == kSSR) {
-        // SSR: spike by spike, the warp in lockstep over words (the per-spike
-        // step is long enough that independent progress does not pay off)
-        for (int g0 = 0; g0 < ngroups; g0 += kBatch) {
-            produce(g0);
-#pragma unroll
-            for (int j = 0; j < kBatch; ++j) {
-                if (g0 + j < ngroups) {
-                    uint32_t w = rg[(g0 + j) & (kRing - 1)][lane];
-                    const int base = (g0 + j) * 32;
-                    while (w) {
-                        const int c = __clz(w);
-                        w ^= 0x80000000u >> c;
+        // SSR, two consumers over the same ring and automaton:
+        //  * bulk: every lane walks its own pixel word by word at its own pace,
+        //    one bit-parallel two-level test (ssr_flags: acceptance up to the
+        //    next event) and at most one exact step per iteration -- fast when
+        //    events are sparse (static scenes: whole words per iteration);
+        //  * spike: the warp in lockstep over words, one exact step per spike
+        //    -- cheaper when events come every few spikes (moving scenes).
+        // The first kSsrProbe words run in bulk mode while counting events;
+        // the warp then keeps the mode that fits its event rate.
+        int wi = -1;  // word of this lane (its ring slot may be reused)
+        uint32_t So = 0u, S = 0u;
+        int prevlast = kNoSpike;
+        int events = 0;
+        auto bulk = [&](int limit) {
+            for (;;) {
+                const bool more = wi + 1 < limit;
+                if (__any_sync(kFull, (S == 0u) & more & (wi + 1 >= produced))) {
+                    const int lowest = (int)__reduce_min_sync(kFull, (unsigned)(more ? wi + 1 : 0x7fffffff));
+                    if (produced < ngroups && produced + kBatch <= lowest + kRing) produce(lowest);
+                }
+                if (!__any_sync(kFull, (S != 0u) | more)) break;
+                if ((S == 0u) & (wi + 1 < produced) & more) {
+                    ++wi;
+                    So = S = rg[wi & (kRing - 1)][lane];
+                    prevlast = sc.last;
+                }
+                if (S) {
+                    const int base = wi * 32;
+                    uint32_t Cs, Cl;
+                    const uint32_t V = ssr_flags(sc, So, S, base, prevlast, Cs, Cl);
+                    const uint32_t A = S & ~bit_shr_clamp(0xffffffffu, 0u, V ? (uint32_t)__clz(V) : 32u);
+                    ssr_accept(sc, A, Cs, Cl, base);
+                    S &= ~A;
+                    if (S) {
+                        const int c = __clz(S);
+                        S ^= 0x80000000u >> c;
                         int rs, cnt;
                         const bool e = sc.step(base + c, rs, cnt);
                         emit(e, rs, cnt);
+                        ++events;
                     }
                 }
+            }
+        };
+        const int probe = min(ngroups, kSsrProbe);
+        bulk(probe);
+        const int ev = __reduce_add_sync(kFull, (unsigned)events);
+        if (ev <= kSsrDense * 32 * probe) {
+            bulk(ngroups);
+        } else {  // lanes all stand at word `probe`
+            auto spikes = [&](int g) {
+                uint32_t w = rg[g & (kRing - 1)][lane];
+                const int base = g * 32;
+                while (w) {
+                    const int c = __clz(w);
+                    w ^= 0x80000000u >> c;
+                    int rs, cnt;
+                    const bool e = sc.step(base + c, rs, cnt);
+                    emit(e, rs, cnt);
+                }
+            };
+            int g = probe;
+            for (; g < produced && g < ngroups; ++g) spikes(g);  // words already in the ring
+            for (int g0 = g; g0 < ngroups; g0 += kBatch) {
+                produce(g0);
+#pragma unroll
+                for (int j = 0; j < kBatch; ++j)
+                    if (g0 + j < ngroups) spikes(g0 + j);
             }
         }
     } else {

@@ -117,16 +117,25 @@ __global__ void __launch_bounds__(64) k_resolve(ShardArgs a) {
         if (done) continue;
         const int base = g * 32;
         const uint32_t wo = w;
+        const int prevT = T.last, prevS = S.last;
         while (w) {
+            // both automata accept in bulk up to the next event of either
             if constexpr (METHOD == kFSR) {
-                // both automata accept in bulk up to the next event of either
                 const uint32_t V = fsr_flags(T, wo, w, base) | fsr_flags(S, wo, w, base);
                 const uint32_t A = w & ~bit_shr_clamp(0xffffffffu, 0u, V ? (uint32_t)__clz(V) : 32u);
                 fsr_accept(T, A, base);
                 fsr_accept(S, A, base);
                 w &= ~A;
-                if (!w) break;
+            } else {
+                uint32_t CsT, ClT, CsS, ClS;
+                const uint32_t V = ssr_flags(T, wo, w, base, prevT, CsT, ClT) |
+                                   ssr_flags(S, wo, w, base, prevS, CsS, ClS);
+                const uint32_t A = w & ~bit_shr_clamp(0xffffffffu, 0u, V ? (uint32_t)__clz(V) : 32u);
+                ssr_accept(T, A, CsT, ClT, base);
+                ssr_accept(S, A, CsS, ClS, base);
+                w &= ~A;
             }
+            if (!w) break;
             const int c = __clz(w);
             w ^= 0x80000000u >> c;
             const int n = base + c;
@@ -286,6 +295,9 @@ __global__ void __launch_bounds__(128) k_junction(ShardArgs a) {
     // exit state in the next shard's frames
     if (X.last != kNoSpike) X.last -= a.frames;
     if (X.lo < kLim) X.rs -= a.frames;
+    if (X.fl0 != kNoSpike) X.fl0 -= a.frames;
+    if (X.fl1 != kNoSpike) X.fl1 -= a.frames;
+    if (X.sf != kNoSpike) X.sf -= a.frames;
     X.nrun = 0;
     X.save(a.exit_state, a.npix, p);
 }

@@ -223,6 +223,8 @@ struct Scan {
     int ii, sub0;         // SSR: S1 index of the next interval, sub-run start
     int l0, l1, g0, g1;   // SSR: per parity slot: last index, gap pair low
     uint32_t h0, h1;      //      gap pair width (0/1)
+    int fl0, fl1;         // SSR: frame of each slot's last occurrence
+    int sf;               // SSR: frame of the spike closing interval sub0
 
     SPK_HD void init() {
         last = kNoSpike;
@@ -233,6 +235,7 @@ struct Scan {
         l0 = l1 = kNoIdx;
         g0 = g1 = kNoPair;
         h0 = h1 = 0;
+        fl0 = fl1 = sf = kNoSpike;
     }
 
     // returns true when the run (rs, cnt) closed before this spike.  Written
@@ -267,11 +270,14 @@ struct Scan {
             const uint32_t nghw = (fresh | gnone) ? 0u : (ghw | (uint32_t)gext);
             l0 = k ? l0 : ii;
             l1 = k ? ii : l1;
+            fl0 = k ? fl0 : n;
+            fl1 = k ? n : fl1;
             g0 = k ? g0 : nglo;
             g1 = k ? nglo : g1;
             h0 = k ? h0 : nghw;
             h1 = k ? nghw : h1;
             sub0 = brk ? ii : sub0;
+            sf = brk ? n : sf;
             ++ii;
         }
         out_rs = rs;
@@ -294,10 +300,10 @@ struct Scan {
 
     // ---- state carried across time shards (SoA: field f of pixel p at
     // st[f * stride + p]; frames relative to the shard's first frame)
-    static constexpr int kFields = 14;
+    static constexpr int kFields = 17;
     SPK_HD void save(int32_t* st, int64_t stride, int64_t p) const {
         const int32_t v[kFields] = {last, lo, rs, cnt, nrun, (int32_t)hw, ii, sub0,
-                                    l0, l1, g0, g1, (int32_t)h0, (int32_t)h1};
+                                    l0, l1, g0, g1, (int32_t)h0, (int32_t)h1, fl0, fl1, sf};
         for (int f = 0; f < kFields; ++f) st[f * stride + p] = v[f];
     }
     SPK_HD void restore(const int32_t* st, int64_t stride, int64_t p) {
@@ -315,6 +321,9 @@ struct Scan {
         g1 = st[11 * stride + p];
         h0 = (uint32_t)st[12 * stride + p];
         h1 = (uint32_t)st[13 * stride + p];
+        fl0 = st[14 * stride + p];
+        fl1 = st[15 * stride + p];
+        sf = st[16 * stride + p];
     }
 
     // Same future: from here on both automata take identical decisions on any
@@ -518,6 +527,117 @@ template <class SC>
 SPK_HD void fsr_accept(SC& sc, uint32_t A, int base) {
     sc.cnt += bit_popc(A);
     sc.last = A ? base + 32 - bit_ffs(A) : sc.last;
+}
+
+// ---- SSR in bulk ----------------------------------------------------------
+// Inside an FSR run with pair [lo, lo+hw] every accepted interval is short
+// (lo) or long (lo+1).  SSR's second level is the pair rule over each value's
+// occurrence gaps (interval-index distance between consecutive occurrences in
+// the sub-run).  Between two consecutive long intervals lie only short ones,
+// so index gap m is a frame distance m*lo + 1 between the spikes closing
+// them; between two short ones lie only long ones: m*(lo+1) - 1.  A slot with
+// gap pair [g, g+h] thus allows the frame distances
+//     long:  D1 = g*lo + 1,      D2 = D1 + h*lo
+//     short: D1 = g*(lo+1) - 1,  D2 = D1 + h*(lo+1)
+// and FsrWord's argument carries over per class (class spikes restricted to
+// the current sub-run): a class spike without a class spike exactly D1 / D2
+// earlier is flagged; the only violation that can escape is a short at index
+// gap 1 (distance lo) -- flagged separately when 1 is not allowed (g >= 2).
+// The first class spike of the word is checked against the slot's last
+// occurrence frame directly.  Slots not yet holding a gap pair (first
+// occurrence / first gap after a sub-run start) and every FSR event go
+// through the exact step.  Cs / Cl receive the class masks for ssr_accept.
+template <class SC>
+SPK_HD uint32_t ssr_flags(const SC& sc, uint32_t So, uint32_t S, int base, int prevlast,
+                          uint32_t& Cs, uint32_t& Cl) {
+    const uint32_t Vf = fsr_flags(sc, So, S, base);
+    const int lo = sc.lo;
+    if (lo >= kLim) {
+        Cs = Cl = 0u;
+        return Vf;
+    }
+    const uint32_t hw = sc.hw;
+    const int f = bit_clz(So | 1u);
+    const uint32_t fb = So ? (0x80000000u >> f) : 0u;
+    const int d0 = base + f - prevlast;
+    // spikes closing an interval of the current sub-run: frames >= sf
+    const uint32_t sub = sc.sf <= base ? 0xffffffffu
+                                       : bit_shr_clamp(0xffffffffu, 0u, (uint32_t)(sc.sf - base));
+    const uint32_t at_lo = bit_shr_clamp(So, 0u, (uint32_t)lo);
+    const uint32_t at_lo1 = bit_shr_clamp(So, 0u, (uint32_t)lo + 1u);
+    Cs = ((So & at_lo) | bit_sel(d0 == lo, fb, 0u)) & sub;
+    Cl = ((So & at_lo1 & ~at_lo) | bit_sel(d0 == lo + 1, fb, 0u)) & bit_sel(hw != 0u, sub, 0u);
+    uint32_t V = Vf;
+#pragma unroll
+    for (int cls = 0; cls < 2; ++cls) {  // 0 = short (value lo), 1 = long (lo + 1)
+        const uint32_t C = cls ? Cl : Cs;
+        const bool x = ((lo + cls) & 1) != 0;  // parity slot of the value
+        const int l = x ? sc.l1 : sc.l0;
+        const int g = x ? sc.g1 : sc.g0;
+        const int h = (int)(x ? sc.h1 : sc.h0);
+        const int fl = x ? sc.fl1 : sc.fl0;
+        const uint32_t CS = C & S;
+        const bool est = (l >= sc.sub0) & (g < kLim);
+        const uint32_t fcs = CS ? (0x80000000u >> bit_clz(CS)) : 0u;
+        const int D1 = cls ? g * lo + 1 : g * (lo + 1) - 1;
+        const int D2 = D1 + h * (cls ? lo : lo + 1);
+        const uint32_t Q = bit_shr_clamp(C, 0u, (uint32_t)D1) |
+                           bit_sel(h != 0, bit_shr_clamp(C, 0u, (uint32_t)D2), 0u);
+        const int fc = bit_clz(C | 1u);
+        const uint32_t fcw = C ? (0x80000000u >> fc) : 0u;
+        const int dfirst = base + fc - fl;
+        const bool badf = ((fcw & S) != 0u) & (dfirst != D1) & (dfirst != D2);
+        const uint32_t gap1 = bit_sel((cls == 0) & (g >= 2), CS & bit_shr_clamp(C, 0u, (uint32_t)lo), 0u);
+        const uint32_t Vc = (CS & ~(Q | fcw)) | bit_sel(badf, fcw, 0u) | gap1;
+        V |= bit_sel(est, Vc, fcs);
+    }
+    return V;
+}
+
+// bookkeeping of an accepted prefix A (no event inside) for SSR
+template <class SC>
+SPK_HD void ssr_accept(SC& sc, uint32_t A, uint32_t Cs, uint32_t Cl, int base) {
+    if (!A) return;
+    const int n = bit_popc(A);
+#pragma unroll
+    for (int cls = 0; cls < 2; ++cls) {
+        const uint32_t Ac = A & (cls ? Cl : Cs);
+        if (Ac) {
+            const int b = bit_ffs(Ac);  // latest class spike: bit b-1
+            const int idx = sc.ii + bit_popc(A >> (b - 1)) - 1;
+            const int fr = base + 32 - b;
+            if (((sc.lo + cls) & 1) != 0) {
+                sc.l1 = idx;
+                sc.fl1 = fr;
+            } else {
+                sc.l0 = idx;
+                sc.fl0 = fr;
+            }
+        }
+    }
+    sc.cnt += n;
+    sc.ii += n;
+    sc.last = base + 32 - bit_ffs(A);
+}
+
+// SSR over one word: bulk acceptance up to each event, the event exact
+template <class SC, class EMIT>
+SPK_HD void ssr_word(SC& sc, uint32_t So, int base, EMIT&& emit) {
+    uint32_t S = So;
+    const int prevlast = sc.last;
+    while (S) {
+        uint32_t Cs, Cl;
+        const uint32_t V = ssr_flags(sc, So, S, base, prevlast, Cs, Cl);
+        const uint32_t A = S & ~bit_shr_clamp(0xffffffffu, 0u, V ? (uint32_t)bit_clz(V) : 32u);
+        ssr_accept(sc, A, Cs, Cl, base);
+        S &= ~A;
+        if (!S) break;
+        const int c = bit_clz(S);
+        S ^= 0x80000000u >> c;
+        int rs, cnt;
+        const bool e = sc.step(base + c, rs, cnt);
+        emit(e, rs, cnt);
+    }
 }
 
 // `emit(pred, rs, cnt)` stores a closed run when pred is true.

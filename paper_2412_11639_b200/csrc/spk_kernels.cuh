@@ -21,6 +21,8 @@ constexpr int kSegThreads = 256;
 constexpr int kSegWarps = kSegThreads / 32;
 constexpr int kDrift = 96;       // max groups a warp may produce ahead of its block's slowest
 constexpr int kBatch = 8;        // 32-frame groups per prefetch batch
+constexpr int kSsrProbe = 64;    // SSR: words scanned in bulk mode before choosing the mode
+constexpr int kSsrDense = 2;     // SSR: events per lane-word above which spike mode wins
 constexpr int kRing = 64;        // transposed words buffered per lane (lane drift bound)
 constexpr int kCausalWarps = 2;  // warps per TFI/TFP block
 

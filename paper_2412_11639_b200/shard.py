@@ -109,7 +109,7 @@ def reconstruct_sharded(volume: PackedVolume, method="fsr", group=None,
 # device buffers; the driver below runs all shards of a volume in one process
 # (one GPU); reconstruct_time_sharded_dist runs one shard per rank.
 
-STATE_FIELDS = 14
+STATE_FIELDS = 17
 SYNC_DT = 4   # spk_sync: 4 x int32
 CLOSE_DT = 8  # spk_close: 8 x int32
 
@@ -285,7 +285,7 @@ def reconstruct_time_sharded_dist(shard: PackedVolume, method="fsr", group=None,
     identical to the same frames of a single-pass reconstruct().
 
     Data path: none; the only exchange is O(W*H) per boundary -- the true
-    automaton state forward (rank r -> r+1, 56 B/px) and the close records of
+    automaton state forward (rank r -> r+1, 68 B/px) and the close records of
     boundary-crossing runs backward (rank r+1 -> r, 2 x 32 B/px)."""
     rank, world = _group_info(group)
     peer = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)

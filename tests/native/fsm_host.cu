@@ -88,8 +88,8 @@ extern "C" long scan_runs(const uint8_t* bits, long frames, int method, long* st
 
 // The segment kernel's word-level driver: 32-frame words with the first frame
 // in bit 31; FSR through fsr_word (bulk acceptance), SSR spike by spike.
-extern "C" long word_runs(const uint8_t* bits, long frames, int method, long* start, long* end,
-                          long* cnt, long cap) {
+static long word_runs_impl(const uint8_t* bits, long frames, int method, long* start, long* end,
+                           long* cnt, long cap, bool ssr_bulk) {
     long n = 0, last = -1;
     auto put = [&](bool e, int rs, int c) {
         if (e) {
@@ -111,6 +111,8 @@ extern "C" long word_runs(const uint8_t* bits, long frames, int method, long* st
                 }
             if (bulk) {
                 spk::fsr_word(sc, w, (int)base, put);
+            } else if (ssr_bulk) {
+                spk::ssr_word(sc, w, (int)base, put);
             } else {
                 while (w) {
                     const int c = spk::bit_clz(w);
@@ -134,6 +136,17 @@ extern "C" long word_runs(const uint8_t* bits, long frames, int method, long* st
     }
     for (long k = 0; k < n && k < cap; ++k) end[k] = (k + 1 < n) ? start[k + 1] : last;
     return n;
+}
+
+extern "C" long word_runs(const uint8_t* bits, long frames, int method, long* start, long* end,
+                          long* cnt, long cap) {
+    return word_runs_impl(bits, frames, method, start, end, cnt, cap, false);
+}
+
+// SSR with the bit-parallel second-level test (ssr_word); FSR as word_runs
+extern "C" long ssrword_runs(const uint8_t* bits, long frames, int method, long* start, long* end,
+                             long* cnt, long cap) {
+    return word_runs_impl(bits, frames, method, start, end, cnt, cap, true);
 }
 
 // The FSR 4-word window driver of the segment kernel (fsr_batch4).

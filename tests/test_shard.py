@@ -150,7 +150,7 @@ class _FakeTimeShard:
         pass
 
     def fresh_entry(self):
-        return torch.zeros((14, self.npix), dtype=torch.int32)
+        return torch.zeros((17, self.npix), dtype=torch.int32)
 
     def resolve(self, entry):
         self.entry = entry.clone()
