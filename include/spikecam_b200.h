@@ -198,6 +198,15 @@ int spk_upload_planes(const spk_geom* g, const void* h_payload, size_t src_pitch
 int spk_reconstruct_host(const spk_geom* g, const void* h_payload, int method, int tfp_window,
                          int out_type, void* h_out, size_t out_pitch);
 
+/* Many volumes of one geometry through the host boundary, pipelined: the
+ * upload and reconstruction of volume i+1 overlap the download of volume i
+ * (two stream lanes), so a sequence is bound by the slower PCIe direction.
+ * h_payloads[i] / h_outs[i] as in spk_reconstruct_host (pinned memory lets the
+ * copies run asynchronously).  The ingest path of SURVEY.md 8(f) rank 2. */
+int spk_reconstruct_host_batch(const spk_geom* g, int32_t count, const void* const* h_payloads,
+                               int method, int tfp_window, int out_type, void* const* h_outs,
+                               size_t out_pitch);
+
 /* Host boundary of segment_fsr / segment_ssr (proj/src/reconstruct.cpp:198-211):
  * dense SPK1 payload in, per-pixel run lists out (layout as spk_segment;
  * h_runs holds W*H*run_cap entries).  Synchronous. */

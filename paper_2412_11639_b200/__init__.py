@@ -18,6 +18,7 @@ from .recon import (  # noqa: F401
     read_spk,
     reconstruct,
     reconstruct_host,
+    reconstruct_host_batch,
     segments,
     synth,
     write_spk,

@@ -41,6 +41,8 @@ SIGNATURES = {
     "spk_upload_planes": (C.c_int, [_G, _P, C.c_size_t, C.c_int, _P, _P]),
     "spk_reconstruct_host": (C.c_int, [_G, _P, C.c_int, C.c_int, C.c_int, _P, C.c_size_t]),
     "spk_segment_host": (C.c_int, [_G, _P, C.c_int, _P, C.c_int64, _P, _P]),
+    "spk_reconstruct_host_batch": (C.c_int, [_G, C.c_int32, _P, C.c_int, C.c_int, C.c_int, _P,
+                                             C.c_size_t]),
     "spk_records": (C.c_int, [_G, _P, C.c_int, C.c_uint32, _P, _P, _P]),
     "spk_records_host": (C.c_int, [_G, _P, C.c_int, C.c_uint32, _P, _P]),
     "spk_free_device": (C.c_int, [_P, _P]),

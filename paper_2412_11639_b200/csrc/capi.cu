@@ -28,6 +28,7 @@ thread_local int64_t g_launches = 0;
 thread_local bool g_timing = false;
 thread_local cudaEvent_t g_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 thread_local int g_ev_used = 0;  // events recorded by the last call
+thread_local bool g_no_split = false;  // pipelined host batches: one pixel part per call
 
 // phase marker k (0..4) on stream s when timing is enabled: 0 before K2,
 // 1 after K2, 2 after K2b/scan/K2c, 3 after K3, 4 after the fixup
@@ -345,7 +346,7 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
     // K2 is issue-bound, K2b..K3 are latency/HBM-bound: with enough pixels
     // the volume is cut into pixel parts (multiples of 512 pixels) and the
     // expand of part k runs on an auxiliary stream while K2 scans part k+1.
-    const int nparts = (npix >= kSplitPixels && !g_timing) ? kParts : 1;
+    const int nparts = (npix >= kSplitPixels && !g_timing && !g_no_split) ? kParts : 1;
     if (nparts == 1) {
         ExpandWork<OUT> w(s);
         if ((rc = prepare_expand<OUT>(a, w, s))) return rc;
@@ -749,6 +750,73 @@ int spk_reconstruct_host(const spk_geom* g, const void* h_payload, int method, i
     }();
     cudaError_t se = cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
+    if (rc) return rc;
+    if (se != cudaSuccess) return cuda_fail(se, "cudaStreamSynchronize");
+    return SPK_OK;
+}
+
+int spk_reconstruct_host_batch(const spk_geom* g, int32_t count, const void* const* h_payloads,
+                               int method, int tfp_window, int out_type, void* const* h_outs,
+                               size_t out_pitch) {
+    spk_geom dg = *g;
+    dg.plane_pitch = spk_plane_pitch(g->width, g->height);
+    int rc = check_geom(&dg, true);
+    if (rc) return rc;
+    if ((rc = check_method(method, tfp_window))) return rc;
+    if (out_type < SPK_OUT_U8 || out_type > SPK_OUT_F64)
+        return fail(SPK_EINVAL, "spk_reconstruct_host_batch: bad out_type");
+    const int64_t npix = npix_of(g);
+    if (out_pitch < (size_t)npix) return fail(SPK_EINVAL, "spk: out_pitch must be >= W*H");
+    if (count < 0 || (count > 0 && (!h_payloads || !h_outs)))
+        return fail(SPK_EINVAL, "spk_reconstruct_host_batch: bad volume list");
+    if (g->frames == 0 || count == 0) return SPK_OK;
+    for (int i = 0; i < count; ++i)
+        if (!h_payloads[i] || !h_outs[i]) return fail(SPK_EINVAL, "spk: null host buffer");
+    const size_t esz = out_type == SPK_OUT_U8 ? 1 : out_type == SPK_OUT_F32 ? 4 : 8;
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    // Two lanes of (H2D, kernels, D2H), round robin: while volume i's frames
+    // come back over PCIe, volume i+1 is uploaded and reconstructed.
+    constexpr int kLanes = 2;
+    cudaStream_t st[kLanes] = {nullptr, nullptr};
+    for (auto& x : st) SPK_CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    g_no_split = true;
+    rc = [&]() -> int {
+        Scratch planes0(st[0]), planes1(st[1]), out0(st[0]), out1(st[1]);
+        Scratch* planes[kLanes] = {&planes0, &planes1};
+        Scratch* outs[kLanes] = {&out0, &out1};
+        for (int l = 0; l < kLanes && l < count; ++l) {
+            SPK_CK(planes[l]->alloc(dg.plane_pitch * (size_t)g->frames));
+            SPK_CK(outs[l]->alloc(out_pitch * esz * (size_t)g->frames));
+        }
+        for (int i = 0; i < count; ++i) {
+            const int l = i % kLanes;
+            cudaStream_t s = st[l];
+            int r = spk_upload_planes(&dg, h_payloads[i], plane_bytes(g), 0, planes[l]->p, s);
+            if (r) return r;
+            if (out_type == SPK_OUT_U8)
+                r = spk_reconstruct_u8(&dg, planes[l]->p, method, tfp_window,
+                                       static_cast<uint8_t*>(outs[l]->p), out_pitch, s);
+            else if (out_type == SPK_OUT_F32)
+                r = spk_reconstruct_f32(&dg, planes[l]->p, method, tfp_window,
+                                        static_cast<float*>(outs[l]->p), out_pitch, s);
+            else
+                r = spk_reconstruct_f64(&dg, planes[l]->p, method, tfp_window,
+                                        static_cast<double*>(outs[l]->p), out_pitch, s);
+            if (r) return r;
+            SPK_CK(cudaMemcpyAsync(h_outs[i], outs[l]->p, out_pitch * esz * (size_t)g->frames,
+                                   cudaMemcpyDeviceToHost, s));
+        }
+        return SPK_OK;
+    }();
+    g_no_split = false;
+    cudaError_t se = cudaSuccess;
+    for (auto& x : st) {
+        const cudaError_t e = cudaStreamSynchronize(x);
+        if (se == cudaSuccess) se = e;
+        cudaStreamDestroy(x);
+    }
     if (rc) return rc;
     if (se != cudaSuccess) return cuda_fail(se, "cudaStreamSynchronize");
     return SPK_OK;

@@ -17,6 +17,7 @@ every call either launches the sm_100a kernels or raises.
 """
 from __future__ import annotations
 
+import ctypes as C
 import enum
 from dataclasses import dataclass
 from pathlib import Path
@@ -257,6 +258,36 @@ def reconstruct_host(payload: np.ndarray, width: int, height: int, frames: int, 
                                                int(m.tfp_window), code, out.ctypes.data,
                                                out.shape[1]))
     return out
+
+
+def reconstruct_host_batch(payloads, width: int, height: int, frames: int, method="fsr",
+                           dtype=np.uint8, outs=None) -> list:
+    """Many volumes of one geometry through spk_reconstruct_host_batch: the
+    upload + reconstruction of volume i+1 overlap the download of volume i.
+    `payloads`: dense SPK1 payloads (numpy / pinned torch host tensors);
+    `outs`: host [T, W*H] buffers (allocated when omitted)."""
+    m = _method(method)
+    code = {np.dtype(np.uint8): capi.SPK_OUT_U8, np.dtype(np.float32): capi.SPK_OUT_F32,
+            np.dtype(np.float64): capi.SPK_OUT_F64}[np.dtype(dtype)]
+    npix = width * height
+    if outs is None:
+        outs = [np.empty((frames, npix), dtype=dtype) for _ in payloads]
+    if len(outs) != len(payloads):
+        raise ValueError("one output buffer per payload")
+
+    def addr(x):
+        if isinstance(x, torch.Tensor):
+            return x.data_ptr()
+        return np.ascontiguousarray(x).ctypes.data
+
+    keep = [np.ascontiguousarray(p) if not isinstance(p, torch.Tensor) else p for p in payloads]
+    pin = (C.c_void_p * len(keep))(*[addr(p) for p in keep])
+    pout = (C.c_void_p * len(outs))(*[addr(o) for o in outs])
+    g = capi.geom(width, height, frames, 0)
+    capi.check(capi.lib().spk_reconstruct_host_batch(g, len(keep), pin, int(m.kind),
+                                                     int(m.tfp_window), code, pout,
+                                                     outs[0].shape[1] if len(outs) else npix))
+    return outs
 
 
 def reconstruct_host_ptr(h_payload: int, width: int, height: int, frames: int, method,
