@@ -7,9 +7,8 @@
 // compile against this header unchanged.  Every reconstruction runs on the
 // GPU; there is no CPU code path for it.
 //
-// Not provided: PixelReconState (the reference's per-frame CPU streaming
-// helper), the simulator, stability oracles, metrics and the PNG writer --
-// outside the accelerated path.
+// Not provided: the simulator, stability oracles, metrics and the PNG writer
+// -- outside the accelerated path.
 #pragma once
 
 #include <cstdint>
@@ -108,6 +107,50 @@ std::vector<Segment> segment_ssr(const SpikeLikeStream& stream);
 double segment_intensity(const Segment& segment);
 std::vector<SegmentEvent> fsr_events(const SpikeLikeStream& stream);
 std::vector<double> reconstruct_pixel(const SpikeLikeStream& stream, ReconMethod method);
+
+// Per-pixel streaming form of FSR (reconstruct.hpp:46-67).  Same contract:
+// push_frame returns the segment that closes at this frame, flush the still-
+// open spans; the events equal fsr_events of the whole stream.  Backed by a
+// one-pixel spk_stream: frames without a spike are buffered (no event can
+// close there) and each spike pushes the buffered frames through the GPU, so
+// this scalar form costs one device round trip per spike -- use EventStream
+// for whole sensors.
+class PixelReconState {
+public:
+    PixelReconState();
+    ~PixelReconState();
+    PixelReconState(const PixelReconState&) = delete;
+    PixelReconState& operator=(const PixelReconState&) = delete;
+    PixelReconState(PixelReconState&& o) noexcept;
+    PixelReconState& operator=(PixelReconState&& o) noexcept;
+    std::optional<SegmentEvent> push_frame(bool bit);
+    std::vector<SegmentEvent> flush();
+    long frames_seen() const { return frame_; }
+
+private:
+    std::vector<SegmentEvent> push_pending();
+    void* stream_ = nullptr;  // spk_stream
+    std::vector<uint8_t> pending_;
+    long frame_ = 0;
+};
+
+// The same for every pixel of a sensor at once: frames arrive in blocks
+// (SPK1 payloads); each push returns, per pixel (row-major), the segments
+// that closed in the block.
+class EventStream {
+public:
+    EventStream(int width, int height);
+    ~EventStream();
+    EventStream(const EventStream&) = delete;
+    EventStream& operator=(const EventStream&) = delete;
+    std::vector<std::vector<SegmentEvent>> push(const std::vector<uint8_t>& payload, long frames);
+    std::vector<std::vector<SegmentEvent>> flush();
+    long frames() const;
+
+private:
+    void* stream_ = nullptr;  // spk_stream
+    int width_, height_;
+};
 
 // `workers` is accepted for signature compatibility: one call = one GPU.
 std::vector<IntensityImage> reconstruct(const SpikeVolume& volume, ReconMethod method,

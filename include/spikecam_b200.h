@@ -231,6 +231,34 @@ int spk_records_host(const spk_geom* g, const void* h_payload, int method, uint3
 int spk_free_device(void* d_ptr, void* stream);
 void spk_free_host(void* h_ptr);
 
+/* ---- streaming FSR (PixelReconState, proj/include/spikecam/reconstruct.hpp:
+ * 46-67, for every pixel at once) --------------------------------------------
+ * Frames arrive in blocks; each push scans its block with the automaton state
+ * carried from the previous block and returns the segments that closed in it
+ * as SegmentEvents -- the events PixelReconState::push_frame yields, in order,
+ * grouped by pixel: pixel p's events are d_events[d_offsets[p] ..
+ * d_offsets[p+1]) (W*H+1 offsets).  spk_stream_flush returns the still-open
+ * spans (PixelReconState::flush) and ends the stream.  Both allocate
+ * *d_events and *d_offsets from the device pool (release with
+ * spk_free_device) and synchronise `stream` once. */
+typedef struct spk_event {
+    int64_t duration;
+    double intensity;
+} spk_event;
+typedef struct spk_stream spk_stream;
+int spk_stream_create(int32_t width, int32_t height, void* stream, spk_stream** out);
+int spk_stream_push(spk_stream* st, const void* d_planes, size_t plane_pitch, int64_t frames,
+                    spk_event** d_events, uint64_t** d_offsets, uint64_t* total, void* stream);
+int spk_stream_flush(spk_stream* st, spk_event** d_events, uint64_t** d_offsets, uint64_t* total,
+                     void* stream);
+/* host boundary: dense SPK1 payload of the block in, malloc'd host events and
+ * offsets out (release both with spk_free_host); synchronous */
+int spk_stream_push_host(spk_stream* st, const void* h_payload, int64_t frames, spk_event** h_events,
+                         uint64_t** h_offsets, uint64_t* total);
+int spk_stream_flush_host(spk_stream* st, spk_event** h_events, uint64_t** h_offsets, uint64_t* total);
+int64_t spk_stream_frames(const spk_stream* st);
+int spk_stream_destroy(spk_stream* st);
+
 /* ---- configuration / diagnostics ------------------------------------------ */
 /* run-list capacity per pixel used by spk_reconstruct_*: 0 = automatic
  * (max(64, T/32)).  Pixels that overflow it are recomputed exactly by a

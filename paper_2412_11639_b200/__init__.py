@@ -23,6 +23,7 @@ from .recon import (  # noqa: F401
     synth,
     write_spk,
 )
+from .stream import EventStream  # noqa: F401
 from .records import RecordVolume, decode, read_spkr, records, records_host, write_spkr  # noqa: F401
 from ._capi import LIB_PATH, SpikecamError  # noqa: F401
 

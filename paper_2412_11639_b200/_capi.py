@@ -56,6 +56,13 @@ SIGNATURES = {
     "spk_shard_close_chain": (C.c_int, [C.c_int64, _P, _P, C.c_int32, _P, _P]),
     "spk_shard_stitch": (C.c_int, [_G, C.c_int, _P, _P, _P, C.c_int32, _P, _P, C.c_int64, _P, _P, _P,
                                    _P, _P, _P, _P, C.c_int64, _P, _P, _P]),
+    "spk_stream_create": (C.c_int, [C.c_int32, C.c_int32, _P, _P]),
+    "spk_stream_push": (C.c_int, [_P, _P, C.c_size_t, C.c_int64, _P, _P, _P, _P]),
+    "spk_stream_flush": (C.c_int, [_P, _P, _P, _P, _P]),
+    "spk_stream_push_host": (C.c_int, [_P, _P, C.c_int64, _P, _P, _P]),
+    "spk_stream_flush_host": (C.c_int, [_P, _P, _P, _P]),
+    "spk_stream_frames": (C.c_int64, [_P]),
+    "spk_stream_destroy": (C.c_int, [_P]),
     "spk_expand_runs_u8": (C.c_int, [_G, _P, C.c_int64, _P, _P, _P, C.c_size_t, _P]),
     "spk_expand_runs_f32": (C.c_int, [_G, _P, C.c_int64, _P, _P, _P, C.c_size_t, _P]),
     "spk_expand_runs_f64": (C.c_int, [_G, _P, C.c_int64, _P, _P, _P, C.c_size_t, _P]),

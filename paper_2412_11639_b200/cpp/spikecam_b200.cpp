@@ -351,6 +351,103 @@ PackedSpikes pack(const SpikeVolume& volume, uint32_t fps) {
     return sp;
 }
 
+// ------------------------------------------------------------- streaming ----
+namespace {
+
+std::vector<std::vector<SegmentEvent>> take_events(spk_event* ev, uint64_t* offs, uint64_t total,
+                                                   size_t npix) {
+    std::vector<std::vector<SegmentEvent>> out(npix);
+    for (size_t p = 0; p < npix; ++p)
+        for (uint64_t i = offs[p]; i < offs[p + 1] && i < total; ++i)
+            out[p].push_back(SegmentEvent{static_cast<long>(ev[i].duration), ev[i].intensity});
+    spk_free_host(ev);
+    spk_free_host(offs);
+    return out;
+}
+
+spk_stream* make_stream(int w, int h) {
+    spk_stream* st = nullptr;
+    ck(spk_stream_create(w, h, nullptr, &st));
+    return st;
+}
+
+}  // namespace
+
+PixelReconState::PixelReconState() : stream_(make_stream(1, 1)) {}
+PixelReconState::~PixelReconState() {
+    if (stream_) spk_stream_destroy(static_cast<spk_stream*>(stream_));
+}
+PixelReconState::PixelReconState(PixelReconState&& o) noexcept
+    : stream_(o.stream_), pending_(std::move(o.pending_)), frame_(o.frame_) {
+    o.stream_ = nullptr;
+}
+PixelReconState& PixelReconState::operator=(PixelReconState&& o) noexcept {
+    if (this != &o) {
+        if (stream_) spk_stream_destroy(static_cast<spk_stream*>(stream_));
+        stream_ = o.stream_;
+        pending_ = std::move(o.pending_);
+        frame_ = o.frame_;
+        o.stream_ = nullptr;
+    }
+    return *this;
+}
+
+std::vector<SegmentEvent> PixelReconState::push_pending() {
+    if (pending_.empty()) return {};
+    spk_event* ev = nullptr;
+    uint64_t* offs = nullptr;
+    uint64_t total = 0;
+    // one pixel: one payload byte per frame, the spike in bit 0
+    ck(spk_stream_push_host(static_cast<spk_stream*>(stream_), pending_.data(),
+                            static_cast<int64_t>(pending_.size()), &ev, &offs, &total));
+    pending_.clear();
+    return take_events(ev, offs, total, 1)[0];
+}
+
+std::optional<SegmentEvent> PixelReconState::push_frame(bool bit) {
+    pending_.push_back(bit ? 1 : 0);
+    ++frame_;
+    if (!bit) return std::nullopt;  // a segment only closes at a spike
+    std::vector<SegmentEvent> ev = push_pending();
+    if (ev.empty()) return std::nullopt;
+    return ev.back();
+}
+
+std::vector<SegmentEvent> PixelReconState::flush() {
+    push_pending();
+    spk_event* ev = nullptr;
+    uint64_t* offs = nullptr;
+    uint64_t total = 0;
+    ck(spk_stream_flush_host(static_cast<spk_stream*>(stream_), &ev, &offs, &total));
+    return take_events(ev, offs, total, 1)[0];
+}
+
+EventStream::EventStream(int width, int height)
+    : stream_(make_stream(width, height)), width_(width), height_(height) {}
+EventStream::~EventStream() {
+    if (stream_) spk_stream_destroy(static_cast<spk_stream*>(stream_));
+}
+
+std::vector<std::vector<SegmentEvent>> EventStream::push(const std::vector<uint8_t>& payload, long frames) {
+    if (payload.size() != plane_bytes(width_, height_) * static_cast<size_t>(frames))
+        throw std::invalid_argument("EventStream::push: payload size does not match the frames");
+    spk_event* ev = nullptr;
+    uint64_t* offs = nullptr;
+    uint64_t total = 0;
+    ck(spk_stream_push_host(static_cast<spk_stream*>(stream_), payload.data(), frames, &ev, &offs, &total));
+    return take_events(ev, offs, total, static_cast<size_t>(width_) * height_);
+}
+
+std::vector<std::vector<SegmentEvent>> EventStream::flush() {
+    spk_event* ev = nullptr;
+    uint64_t* offs = nullptr;
+    uint64_t total = 0;
+    ck(spk_stream_flush_host(static_cast<spk_stream*>(stream_), &ev, &offs, &total));
+    return take_events(ev, offs, total, static_cast<size_t>(width_) * height_);
+}
+
+long EventStream::frames() const { return static_cast<long>(spk_stream_frames(static_cast<spk_stream*>(stream_))); }
+
 // ------------------------------------------------------------------- io ----
 PackedSpikes read_spk_packed(const std::filesystem::path& path) {
     std::vector<uint8_t> data = read_file(path);

@@ -998,6 +998,250 @@ int spk_free_device(void* d_ptr, void* stream) {
 
 void spk_free_host(void* h_ptr) { std::free(h_ptr); }
 
+}  // extern "C"
+
+struct spk_stream {
+    int32_t width, height;
+    int64_t npix;
+    int64_t frames;      // pushed so far
+    int32_t* state;      // automaton state, relative to frame `frames`
+    double* last_value;  // per pixel: intensity of the last closed run
+};
+
+namespace {
+
+// count -> scan -> allocate -> write the events of one push / the flush
+int stream_events(spk_stream* st, StreamArgs& a, spk_event** d_events, uint64_t** d_offsets,
+                  uint64_t* total, cudaStream_t s) {
+    const int64_t npix = st->npix;
+    Scratch ecount(s);
+    SPK_CK(ecount.alloc((size_t)(npix + 1) * sizeof(uint32_t)));
+    SPK_CK(cudaMemsetAsync(static_cast<uint32_t*>(ecount.p) + npix, 0, sizeof(uint32_t), s));
+    void* offs = nullptr;
+    SPK_CK(cudaMallocAsync(&offs, (size_t)(npix + 1) * sizeof(unsigned long long), s));
+    a.ecount = static_cast<uint32_t*>(ecount.p);
+    a.eoffs = static_cast<unsigned long long*>(offs);
+    const unsigned blocks = (unsigned)((npix + 127) / 128);
+    k_stream_count<<<blocks, 128, 0, s>>>(a);
+    SPK_LAUNCHED("k_stream_count");
+    int rc = launch_scan(a.ecount, static_cast<unsigned long long*>(offs), npix + 1, s);
+    if (rc) {
+        cudaFreeAsync(offs, s);
+        return rc;
+    }
+    unsigned long long tot = 0;
+    SPK_CK(cudaMemcpyAsync(&tot, static_cast<unsigned long long*>(offs) + npix, sizeof(tot),
+                           cudaMemcpyDeviceToHost, s));
+    SPK_CK(cudaStreamSynchronize(s));
+    void* ev = nullptr;
+    SPK_CK(cudaMallocAsync(&ev, std::max<size_t>(16, (size_t)tot * sizeof(spk_event)), s));
+    a.events = static_cast<spk_event*>(ev);
+    k_stream_write<<<blocks, 128, 0, s>>>(a);
+    SPK_LAUNCHED("k_stream_write");
+    *d_events = static_cast<spk_event*>(ev);
+    *d_offsets = static_cast<uint64_t*>(offs);
+    *total = tot;
+    return SPK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spk_stream_create(int32_t width, int32_t height, void* stream, spk_stream** out) {
+    if (!out) return fail(SPK_EINVAL, "spk_stream_create: null handle");
+    *out = nullptr;
+    spk_geom g{width, height, 0, 0};
+    int rc = check_geom(&g, false);
+    if (rc) return rc;
+    cudaStream_t s = as_stream(stream);
+    spk_stream* st = new spk_stream{width, height, npix_of(&g), 0, nullptr, nullptr};
+    const int64_t npix = st->npix;
+    cudaError_t e = cudaMalloc(&st->state, (size_t)Scan<kFSR>::kFields * npix * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&st->last_value, (size_t)npix * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemsetAsync(st->last_value, 0, (size_t)npix * sizeof(double), s);
+    if (e != cudaSuccess) {
+        cudaFree(st->state);
+        cudaFree(st->last_value);
+        delete st;
+        return cuda_fail(e, "spk_stream_create");
+    }
+    k_state_fresh<<<(unsigned)((npix + 255) / 256), 256, 0, s>>>(st->state, npix);
+    ++g_launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) {
+        cudaFree(st->state);
+        cudaFree(st->last_value);
+        delete st;
+        return cuda_fail(e, "k_state_fresh");
+    }
+    *out = st;
+    return SPK_OK;
+}
+
+int spk_stream_push(spk_stream* st, const void* d_planes, size_t plane_pitch, int64_t frames,
+                    spk_event** d_events, uint64_t** d_offsets, uint64_t* total, void* stream) {
+    if (!st || !d_events || !d_offsets || !total) return fail(SPK_EINVAL, "spk_stream_push: null argument");
+    spk_geom g{st->width, st->height, frames, plane_pitch};
+    int rc = check_geom(&g, true);
+    if (rc) return rc;
+    if (st->frames + frames >= (int64_t)1 << 29) return fail(SPK_EINVAL, "spk_stream_push: frames must stay < 2^29");
+    if (frames > 0 && !d_planes) return fail(SPK_EINVAL, "spk: null device buffer");
+    cudaStream_t s = as_stream(stream);
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    const int64_t npix = st->npix;
+    Scratch state_out(s), counts(s), last(s), mx(s);
+    SPK_CK(state_out.alloc((size_t)Scan<kFSR>::kFields * npix * sizeof(int32_t)));
+    SPK_CK(counts.alloc((size_t)npix * sizeof(uint32_t)));
+    SPK_CK(last.alloc((size_t)npix * sizeof(int32_t)));
+    SPK_CK(mx.alloc(sizeof(uint32_t)));
+    // the block's run lists (capacity grown once if any pixel needs more)
+    int cap = (int)std::max<int64_t>(64, frames / 32);
+    Scratch runs(s);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        if (runs.p) {
+            cudaFreeAsync(runs.p, s);
+            runs.p = nullptr;
+        }
+        SPK_CK(runs.alloc((size_t)npix * cap * sizeof(spk_run)));
+        if (frames > 0) {
+            SegArgs a;
+            a.planes = d_planes;
+            a.pitch = plane_pitch;
+            a.npix = npix;
+            a.frames = (int)frames;
+            a.cap = cap;
+            a.nchunks = (int)((frames + kChunk - 1) / kChunk);
+            a.runs = static_cast<spk_run*>(runs.p);
+            a.counts = static_cast<uint32_t*>(counts.p);
+            a.last = static_cast<int32_t*>(last.p);
+            a.state_in = st->state;
+            a.state_out = static_cast<int32_t*>(state_out.p);
+            if ((rc = launch_segment(SPK_FSR, a, s))) return rc;
+        } else {
+            SPK_CK(cudaMemsetAsync(counts.p, 0, (size_t)npix * sizeof(uint32_t), s));
+            SPK_CK(cudaMemcpyAsync(state_out.p, st->state, (size_t)Scan<kFSR>::kFields * npix * sizeof(int32_t),
+                                   cudaMemcpyDeviceToDevice, s));
+        }
+        SPK_CK(cudaMemsetAsync(mx.p, 0, sizeof(uint32_t), s));
+        k_max_u32<<<148, 256, 0, s>>>(static_cast<uint32_t*>(counts.p), npix, static_cast<uint32_t*>(mx.p));
+        SPK_LAUNCHED("k_max_u32");
+        uint32_t need = 0;
+        SPK_CK(cudaMemcpyAsync(&need, mx.p, sizeof(need), cudaMemcpyDeviceToHost, s));
+        SPK_CK(cudaStreamSynchronize(s));
+        if (need <= (uint32_t)cap) break;
+        cap = (int)need;
+    }
+    StreamArgs a{};
+    a.npix = npix;
+    a.frame0 = st->frames;
+    a.flush = 0;
+    a.state_in = st->state;
+    a.state_out = static_cast<int32_t*>(state_out.p);
+    a.runs = static_cast<spk_run*>(runs.p);
+    a.cap = cap;
+    a.counts = static_cast<uint32_t*>(counts.p);
+    a.last_value = st->last_value;
+    if ((rc = stream_events(st, a, d_events, d_offsets, total, s))) return rc;
+    // the end state, in the next block's frames, becomes the stream's state
+    k_stream_shift<<<(unsigned)((npix + 255) / 256), 256, 0, s>>>(static_cast<int32_t*>(state_out.p), npix,
+                                                                 (int)frames);
+    SPK_LAUNCHED("k_stream_shift");
+    SPK_CK(cudaMemcpyAsync(st->state, state_out.p, (size_t)Scan<kFSR>::kFields * npix * sizeof(int32_t),
+                           cudaMemcpyDeviceToDevice, s));
+    st->frames += frames;
+    return SPK_OK;
+}
+
+int spk_stream_flush(spk_stream* st, spk_event** d_events, uint64_t** d_offsets, uint64_t* total,
+                     void* stream) {
+    if (!st || !d_events || !d_offsets || !total) return fail(SPK_EINVAL, "spk_stream_flush: null argument");
+    cudaStream_t s = as_stream(stream);
+    StreamArgs a{};
+    a.npix = st->npix;
+    a.frame0 = st->frames;
+    a.flush = 1;
+    a.state_in = st->state;
+    a.last_value = st->last_value;
+    return stream_events(st, a, d_events, d_offsets, total, s);
+}
+
+namespace {
+
+// device events / offsets of one stream call -> malloc'd host copies
+int stream_to_host(spk_stream* st, spk_event* d_ev, uint64_t* d_offs, uint64_t tot, spk_event** h_events,
+                   uint64_t** h_offsets, cudaStream_t s) {
+    const size_t ob = (size_t)(st->npix + 1) * sizeof(uint64_t), eb = (size_t)tot * sizeof(spk_event);
+    *h_offsets = static_cast<uint64_t*>(std::malloc(ob));
+    *h_events = static_cast<spk_event*>(std::malloc(std::max<size_t>(eb, 16)));
+    int rc = SPK_OK;
+    if (!*h_offsets || !*h_events) rc = fail(SPK_ENOMEM, "spk_stream: host allocation failed");
+    cudaError_t e = cudaSuccess;
+    if (!rc) e = cudaMemcpyAsync(*h_offsets, d_offs, ob, cudaMemcpyDeviceToHost, s);
+    if (!rc && e == cudaSuccess && eb) e = cudaMemcpyAsync(*h_events, d_ev, eb, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(d_ev, s);
+    cudaFreeAsync(d_offs, s);
+    const cudaError_t se = cudaStreamSynchronize(s);
+    if (!rc && e != cudaSuccess) rc = cuda_fail(e, "spk_stream: copy to host");
+    if (!rc && se != cudaSuccess) rc = cuda_fail(se, "cudaStreamSynchronize");
+    if (rc) {
+        std::free(*h_offsets);
+        std::free(*h_events);
+        *h_offsets = nullptr;
+        *h_events = nullptr;
+    }
+    return rc;
+}
+
+}  // namespace
+
+int spk_stream_push_host(spk_stream* st, const void* h_payload, int64_t frames, spk_event** h_events,
+                         uint64_t** h_offsets, uint64_t* total) {
+    if (!st || !h_events || !h_offsets || !total || (frames > 0 && !h_payload))
+        return fail(SPK_EINVAL, "spk_stream_push_host: null argument");
+    spk_geom g{st->width, st->height, frames, spk_plane_pitch(st->width, st->height)};
+    int rc = check_geom(&g, true);
+    if (rc) return rc;
+    cudaStream_t s;
+    SPK_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    rc = [&]() -> int {
+        Scratch planes(s);
+        SPK_CK(planes.alloc(g.plane_pitch * (size_t)std::max<int64_t>(1, frames)));
+        int r = spk_upload_planes(&g, h_payload, plane_bytes(&g), 0, planes.p, s);
+        if (r) return r;
+        spk_event* dev = nullptr;
+        uint64_t* doffs = nullptr;
+        r = spk_stream_push(st, planes.p, g.plane_pitch, frames, &dev, &doffs, total, s);
+        if (r) return r;
+        return stream_to_host(st, dev, doffs, *total, h_events, h_offsets, s);
+    }();
+    cudaStreamDestroy(s);
+    return rc;
+}
+
+int spk_stream_flush_host(spk_stream* st, spk_event** h_events, uint64_t** h_offsets, uint64_t* total) {
+    if (!st || !h_events || !h_offsets || !total) return fail(SPK_EINVAL, "spk_stream_flush_host: null argument");
+    cudaStream_t s;
+    SPK_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    spk_event* dev = nullptr;
+    uint64_t* doffs = nullptr;
+    int rc = spk_stream_flush(st, &dev, &doffs, total, s);
+    if (!rc) rc = stream_to_host(st, dev, doffs, *total, h_events, h_offsets, s);
+    cudaStreamDestroy(s);
+    return rc;
+}
+
+int64_t spk_stream_frames(const spk_stream* st) { return st ? st->frames : -1; }
+
+int spk_stream_destroy(spk_stream* st) {
+    if (!st) return SPK_OK;
+    cudaFree(st->state);
+    cudaFree(st->last_value);
+    delete st;
+    return SPK_OK;
+}
+
 int spk_set_run_capacity(int64_t per_pixel) {
     if (per_pixel < 0 || per_pixel > INT_MAX) return fail(SPK_EINVAL, "spk: bad run capacity");
     g_run_cap.store(per_pixel);

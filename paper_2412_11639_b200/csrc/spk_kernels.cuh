@@ -12,6 +12,7 @@ namespace spk {
 using spk_run_t = ::spk_run;
 using spk_sync_t = ::spk_sync;
 using spk_close_t = ::spk_close;
+using spk_event_t = ::spk_event;
 
 // K2 block = 8 warps = 256 pixels = one 32-byte sector of every plane row;
 // the warps share each sector through L2, so they are kept within kDrift
@@ -165,6 +166,26 @@ struct RecArgs {
     int width, height;
     uint32_t fps;
 };
+
+// streaming FSR (stream.cu)
+struct StreamArgs {
+    int64_t npix;
+    int64_t frame0;           // absolute frame of the block start (flush: frames pushed)
+    int flush;
+    const int32_t* state_in;  // state before the block (flush: the final state)
+    const int32_t* state_out; // state after the block
+    const spk_run_t* runs;    // the block's run lists (K2 with state_in)
+    int cap;
+    const uint32_t* counts;
+    uint32_t* ecount;                 // events per pixel
+    const unsigned long long* eoffs;  // exclusive prefix of ecount
+    spk_event_t* events;
+    double* last_value;       // per pixel: intensity of the last closed run
+};
+__global__ void k_stream_count(StreamArgs a);
+__global__ void k_stream_write(StreamArgs a);
+__global__ void k_stream_shift(int32_t* st, int64_t npix, int frames);
+__global__ void k_max_u32(const uint32_t* v, int64_t n, uint32_t* out);
 
 template <int METHOD>
 __global__ void k_segment(SegArgs a);

@@ -205,6 +205,42 @@ static void gpucheck() {
             EXPECT(j < f.size() && f[j].start_frame <= seg.start_frame && seg.end_frame <= f[j].end_frame);
         }
     }
+    // streaming form: PixelReconState events == fsr_events (reconstruct.hpp:46-50),
+    // flush yields the open spans; EventStream gives the same per pixel in blocks
+    {
+        std::mt19937 rng(11);
+        for (int trial = 0; trial < 12; ++trial) {
+            const int t = 50 + trial * 37;
+            std::vector<int> bits(t);
+            std::bernoulli_distribution b(0.05 + 0.07 * (trial % 5));
+            for (int& x : bits) x = b(rng) ? 1 : 0;
+            if (trial == 0) std::fill(bits.begin(), bits.end(), 0);
+            const SpikeLikeStream st(bits, 1, 0);
+            PixelReconState ps;
+            std::vector<SegmentEvent> got;
+            for (int x : bits)
+                if (auto e = ps.push_frame(x != 0)) got.push_back(*e);
+            for (const auto& e : ps.flush()) got.push_back(e);
+            EXPECT(ps.frames_seen() == t);
+            EXPECT(got == fsr_events(st));
+        }
+        EventStream es(11, 6);
+        std::vector<std::vector<SegmentEvent>> per(66);
+        const PackedSpikes pk = pack(vol);
+        const size_t fb = (66 + 7) / 8;
+        for (long f0 = 0; f0 < 300; f0 += 70) {
+            const long n = std::min<long>(70, 300 - f0);
+            std::vector<uint8_t> blk(pk.payload.begin() + f0 * fb, pk.payload.begin() + (f0 + n) * fb);
+            auto ev = es.push(blk, n);
+            for (int p = 0; p < 66; ++p) per[p].insert(per[p].end(), ev[p].begin(), ev[p].end());
+        }
+        auto ev = es.flush();
+        EXPECT(es.frames() == 300);
+        for (int p = 0; p < 66; ++p) {
+            per[p].insert(per[p].end(), ev[p].begin(), ev[p].end());
+            EXPECT(per[p] == fsr_events(pixel_stream(vol, p % 11, p / 11)));
+        }
+    }
     // errors surface as the reference's exceptions
     EXPECT(throws<std::invalid_argument>([&] { reconstruct(vol, ReconMethod{Method::tfp, 0}); }));
     EXPECT(reconstruct(SpikeVolume(3, 2, 0), ReconMethod{}).empty());
