@@ -282,3 +282,32 @@ def test_c1_static_full_size(oracle):
 def test_c2_moving_full_size(oracle):
     """configs[1]: 400x250x40000 moving texture + occluding bar."""
     full_size_check(oracle, "moving", 400, 250, 40000, 0, [0, 37000, 99200])
+
+
+def test_c3_sensor_full_size(oracle):
+    """configs[2]: 1000x1000x20000 sensor with slow illumination (1M pixels:
+    the pixel-part pipeline of the C-ABI) -- exact oracle parity on tiles and
+    run-interval sums everywhere (u8 only: f64 frames would be 160 GB)."""
+    w, h, t = 1000, 1000, 20000
+    v = spk.synth("sensor", 0, w, h, t)
+    host = v.planes.cpu().numpy()
+    npix = w * h
+    for tag in ("fsr", "ssr"):
+        m, _ = TAGS[tag]
+        u8 = run(v, method_of(tag)).reshape(t, npix)
+        for p0 in (0, 524_000, 999_200):  # first part, across the part split, last pixels
+            p1 = min(npix, p0 + 800)
+            want = oracle.reconstruct(host, w, h, t, v.pitch, m, pix_begin=p0, pix_end=p1)
+            assert np.array_equal(u8[:, p0:p1].cpu().numpy(), want), (tag, p0)
+        del u8
+        runs, counts, last = spk.segments(v, method_of(tag), run_cap=256)
+        spikes = torch.zeros(npix, dtype=torch.int64, device="cuda")
+        for f0 in range(0, t, 2000):  # chunked: a whole-volume int64 cast is 160 GB
+            sub = spk.PackedVolume(w, h, min(t, f0 + 2000) - f0, v.planes[f0:f0 + 2000])
+            spikes += sub.to_bytes().reshape(-1, npix).sum(0, dtype=torch.int32)
+        mask = torch.arange(256, device="cuda")[None, :] < counts[:, None].clamp(max=256)
+        tot = (runs[..., 1].to(torch.int64) * mask).sum(1)
+        ok = counts <= 256
+        assert int(ok.sum()) > npix * 0.99
+        assert torch.equal(tot[ok], (spikes - 1).clamp(min=0)[ok]), tag
+        del runs, counts, last, spikes, mask, tot
