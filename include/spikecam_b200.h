@@ -279,6 +279,44 @@ int spk_last_timing(float* segment_ms, float* finalize_ms, float* expand_ms, flo
 const char* spk_last_error(void);
 int spk_version(void);
 
+/* ---- quality metrics and the stability check ------- */
+/* Per-frame metrics of a reconstruction on the device, replacing the
+ * per-image loops of the CLI's `compare` (proj/tools/spikecam_main.cpp:
+ * 263-299): d_te[n] = two_dimensional_entropy of frame n
+ * (proj/src/metrics.cpp:12-43) and, when d_ref is given, d_mse[n] = mse of
+ * frame n against the uint8 reference image n (metrics.cpp:45-55; psnr is
+ * 10*log10(255^2/mse), 57-61).  Frames are [g->frames][pitch] elements of
+ * frame_type (SPK_OUT_U8: quantized values, as the entropy uses them;
+ * SPK_OUT_F32 / SPK_OUT_F64: values, quantized for the entropy with
+ * round(clamp(v, 0, 255))); reference images are [g->frames][ref_pitch]
+ * bytes.  Either output may be null.  Entropy needs W, H >= 3 (SPK_EINVAL,
+ * the reference's invalid_argument).  Sums are reduced in a fixed order:
+ * deterministic, equal to the reference's sequential sums up to double
+ * rounding (tests hold them to 1e-12 relative). */
+int spk_frame_metrics(const spk_geom* g, const void* d_frames, int frame_type, size_t pitch,
+                      const uint8_t* d_ref, size_t ref_pitch, double* d_te, double* d_mse,
+                      void* stream);
+
+/* stability_order (proj/src/stability.cpp:61-128) of one pixel stream:
+ * depth of the shallowest zero-order violation (0: none; 1 = S1), its index
+ * in that sequence, its '-'/'+' path (bit j = branch j+1 -> j+2, '+' = 1;
+ * path_len = depth - 1 characters), verified_order and absolute. */
+typedef struct spk_stab {
+    int32_t depth;
+    int32_t verified_order;
+    int32_t absolute;
+    int32_t path_len;
+    int64_t index;
+    uint64_t path;
+} spk_stab;
+/* stability_order of every pixel of a packed volume (the per-pixel loop of
+ * `verify-stability --in`, spikecam_main.cpp:189-207), d_out[p] for p =
+ * y*W + x.  max_depth in [1, 63] (SPK_EINVAL otherwise; the reference
+ * rejects < 1).  Synchronous with respect to `stream` (it sizes per-pixel
+ * scratch from the spike counts). */
+int spk_stability(const spk_geom* g, const void* d_planes, int max_depth, spk_stab* d_out,
+                  void* stream);
+
 /* ---- synthetic inputs (benchmark / test harness, not the hot path) -------- */
 /* Integrate-and-fire streams (threshold 1, subtractive reset, uniform initial
  * residual; proj/src/simulator.cpp:41-68) of the BASELINE.json configs:

@@ -61,6 +61,13 @@ class Oracle:
         h.orc_fsr_events.argtypes = [_P, _L, _P, _P, _L]
         h.orc_encode.restype = _L
         h.orc_encode.argtypes = [_L, C.c_double, _P, _L]
+        h.orc_te_u8.restype = C.c_double
+        h.orc_te_u8.argtypes = [_P, C.c_int, C.c_int]
+        h.orc_te_f64.restype = C.c_double
+        h.orc_te_f64.argtypes = [_P, C.c_int, C.c_int]
+        h.orc_mse.restype = C.c_double
+        h.orc_mse.argtypes = [_P, _P, _L]
+        h.orc_stability.argtypes = [_P, _L, C.c_int, _P, C.c_char_p, _L]
         self.h = h
 
     # framing
@@ -150,6 +157,29 @@ class Oracle:
         return b"".join(out)
 
     # volumes (planes: [T, pitch] uint8, LSB-first)
+    # quality metrics and the stability check (metrics.cpp:12-61, stability.cpp:61-128)
+    def te(self, frame: np.ndarray) -> float:
+        """two_dimensional_entropy of one [H, W] frame (uint8 = quantized, or doubles)."""
+        f = np.ascontiguousarray(frame)
+        hh, ww = f.shape
+        if f.dtype == np.uint8:
+            return float(self.h.orc_te_u8(_ptr(f), ww, hh))
+        f = f.astype(np.float64)
+        return float(self.h.orc_te_f64(_ptr(f), ww, hh))
+
+    def mse(self, a: np.ndarray, b: np.ndarray) -> float:
+        a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+        b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+        return float(self.h.orc_mse(_ptr(a), _ptr(b), a.size))
+
+    def stability(self, bits: np.ndarray, depth: int = 8) -> dict:
+        bits = np.ascontiguousarray(bits, dtype=np.uint8)
+        out = np.zeros(4, np.int64)
+        path = C.create_string_buffer(64)
+        if self.h.orc_stability(_ptr(bits), bits.size, depth, _ptr(out), path, 64):
+            raise ValueError("stability_order: max_depth must be in [1, 60]")
+        return _stab_result(out, path)
+
     def reconstruct(self, planes: np.ndarray, w: int, h: int, t: int, pitch: int, method: int,
                     window: int = 32, dtype=np.uint8, pix_begin: int = 0,
                     pix_end: int | None = None, threads: int = 0) -> np.ndarray:
@@ -163,6 +193,11 @@ class Oracle:
         if rc != 0:
             raise ValueError("bad method/window")
         return out
+
+
+def _stab_result(out, path):
+    return {"depth": int(out[0]), "index": int(out[1]), "verified_order": int(out[2]),
+            "absolute": bool(out[3]), "path": path.value.decode()}
 
 
 class Reference:
@@ -210,6 +245,14 @@ class Reference:
         h.ref_emit_records.restype = _L
         h.ref_emit_records.argtypes = [_P, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int,
                                        C.c_uint32, C.c_char_p]
+        for f in (h.ref_te,):
+            f.restype = C.c_double
+            f.argtypes = [_P, C.c_int, C.c_int]
+        for f in (h.ref_mse, h.ref_psnr):
+            f.restype = C.c_double
+            f.argtypes = [_P, _P, C.c_int, C.c_int]
+        h.ref_stability.restype = _L
+        h.ref_stability.argtypes = [_P, _L, C.c_int, _P, C.c_char_p, _L]
         self.h = h
 
     def _err(self):
@@ -315,6 +358,33 @@ class Reference:
         planes = np.ascontiguousarray(planes, dtype=np.uint8)
         if self.h.ref_emit_records(_ptr(planes), pitch, w, h, t, method, fps, str(path).encode()) < 0:
             raise ValueError(self._err())
+
+
+    def te(self, values: np.ndarray) -> float:
+        """two_dimensional_entropy of one [H, W] image of doubles."""
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        r = self.h.ref_te(_ptr(v), v.shape[1], v.shape[0])
+        if np.isnan(r):
+            raise ValueError(self._err())
+        return float(r)
+
+    def mse(self, a: np.ndarray, b: np.ndarray) -> float:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        return float(self.h.ref_mse(_ptr(a), _ptr(b), a.shape[1], a.shape[0]))
+
+    def psnr(self, a: np.ndarray, b: np.ndarray) -> float:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        return float(self.h.ref_psnr(_ptr(a), _ptr(b), a.shape[1], a.shape[0]))
+
+    def stability(self, bits: np.ndarray, depth: int = 8) -> dict:
+        bits = np.ascontiguousarray(bits, dtype=np.uint8)
+        out = np.zeros(4, np.int64)
+        path = C.create_string_buffer(256)
+        if self.h.ref_stability(_ptr(bits), bits.size, depth, _ptr(out), path, 256) < 0:
+            raise ValueError(self._err())
+        return _stab_result(out, path)
 
 
 def ref_available() -> bool:

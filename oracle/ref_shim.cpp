@@ -22,6 +22,7 @@
 #include "spikecam/metrics.hpp"
 #include "spikecam/reconstruct.hpp"
 #include "spikecam/simulator.hpp"
+#include "spikecam/stability.hpp"
 
 using namespace spikecam;
 
@@ -295,6 +296,67 @@ long ref_emit_records(const uint8_t* planes, size_t pitch, int w, int h, int t, 
             }
         }
         write_spkr(rv, path);
+        return 0;
+    });
+}
+
+// ---- quality metrics and the stability check ----
+
+// two_dimensional_entropy (metrics.cpp:12-43) of a W x H image of doubles;
+// NaN on an error (message in ref_last_error).
+double ref_te(const double* values, int w, int h) {
+    double r = std::nan("");
+    guarded([&]() -> long {
+        IntensityImage im(w, h);
+        std::copy(values, values + static_cast<size_t>(w) * h, im.values.begin());
+        r = two_dimensional_entropy(im);
+        return 0;
+    });
+    return r;
+}
+
+// mse / psnr (metrics.cpp:45-61) of two W x H images of doubles
+double ref_mse(const double* a, const double* b, int w, int h) {
+    double r = std::nan("");
+    guarded([&]() -> long {
+        IntensityImage x(w, h), y(w, h);
+        std::copy(a, a + static_cast<size_t>(w) * h, x.values.begin());
+        std::copy(b, b + static_cast<size_t>(w) * h, y.values.begin());
+        r = mse(x, y);
+        return 0;
+    });
+    return r;
+}
+double ref_psnr(const double* a, const double* b, int w, int h) {
+    double r = std::nan("");
+    guarded([&]() -> long {
+        IntensityImage x(w, h), y(w, h);
+        std::copy(a, a + static_cast<size_t>(w) * h, x.values.begin());
+        std::copy(b, b + static_cast<size_t>(w) * h, y.values.begin());
+        r = psnr(x, y);
+        return 0;
+    });
+    return r;
+}
+
+// stability_order (stability.cpp:112-128) of one pixel row.  out[0] =
+// violation depth (0: none), out[1] = violation index, out[2] =
+// verified_order, out[3] = absolute; `path` receives the violation path
+// ('-'/'+', NUL-terminated, cap bytes).  Returns 0 or -1.
+long ref_stability(const uint8_t* bits, long frames, int depth, long* out, char* path,
+                   long cap) {
+    return guarded([&]() -> long {
+        StabilityReport r = stability_order(stream_of(bits, frames), depth);
+        out[0] = r.first_violation ? r.first_violation->depth : 0;
+        out[1] = r.first_violation ? static_cast<long>(r.first_violation->index) : 0;
+        out[2] = r.verified_order;
+        out[3] = r.absolute ? 1 : 0;
+        const std::string p = r.first_violation ? r.first_violation->path : std::string();
+        if (cap > 0) {
+            const size_t n = std::min(p.size(), static_cast<size_t>(cap - 1));
+            std::memcpy(path, p.data(), n);
+            path[n] = 0;
+        }
         return 0;
     });
 }

@@ -434,3 +434,158 @@ long orc_encode(long duration, double intensity, uint16_t* words, long cap) {
     if (nw < cap) words[nw] = (uint16_t)((unsigned)duration << 8 | q);
     return nw + 1;
 }
+
+/* ---- quality metrics and the stability check ---- */
+
+double orc_te_u8(const uint8_t* q, int w, int h) {
+    /* two_dimensional_entropy, proj/src/metrics.cpp:12-43, on the already
+     * quantized image (q = round(clamp(v, 0, 255)), line 18): histogram of
+     * (gray, lround(3x3 sum / 9)) over interior pixels, entropy summed over
+     * bins in index order.  NaN for images smaller than 3x3 (line 13). */
+    if (w < 3 || h < 3) return NAN;
+    long* hist = (long*)calloc(256 * 256, sizeof(long));
+    long total = 0;
+    for (int y = 1; y < h - 1; ++y)
+        for (int x = 1; x < w - 1; ++x) {
+            long sum = 0;
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) sum += q[(size_t)(y + dy) * w + (x + dx)];
+            const int gbar = (int)lround((double)sum / 9.0);
+            ++hist[(size_t)q[(size_t)y * w + x] * 256 + gbar];
+            ++total;
+        }
+    double e = 0.0;
+    for (int i = 0; i < 256 * 256; ++i) {
+        if (!hist[i]) continue;
+        const double p = (double)hist[i] / (double)total;
+        e -= p * log2(p);
+    }
+    free(hist);
+    return e;
+}
+
+double orc_te_f64(const double* v, int w, int h) {
+    if (w < 3 || h < 3) return NAN;
+    uint8_t* q = (uint8_t*)malloc((size_t)w * h);
+    for (size_t i = 0; i < (size_t)w * h; ++i) q[i] = orc_quantize(v[i]);
+    const double e = orc_te_u8(q, w, h);
+    free(q);
+    return e;
+}
+
+double orc_mse(const double* a, const double* b, long n) {
+    /* mse, metrics.cpp:45-55: sequential sum of squared differences / n */
+    double acc = 0.0;
+    for (long i = 0; i < n; ++i) {
+        const double d = a[i] - b[i];
+        acc += d * d;
+    }
+    return acc / (double)n;
+}
+
+/* interval_stream(values, firing), proj/src/stability.cpp:93-106 */
+static long gaps_of(const int* v, long n, int firing, int* out) {
+    long last = -1, m = 0;
+    for (long i = 0; i < n; ++i) {
+        if (v[i] != firing) continue;
+        if (last >= 0) out[m++] = (int)(i - last);
+        last = i;
+    }
+    return m;
+}
+
+/* first_violation_index, stability.cpp:41-59 (-1: stable) */
+static long first_violation(const int* v, long n) {
+    int have_a = 0, have_b = 0, a = 0, b = 0;
+    for (long i = 0; i < n; ++i) {
+        const int x = v[i];
+        if (!have_a) {
+            a = x;
+            have_a = 1;
+        } else if (x == a || (have_b && x == b)) {
+        } else if (!have_b && abs(x - a) == 1) {
+            b = x;
+            have_b = 1;
+        } else {
+            return i;
+        }
+    }
+    return -1;
+}
+
+typedef struct {
+    int max_depth, deepest_ok, truncated;
+    int vdepth;  /* 0: no violation */
+    long vindex;
+    char vpath[64];
+} orc_tree;
+
+/* explore, stability.cpp:61-91: depth-first, '-' (smaller firing value) first */
+static void explore(const int* seq, long n, int depth, char* path, orc_tree* st) {
+    if (st->vdepth && st->vdepth <= depth) return;
+    if (n == 0) {
+        if (depth > st->deepest_ok) st->deepest_ok = depth;
+        return;
+    }
+    const long bad = first_violation(seq, n);
+    if (bad >= 0) {
+        if (!st->vdepth || depth < st->vdepth) {
+            st->vdepth = depth;
+            st->vindex = bad;
+            strcpy(st->vpath, path);
+        }
+        return;
+    }
+    if (depth > st->deepest_ok) st->deepest_ok = depth;
+    int lo = seq[0], hi = seq[0];
+    for (long i = 1; i < n; ++i) {
+        if (seq[i] < lo) lo = seq[i];
+        if (seq[i] > hi) hi = seq[i];
+    }
+    if (lo == hi) return;
+    if (depth >= st->max_depth) {
+        st->truncated = 1;
+        return;
+    }
+    int* child = (int*)malloc((size_t)n * sizeof(int));
+    for (int br = 0; br < 2; ++br) {
+        const long m = gaps_of(seq, n, br ? hi : lo, child);
+        const size_t k = strlen(path);
+        path[k] = br ? '+' : '-';
+        path[k + 1] = 0;
+        explore(child, m, depth + 1, path, st);
+        path[k] = 0;
+    }
+    free(child);
+}
+
+int orc_stability(const uint8_t* bits, long frames, int max_depth, long* out, char* path,
+                  long cap) {
+    /* stability_order, stability.cpp:112-128, of a pixel stream
+     * (pixel_stream, core.cpp:109-118: firing value 1) */
+    if (max_depth < 1 || max_depth > 60) return -1;
+    int* s1 = (int*)malloc((size_t)(frames > 0 ? frames : 1) * sizeof(int));
+    long m = 0, last = -1;
+    for (long i = 0; i < frames; ++i) {
+        if (!bits[i]) continue;
+        if (last >= 0) s1[m++] = (int)(i - last);
+        last = i;
+    }
+    orc_tree st;
+    memset(&st, 0, sizeof st);
+    st.max_depth = max_depth;
+    char buf[64] = {0};
+    explore(s1, m, 1, buf, &st);
+    free(s1);
+    out[0] = st.vdepth;
+    out[1] = st.vdepth ? st.vindex : 0;
+    out[2] = st.vdepth ? st.vdepth - 1 : (st.truncated ? max_depth : st.deepest_ok);
+    out[3] = st.vdepth ? 0 : !st.truncated;
+    if (cap > 0) {
+        const char* p = st.vdepth ? st.vpath : "";
+        const size_t k = strlen(p) < (size_t)(cap - 1) ? strlen(p) : (size_t)(cap - 1);
+        memcpy(path, p, k);
+        path[k] = 0;
+    }
+    return 0;
+}

@@ -72,6 +72,20 @@ long orc_fsr_events(const uint8_t* bits, long frames, long* duration, double* in
 /* 16-bit record codec (proj/src/codec.cpp:8-42). Returns words written or -1. */
 long orc_encode(long duration, double intensity, uint16_t* words, long cap);
 
+/* Quality metrics (proj/src/metrics.cpp:12-61): two_dimensional_entropy of a
+ * W x H image (from its quantized uint8 values, or from doubles), NaN when
+ * smaller than 3x3; mse of two n-value images. */
+double orc_te_u8(const uint8_t* q, int width, int height);
+double orc_te_f64(const double* values, int width, int height);
+double orc_mse(const double* a, const double* b, long n);
+
+/* stability_order (proj/src/stability.cpp:61-128) of one pixel row:
+ * out[0] = depth of the first violation (0: none), out[1] = its index,
+ * out[2] = verified_order, out[3] = absolute; `path` gets the violation's
+ * '-'/'+' path.  Returns 0, or -1 for max_depth outside [1, 60]. */
+int orc_stability(const uint8_t* bits, long frames, int max_depth, long* out, char* path,
+                  long cap);
+
 #ifdef __cplusplus
 }
 #endif

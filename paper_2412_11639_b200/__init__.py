@@ -24,6 +24,8 @@ from .recon import (  # noqa: F401
     write_spk,
 )
 from .stream import EventStream  # noqa: F401
+from .metrics import (  # noqa: F401
+    compare, frame_metrics, mse, psnr, stability, two_dimensional_entropy, verify_stability)
 from .records import RecordVolume, decode, read_spkr, records, records_host, write_spkr  # noqa: F401
 from ._capi import LIB_PATH, SpikecamError  # noqa: F401
 

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "spk_common.cuh"
 #include "spk_fsm.cuh"
@@ -1276,6 +1277,104 @@ int spk_last_timing(float* segment_ms, float* finalize_ms, float* expand_ms, flo
 const char* spk_last_error(void) { return g_err.c_str(); }
 
 int spk_version(void) { return 100; }
+
+// ---- quality metrics and the stability check (metrics.cu) ----
+int spk_frame_metrics(const spk_geom* g, const void* d_frames, int frame_type, size_t pitch,
+                      const uint8_t* d_ref, size_t ref_pitch, double* d_te, double* d_mse,
+                      void* stream) {
+    int rc = check_geom(g, false);
+    if (rc) return rc;
+    if (frame_type != SPK_OUT_U8 && frame_type != SPK_OUT_F32 && frame_type != SPK_OUT_F64)
+        return fail(SPK_EINVAL, "spk_frame_metrics: bad frame_type");
+    if (d_te && (g->width < 3 || g->height < 3))
+        return fail(SPK_EINVAL, "two_dimensional_entropy: image must be at least 3x3");
+    if (d_mse && !d_ref) return fail(SPK_EINVAL, "spk_frame_metrics: mse needs reference images");
+    const int64_t npix = npix_of(g);
+    if (g->frames == 0 || (!d_te && !d_mse)) return SPK_OK;
+    if (!d_frames) return fail(SPK_EINVAL, "spk: null device buffer");
+    if (pitch < (size_t)npix || (d_mse && ref_pitch < (size_t)npix))
+        return fail(SPK_EINVAL, "spk_frame_metrics: pitch must be >= W*H");
+    cudaStream_t s = as_stream(stream);
+    MetArgs a;
+    a.frames = d_frames;
+    a.pitch = (int64_t)pitch;
+    a.ref = d_ref;
+    a.ref_pitch = (int64_t)ref_pitch;
+    a.width = g->width;
+    a.height = g->height;
+    a.te = d_te;
+    a.mse = d_mse;
+    const size_t smem = d_te ? (size_t)kMetHalf * sizeof(uint32_t) : 0;
+    auto go = [&](auto kern) -> int {
+        SPK_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)((size_t)kMetHalf * sizeof(uint32_t))));
+        kern<<<(unsigned)g->frames, kMetThreads, smem, s>>>(a);
+        SPK_LAUNCHED("k_frame_metrics");
+        return SPK_OK;
+    };
+    return frame_type == SPK_OUT_U8    ? go(k_frame_metrics<uint8_t>)
+           : frame_type == SPK_OUT_F32 ? go(k_frame_metrics<float>)
+                                       : go(k_frame_metrics<double>);
+}
+
+int spk_stability(const spk_geom* g, const void* d_planes, int max_depth, spk_stab* d_out,
+                  void* stream) {
+    int rc = check_geom(g, true);
+    if (rc) return rc;
+    if (max_depth < 1 || max_depth > kStabMaxDepth)
+        return fail(SPK_EINVAL, "stability_order: max_depth must be in [1, 63]");
+    if (!d_out || (g->frames > 0 && !d_planes)) return fail(SPK_EINVAL, "spk: null device buffer");
+    const int64_t npix = npix_of(g);
+    cudaStream_t s = as_stream(stream);
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    Scratch cnt(s);
+    SPK_CK(cnt.alloc((size_t)npix * sizeof(uint32_t)));
+    StabArgs a;
+    a.planes = d_planes;
+    a.pitch = g->plane_pitch;
+    a.npix = npix;
+    a.frames = g->frames;
+    a.max_depth = max_depth;
+    a.count = static_cast<uint32_t*>(cnt.p);
+    a.out = d_out;
+    k_stab_count<<<(unsigned)((npix + 255) / 256), 256, 0, s>>>(a);
+    SPK_LAUNCHED("k_stab_count");
+    std::vector<uint32_t> hc((size_t)npix);
+    SPK_CK(cudaMemcpyAsync(hc.data(), cnt.p, (size_t)npix * sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, s));
+    SPK_CK(cudaStreamSynchronize(s));
+    // per-pixel stack of sequences: a child is at most its parent's length,
+    // and the deepest level is max_depth, so max_depth * |S1| ints suffice
+    constexpr int64_t kBudget = (int64_t)1 << 30;  // scratch ints per batch (4 GB)
+    for (int64_t p0 = 0; p0 < npix;) {
+        std::vector<int64_t> offs;
+        int64_t tot = 0, p1 = p0;
+        while (p1 < npix) {
+            const int64_t len = hc[(size_t)p1] > 1 ? (int64_t)hc[(size_t)p1] - 1 : 0;
+            const int64_t need = (int64_t)max_depth * len + 1;
+            if (p1 > p0 && tot + need > kBudget) break;
+            offs.push_back(tot);
+            tot += need;
+            ++p1;
+        }
+        Scratch doffs(s), scr(s);
+        SPK_CK(doffs.alloc(offs.size() * sizeof(int64_t)));
+        SPK_CK(scr.alloc((size_t)tot * sizeof(int32_t)));
+        SPK_CK(cudaMemcpyAsync(doffs.p, offs.data(), offs.size() * sizeof(int64_t),
+                               cudaMemcpyHostToDevice, s));
+        a.pix0 = p0;
+        a.nbatch = p1 - p0;
+        a.offs = static_cast<const int64_t*>(doffs.p);
+        a.scratch = static_cast<int32_t*>(scr.p);
+        k_stab<<<(unsigned)((a.nbatch + 127) / 128), 128, 0, s>>>(a);
+        SPK_LAUNCHED("k_stab");
+        SPK_CK(cudaStreamSynchronize(s));  // `offs` is pageable host memory
+        p0 = p1;
+    }
+    return SPK_OK;
+}
 
 int spk_synth(int scene, uint64_t seed, const spk_geom* g, int64_t frame0, double param,
               void* d_planes, void* stream) {

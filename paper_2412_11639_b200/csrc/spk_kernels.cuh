@@ -13,6 +13,7 @@ using spk_run_t = ::spk_run;
 using spk_sync_t = ::spk_sync;
 using spk_close_t = ::spk_close;
 using spk_event_t = ::spk_event;
+using spk_stab_t = ::spk_stab;
 
 // K2 block = 8 warps = 256 pixels = one 32-byte sector of every plane row;
 // the warps share each sector through L2, so they are kept within kDrift
@@ -222,6 +223,36 @@ __global__ void k_scan_add(T* out, const T* sums, int64_t n);
 constexpr int kScanBlock = 1024;
 template <int METHOD, typename OUT>
 __global__ void k_causal(CausalArgs a);
+
+// quality metrics / stability check (metrics.cu)
+constexpr int kMetThreads = 512;
+constexpr int kMetHalf = 128 * 256;  // histogram bins of one half (128 gray levels)
+constexpr int kStabMaxDepth = 63;    // violation paths are 64-bit masks
+struct MetArgs {
+    const void* frames;  // [frames][pitch] elements
+    int64_t pitch;
+    const uint8_t* ref;  // [frames][ref_pitch] uint8 reference images (mse)
+    int64_t ref_pitch;
+    int width, height;
+    double* te;   // per frame, or null
+    double* mse;  // per frame, or null (then `ref` is unused)
+};
+struct StabArgs {
+    const void* planes;
+    size_t pitch;
+    int64_t npix;
+    int64_t frames;
+    int max_depth;
+    uint32_t* count;        // k_stab_count: spikes per pixel
+    int64_t pix0, nbatch;   // k_stab: pixels [pix0, pix0 + nbatch)
+    const int64_t* offs;    // per batch pixel: region start (ints, exclusive prefix)
+    int32_t* scratch;       // the batch's regions (starting at offs[0])
+    spk_stab_t* out;        // per pixel (all npix)
+};
+template <typename IN>
+__global__ void k_frame_metrics(MetArgs a);
+__global__ void k_stab_count(StabArgs a);
+__global__ void k_stab(StabArgs a);
 
 __global__ void k_pack(const uint8_t* bytes, int64_t npix, int64_t frames, uint8_t* planes,
                        size_t pitch);

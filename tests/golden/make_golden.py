@@ -222,10 +222,69 @@ def main():
                         quant_out=pgm)
     print("formats.npz")
     save_records()
+    save_metrics()
+
+
+def stab_rows(bits_list, depth):
+    res = [REF.stability(b, depth) for b in bits_list]
+    arr = np.array([[r["depth"], r["index"], r["verified_order"], int(r["absolute"])]
+                    for r in res], np.int64)
+    return arr, np.array([r["path"] for r in res])
+
+
+def save_metrics():
+    """Quality metrics (two_dimensional_entropy / mse / psnr, metrics.cpp:12-61)
+    and stability_order (stability.cpp:112-128) from the reference library."""
+    data = {}
+    rng = np.random.default_rng(97)
+    imgs = {"rand9x13": rng.uniform(-5.0, 260.0, (9, 13)), "const3x3": np.full((3, 3), 77.25),
+            "ramp5x4": np.arange(20, dtype=np.float64).reshape(4, 5) * 12.75}
+    for k, v in imgs.items():
+        data[f"img/{k}"] = v
+        data[f"img/{k}/te"] = np.float64(REF.te(v))
+    # frames of the moving-bar volume: FSR values vs TFI frames as the reference images
+    g = np.load(OUT / "vol_bar64x48.npz")
+    planes = g["planes"]
+    w, h, t = (int(x) for x in g["geom"])
+    f, _ = REF.reconstruct(planes, planes.shape[1], w, h, t, 0, 32)
+    _, tfi = REF.reconstruct(planes, planes.shape[1], w, h, t, 2, 32)
+    f = f.reshape(t, h, w)
+    tfi = tfi.reshape(t, h, w).astype(np.float64)
+    data["bar/te_fsr"] = np.array([REF.te(f[n]) for n in range(t)])
+    data["bar/mse_fsr_tfi"] = np.array([REF.mse(f[n], tfi[n]) for n in range(t)])
+    data["bar/psnr_fsr_tfi"] = np.array([REF.psnr(f[n], tfi[n]) for n in range(t)])
+    # stability_order on the known-answer rows and a constant-rate sweep
+    # (cmd_verify_stability, spikecam_main.cpp:209-225: log-spaced q, length 2048)
+    cases = rows()
+    names = sorted(cases)
+    data["rows/names"] = np.array(names)
+    for depth in (1, 3, 8):
+        a, pth = stab_rows([cases[n] for n in names], depth)
+        data[f"rows/d{depth}"] = a
+        data[f"rows/d{depth}/path"] = pth
+    qs = 0.01 * (1.0 / 0.01) ** (np.arange(40) / 39.0)
+    sweep = [REF.simulate_pixel(np.full(2048, q)) for q in qs]
+    data["sweep/bits"] = np.stack(sweep)
+    a, pth = stab_rows(sweep, 8)
+    data["sweep/d8"] = a
+    data["sweep/d8/path"] = pth
+    # per-pixel reports of whole golden volumes (verify-stability --in)
+    for name, depth in (("bar64x48", 8), ("noise40x25", 8), ("par12x9", 4), ("odd9x1", 8)):
+        gv = np.load(OUT / f"vol_{name}.npz")
+        pl = gv["planes"]
+        w, h, t = (int(x) for x in gv["geom"])
+        bits = np.stack([(pl[:, p >> 3] >> (p & 7)) & 1 for p in range(w * h)]).astype(np.uint8)
+        a, pth = stab_rows(list(bits), depth)
+        data[f"vol/{name}/d{depth}"] = a
+        data[f"vol/{name}/d{depth}/path"] = pth
+    np.savez_compressed(OUT / "metrics.npz", **data)
+    print("metrics.npz")
 
 
 if __name__ == "__main__":
     if sys.argv[1:] == ["records"]:
         save_records()
+    elif sys.argv[1:] == ["metrics"]:
+        save_metrics()
     else:
         main()

@@ -188,3 +188,25 @@ extern "C" long batch_runs(const uint8_t* bits, long frames, int method, long* s
 extern "C" void host_run_u8(const uint32_t* n, const uint32_t* span, uint32_t* out, long m) {
     for (long i = 0; i < m; ++i) out[i] = spk::run_u8(n[i], span[i]);
 }
+
+// profiling aid: fsr_batch4 iterations and events (exact steps) for one pixel
+extern "C" void batch_iters(const uint8_t* bits, long frames, long* iters, long* events) {
+    const long ngroups = (frames + 31) / 32;
+    std::vector<uint32_t> words(ngroups + 4, 0u);
+    for (long f = 0; f < frames; ++f)
+        if (bits[f]) words[f / 32] |= 0x80000000u >> (f % 32);
+    spk::Scan<spk::kFSR> sc;
+    sc.init();
+    long wi = 0, it = 0, ev = 0;
+    int cpos = 0;
+    auto put = [&](bool, int, int) {};
+    while (wi < ngroups) {
+        const int k = spk::fsr_batch4(sc, words[wi], words[wi + 1], words[wi + 2], words[wi + 3],
+                                      (int)(wi * 32), cpos, put);
+        ev += cpos != 0;
+        wi += k;
+        ++it;
+    }
+    *iters = it;
+    *events = ev;
+}
