@@ -7,8 +7,9 @@
 // compile against this header unchanged.  Every reconstruction runs on the
 // GPU; there is no CPU code path for it.
 //
-// Not provided: the simulator, stability oracles, metrics and the PNG writer
-// -- outside the accelerated path.
+// Also on the device: the quality metrics (metrics.hpp) and stability_order
+// (stability.hpp), SURVEY.md 8(f) row 4.  Not provided: the simulator, the
+// Lemma 1/2 helpers and the PNG writer -- outside the accelerated path.
 #pragma once
 
 #include <cstdint>
@@ -162,6 +163,32 @@ std::vector<IntensityImage> reconstruct_serial(const SpikeVolume& volume, ReconM
 // uint8 frames straight from the GPU (the CLI's per-frame output, quantize()
 // of io.cpp:78-81 applied on the device): frames[n][y*W + x].
 std::vector<std::vector<uint8_t>> reconstruct_u8(const SpikeVolume& volume, ReconMethod method);
+
+// ------------------------------------------ metrics / stability (device) ----
+// metrics.hpp: two_dimensional_entropy (>= 3x3, else invalid_argument), mse
+// (dimension mismatch -> invalid_argument), psnr (+inf for identical images).
+// Each single-image call is one device round trip; the vector form does a
+// whole sequence in one call.
+double two_dimensional_entropy(const IntensityImage& image);
+std::vector<double> two_dimensional_entropy(const std::vector<IntensityImage>& images);
+double mse(const IntensityImage& image, const IntensityImage& reference);
+double psnr(const IntensityImage& image, const IntensityImage& reference);
+
+// stability.hpp: the shallowest zero-order violation of the interval tree
+// ('-' = smaller firing value first), explored to max_depth (1..63 here).
+struct ViolationInfo {
+    std::string path;
+    int depth = 0;     // 1 = S1
+    size_t index = 0;  // first offending element in that sequence
+};
+struct StabilityReport {
+    int verified_order = 0;
+    bool absolute = false;
+    std::optional<ViolationInfo> first_violation;
+};
+StabilityReport stability_order(const SpikeLikeStream& stream, int max_depth);
+// every pixel of a volume at once, row-major (verify-stability --in)
+std::vector<StabilityReport> stability_order(const SpikeVolume& volume, int max_depth);
 
 // ------------------------------------------------------------------- io ----
 struct io_error : std::runtime_error {

@@ -27,6 +27,10 @@
  *   spk_segment_host       segment_fsr / segment_ssr on a host payload
  *   spk_records[_host]     --emit-records: segment_* -> encode_events -> write_spkr
  *                          (proj/tools/spikecam_main.cpp:146-172) as one SPKR image
+ *   spk_frame_metrics[_host]  two_dimensional_entropy / mse per frame
+ *                          (proj/src/metrics.cpp:12-61; the CLI's compare)
+ *   spk_stability[_host]   stability_order per pixel (proj/src/stability.cpp:
+ *                          112-128; the CLI's verify-stability --in)
  *
  * Error behaviour mirrors the reference's exceptions: SPK_EINVAL where the
  * reference throws std::invalid_argument (bad method / window / geometry,
@@ -284,18 +288,19 @@ int spk_version(void);
  * per-image loops of the CLI's `compare` (proj/tools/spikecam_main.cpp:
  * 263-299): d_te[n] = two_dimensional_entropy of frame n
  * (proj/src/metrics.cpp:12-43) and, when d_ref is given, d_mse[n] = mse of
- * frame n against the uint8 reference image n (metrics.cpp:45-55; psnr is
+ * frame n against reference image n (metrics.cpp:45-55; psnr is
  * 10*log10(255^2/mse), 57-61).  Frames are [g->frames][pitch] elements of
  * frame_type (SPK_OUT_U8: quantized values, as the entropy uses them;
  * SPK_OUT_F32 / SPK_OUT_F64: values, quantized for the entropy with
  * round(clamp(v, 0, 255))); reference images are [g->frames][ref_pitch]
- * bytes.  Either output may be null.  Entropy needs W, H >= 3 (SPK_EINVAL,
+ * elements of ref_type (uint8 for PGM images read back, or values).  Either
+ * output may be null.  Entropy needs W, H >= 3 (SPK_EINVAL,
  * the reference's invalid_argument).  Sums are reduced in a fixed order:
  * deterministic, equal to the reference's sequential sums up to double
  * rounding (tests hold them to 1e-12 relative). */
 int spk_frame_metrics(const spk_geom* g, const void* d_frames, int frame_type, size_t pitch,
-                      const uint8_t* d_ref, size_t ref_pitch, double* d_te, double* d_mse,
-                      void* stream);
+                      const void* d_ref, int ref_type, size_t ref_pitch, double* d_te,
+                      double* d_mse, void* stream);
 
 /* stability_order (proj/src/stability.cpp:61-128) of one pixel stream:
  * depth of the shallowest zero-order violation (0: none; 1 = S1), its index
@@ -316,6 +321,13 @@ typedef struct spk_stab {
  * scratch from the spike counts). */
 int spk_stability(const spk_geom* g, const void* d_planes, int max_depth, spk_stab* d_out,
                   void* stream);
+
+/* Host-buffer forms (upload, compute, download; synchronous): frames /
+ * reference images as above in host memory, h_payload a dense SPK1 payload. */
+int spk_frame_metrics_host(const spk_geom* g, const void* h_frames, int frame_type, size_t pitch,
+                           const void* h_ref, int ref_type, size_t ref_pitch, double* h_te,
+                           double* h_mse);
+int spk_stability_host(const spk_geom* g, const void* h_payload, int max_depth, spk_stab* h_out);
 
 /* ---- synthetic inputs (benchmark / test harness, not the hot path) -------- */
 /* Integrate-and-fire streams (threshold 1, subtractive reset, uniform initial

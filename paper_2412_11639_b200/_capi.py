@@ -74,8 +74,12 @@ SIGNATURES = {
     "spk_last_error": (C.c_char_p, []),
     "spk_version": (C.c_int, []),
     "spk_synth": (C.c_int, [C.c_int, C.c_uint64, _G, C.c_int64, C.c_double, _P, _P]),
-    "spk_frame_metrics": (C.c_int, [_G, _P, C.c_int, C.c_size_t, _P, C.c_size_t, _P, _P, _P]),
+    "spk_frame_metrics": (C.c_int, [_G, _P, C.c_int, C.c_size_t, _P, C.c_int, C.c_size_t, _P, _P,
+                                    _P]),
     "spk_stability": (C.c_int, [_G, _P, C.c_int, _P, _P]),
+    "spk_frame_metrics_host": (C.c_int, [_G, _P, C.c_int, C.c_size_t, _P, C.c_int, C.c_size_t,
+                                         _P, _P]),
+    "spk_stability_host": (C.c_int, [_G, _P, C.c_int, _P]),
 }
 
 _lib = None

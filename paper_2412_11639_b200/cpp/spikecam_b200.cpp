@@ -13,6 +13,7 @@
 #include <cstring>
 #include <fstream>
 #include <iterator>
+#include <limits>
 #include <set>
 
 #include "spikecam_b200.h"
@@ -447,6 +448,99 @@ std::vector<std::vector<SegmentEvent>> EventStream::flush() {
 }
 
 long EventStream::frames() const { return static_cast<long>(spk_stream_frames(static_cast<spk_stream*>(stream_))); }
+
+// ------------------------------------------ metrics / stability (device) ----
+namespace {
+
+std::vector<double> metrics_of(const std::vector<IntensityImage>& images,
+                               const std::vector<IntensityImage>* refs) {
+    if (images.empty()) return {};
+    const int w = images[0].width, h = images[0].height;
+    const size_t npix = static_cast<size_t>(w) * h, t = images.size();
+    std::vector<double> frames(npix * t), ref;
+    for (size_t n = 0; n < t; ++n) {
+        if (images[n].width != w || images[n].height != h)
+            throw std::invalid_argument("two_dimensional_entropy: images differ in size");
+        std::copy(images[n].values.begin(), images[n].values.end(), frames.begin() + n * npix);
+    }
+    if (refs) {
+        ref.resize(npix * t);
+        for (size_t n = 0; n < t; ++n)
+            std::copy((*refs)[n].values.begin(), (*refs)[n].values.end(), ref.begin() + n * npix);
+    }
+    const spk_geom g = geom(w, h, static_cast<long>(t));
+    std::vector<double> out(t);
+    ck(spk_frame_metrics_host(&g, frames.data(), SPK_OUT_F64, npix, refs ? ref.data() : nullptr,
+                              SPK_OUT_F64, npix, refs ? nullptr : out.data(),
+                              refs ? out.data() : nullptr));
+    return out;
+}
+
+StabilityReport report_of(const spk_stab& r) {
+    StabilityReport rep;
+    rep.verified_order = r.verified_order;
+    rep.absolute = r.absolute != 0;
+    if (r.depth > 0) {
+        ViolationInfo v;
+        v.depth = r.depth;
+        v.index = static_cast<size_t>(r.index);
+        for (int j = 0; j < r.path_len; ++j) v.path.push_back((r.path >> j) & 1 ? '+' : '-');
+        rep.first_violation = std::move(v);
+    }
+    return rep;
+}
+
+void check_depth(int max_depth) {
+    if (max_depth < 1) throw std::invalid_argument("stability_order: max_depth must be >= 1");
+}
+
+}  // namespace
+
+double two_dimensional_entropy(const IntensityImage& image) {
+    if (image.width < 3 || image.height < 3)
+        throw std::invalid_argument("two_dimensional_entropy: image must be at least 3x3");
+    return metrics_of({image}, nullptr)[0];
+}
+
+std::vector<double> two_dimensional_entropy(const std::vector<IntensityImage>& images) {
+    if (!images.empty() && (images[0].width < 3 || images[0].height < 3))
+        throw std::invalid_argument("two_dimensional_entropy: image must be at least 3x3");
+    return metrics_of(images, nullptr);
+}
+
+double mse(const IntensityImage& image, const IntensityImage& reference) {
+    if (image.width != reference.width || image.height != reference.height)
+        throw std::invalid_argument("mse: dimension mismatch");
+    const std::vector<IntensityImage> refs{reference};
+    return metrics_of({image}, &refs)[0];
+}
+
+double psnr(const IntensityImage& image, const IntensityImage& reference) {
+    const double m = mse(image, reference);
+    if (m == 0.0) return std::numeric_limits<double>::infinity();
+    return 10.0 * std::log10(255.0 * 255.0 / m);
+}
+
+StabilityReport stability_order(const SpikeLikeStream& stream, int max_depth) {
+    check_depth(max_depth);
+    const std::vector<uint8_t> pay = stream_payload(stream);
+    const spk_geom g = geom(1, 1, static_cast<long>(stream.size()));
+    spk_stab r{};
+    ck(spk_stability_host(&g, pay.data(), max_depth, &r));
+    return report_of(r);
+}
+
+std::vector<StabilityReport> stability_order(const SpikeVolume& volume, int max_depth) {
+    check_depth(max_depth);
+    const PackedSpikes sp = pack(volume);
+    const spk_geom g = geom(volume.width(), volume.height(), volume.frames());
+    std::vector<spk_stab> r(static_cast<size_t>(volume.width()) * volume.height());
+    ck(spk_stability_host(&g, sp.payload.data(), max_depth, r.data()));
+    std::vector<StabilityReport> out;
+    out.reserve(r.size());
+    for (const auto& x : r) out.push_back(report_of(x));
+    return out;
+}
 
 // ------------------------------------------------------------------- io ----
 PackedSpikes read_spk_packed(const std::filesystem::path& path) {

@@ -1280,8 +1280,8 @@ int spk_version(void) { return 100; }
 
 // ---- quality metrics and the stability check (metrics.cu) ----
 int spk_frame_metrics(const spk_geom* g, const void* d_frames, int frame_type, size_t pitch,
-                      const uint8_t* d_ref, size_t ref_pitch, double* d_te, double* d_mse,
-                      void* stream) {
+                      const void* d_ref, int ref_type, size_t ref_pitch, double* d_te,
+                      double* d_mse, void* stream) {
     int rc = check_geom(g, false);
     if (rc) return rc;
     if (frame_type != SPK_OUT_U8 && frame_type != SPK_OUT_F32 && frame_type != SPK_OUT_F64)
@@ -1289,6 +1289,8 @@ int spk_frame_metrics(const spk_geom* g, const void* d_frames, int frame_type, s
     if (d_te && (g->width < 3 || g->height < 3))
         return fail(SPK_EINVAL, "two_dimensional_entropy: image must be at least 3x3");
     if (d_mse && !d_ref) return fail(SPK_EINVAL, "spk_frame_metrics: mse needs reference images");
+    if (d_mse && ref_type != SPK_OUT_U8 && ref_type != SPK_OUT_F32 && ref_type != SPK_OUT_F64)
+        return fail(SPK_EINVAL, "spk_frame_metrics: bad ref_type");
     const int64_t npix = npix_of(g);
     if (g->frames == 0 || (!d_te && !d_mse)) return SPK_OK;
     if (!d_frames) return fail(SPK_EINVAL, "spk: null device buffer");
@@ -1300,6 +1302,7 @@ int spk_frame_metrics(const spk_geom* g, const void* d_frames, int frame_type, s
     a.pitch = (int64_t)pitch;
     a.ref = d_ref;
     a.ref_pitch = (int64_t)ref_pitch;
+    a.ref_type = ref_type;
     a.width = g->width;
     a.height = g->height;
     a.te = d_te;
@@ -1373,6 +1376,90 @@ int spk_stability(const spk_geom* g, const void* d_planes, int max_depth, spk_st
         SPK_CK(cudaStreamSynchronize(s));  // `offs` is pageable host memory
         p0 = p1;
     }
+    return SPK_OK;
+}
+
+int spk_frame_metrics_host(const spk_geom* g, const void* h_frames, int frame_type, size_t pitch,
+                           const void* h_ref, int ref_type, size_t ref_pitch, double* h_te,
+                           double* h_mse) {
+    int rc = check_geom(g, false);
+    if (rc) return rc;
+    if (frame_type != SPK_OUT_U8 && frame_type != SPK_OUT_F32 && frame_type != SPK_OUT_F64)
+        return fail(SPK_EINVAL, "spk_frame_metrics: bad frame_type");
+    const size_t esz = frame_type == SPK_OUT_U8 ? 1 : frame_type == SPK_OUT_F32 ? 4 : 8;
+    const size_t npix = (size_t)npix_of(g), t = (size_t)g->frames;
+    if (h_te && (g->width < 3 || g->height < 3))
+        return fail(SPK_EINVAL, "two_dimensional_entropy: image must be at least 3x3");
+    if (h_mse && !h_ref) return fail(SPK_EINVAL, "spk_frame_metrics: mse needs reference images");
+    if (h_mse && ref_type != SPK_OUT_U8 && ref_type != SPK_OUT_F32 && ref_type != SPK_OUT_F64)
+        return fail(SPK_EINVAL, "spk_frame_metrics: bad ref_type");
+    const size_t rsz = ref_type == SPK_OUT_U8 ? 1 : ref_type == SPK_OUT_F32 ? 4 : 8;
+    if (t == 0 || (!h_te && !h_mse)) return SPK_OK;
+    if (!h_frames) return fail(SPK_EINVAL, "spk: null host buffer");
+    if (pitch < npix || (h_mse && ref_pitch < npix))
+        return fail(SPK_EINVAL, "spk_frame_metrics: pitch must be >= W*H");
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    cudaStream_t s;
+    SPK_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    rc = [&]() -> int {
+        Scratch fr(s), rf(s), te(s), ms(s);
+        SPK_CK(fr.alloc(pitch * esz * t));
+        SPK_CK(cudaMemcpyAsync(fr.p, h_frames, pitch * esz * t, cudaMemcpyHostToDevice, s));
+        if (h_mse) {
+            SPK_CK(rf.alloc(ref_pitch * rsz * t));
+            SPK_CK(cudaMemcpyAsync(rf.p, h_ref, ref_pitch * rsz * t, cudaMemcpyHostToDevice, s));
+            SPK_CK(ms.alloc(t * sizeof(double)));
+        }
+        if (h_te) SPK_CK(te.alloc(t * sizeof(double)));
+        int r = spk_frame_metrics(g, fr.p, frame_type, pitch, rf.p, ref_type,
+                                  ref_pitch, h_te ? static_cast<double*>(te.p) : nullptr,
+                                  h_mse ? static_cast<double*>(ms.p) : nullptr, s);
+        if (r) return r;
+        if (h_te) SPK_CK(cudaMemcpyAsync(h_te, te.p, t * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (h_mse)
+            SPK_CK(cudaMemcpyAsync(h_mse, ms.p, t * sizeof(double), cudaMemcpyDeviceToHost, s));
+        return SPK_OK;
+    }();
+    cudaError_t se = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (rc) return rc;
+    if (se != cudaSuccess) return cuda_fail(se, "cudaStreamSynchronize");
+    return SPK_OK;
+}
+
+int spk_stability_host(const spk_geom* g, const void* h_payload, int max_depth, spk_stab* h_out) {
+    spk_geom dg = *g;
+    dg.plane_pitch = spk_plane_pitch(g->width, g->height);
+    int rc = check_geom(&dg, true);
+    if (rc) return rc;
+    if (max_depth < 1 || max_depth > kStabMaxDepth)
+        return fail(SPK_EINVAL, "stability_order: max_depth must be in [1, 63]");
+    if (!h_out || (g->frames > 0 && !h_payload)) return fail(SPK_EINVAL, "spk: null host buffer");
+    const size_t npix = (size_t)npix_of(g);
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    cudaStream_t s;
+    SPK_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    rc = [&]() -> int {
+        Scratch planes(s), out(s);
+        SPK_CK(planes.alloc(dg.plane_pitch * (size_t)std::max<int64_t>(g->frames, 1)));
+        SPK_CK(out.alloc(npix * sizeof(spk_stab)));
+        if (g->frames > 0) {
+            const int r = spk_upload_planes(&dg, h_payload, plane_bytes(g), 0, planes.p, s);
+            if (r) return r;
+        }
+        const int r = spk_stability(&dg, planes.p, max_depth, static_cast<spk_stab*>(out.p), s);
+        if (r) return r;
+        SPK_CK(cudaMemcpyAsync(h_out, out.p, npix * sizeof(spk_stab), cudaMemcpyDeviceToHost, s));
+        return SPK_OK;
+    }();
+    cudaError_t se = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (rc) return rc;
+    if (se != cudaSuccess) return cuda_fail(se, "cudaStreamSynchronize");
     return SPK_OK;
 }
 

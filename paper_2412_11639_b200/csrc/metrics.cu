@@ -2,7 +2,7 @@
 // (SURVEY.md 8(f) row 4).
 //
 // K_te/mse  one block per frame: two_dimensional_entropy (proj/src/metrics.cpp:
-//           12-43) and mse against a uint8 reference image (45-55).  The
+//           12-43) and mse against a reference image (45-55).  The
 //           256x256 (gray, rounded 3x3 mean) histogram is built in shared
 //           memory in two halves of 128 gray levels (128 KB each, 32-bit
 //           counts: a 1000x1000 frame has ~1M interior pixels); each half is
@@ -61,10 +61,15 @@ __global__ void __launch_bounds__(kMetThreads) k_frame_metrics(MetArgs a) {
     const int w = a.width, h = a.height;
     const IN* f = reinterpret_cast<const IN*>(a.frames) + n * (int64_t)a.pitch;
     if (a.mse != nullptr) {
-        const uint8_t* r = a.ref + n * (int64_t)a.ref_pitch;
+        const int64_t r0 = n * a.ref_pitch;
         double acc = 0.0;
         for (int64_t i = threadIdx.x; i < (int64_t)w * h; i += blockDim.x) {
-            const double d = dv(f[i]) - (double)r[i];
+            const double rv = a.ref_type == SPK_OUT_U8
+                                  ? (double)static_cast<const uint8_t*>(a.ref)[r0 + i]
+                              : a.ref_type == SPK_OUT_F32
+                                  ? (double)static_cast<const float*>(a.ref)[r0 + i]
+                                  : static_cast<const double*>(a.ref)[r0 + i];
+            const double d = dv(f[i]) - rv;
             acc += d * d;
         }
         const double s = block_sum(acc, red);

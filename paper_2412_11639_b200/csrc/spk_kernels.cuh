@@ -231,8 +231,9 @@ constexpr int kStabMaxDepth = 63;    // violation paths are 64-bit masks
 struct MetArgs {
     const void* frames;  // [frames][pitch] elements
     int64_t pitch;
-    const uint8_t* ref;  // [frames][ref_pitch] uint8 reference images (mse)
+    const void* ref;     // [frames][ref_pitch] reference images (mse)
     int64_t ref_pitch;
+    int ref_type;        // SPK_OUT_U8 / F32 / F64
     int width, height;
     double* te;   // per frame, or null
     double* mse;  // per frame, or null (then `ref` is unused)

@@ -41,7 +41,7 @@ def _frames2d(frames: torch.Tensor, width: int | None, height: int | None):
 def frame_metrics(frames: torch.Tensor, ref: torch.Tensor | None = None, te: bool = True,
                   width: int | None = None, height: int | None = None, stream=None):
     """Per-frame two_dimensional_entropy (quantized values) and, with `ref`
-    (uint8 reference images, same shape), mse.  Returns (te, mse); an output
+    (reference images, same shape: uint8 as read back from PGM, or values), mse.  Returns (te, mse); an output
     not asked for is None."""
     if frames.dtype not in _FTYPE:
         raise ValueError("frames must be uint8, float32 or float64")
@@ -50,8 +50,8 @@ def frame_metrics(frames: torch.Tensor, ref: torch.Tensor | None = None, te: boo
     dev = f2.device
     r2 = None
     if ref is not None:
-        if ref.dtype != torch.uint8:
-            raise ValueError("reference images must be uint8")
+        if ref.dtype not in _FTYPE:
+            raise ValueError("reference images must be uint8, float32 or float64")
         r2, rw, rh = _frames2d(ref, width or w, height or h)
         if (rw, rh) != (w, h) or r2.shape[0] != t:
             raise ValueError("reference geometry differs")
@@ -62,6 +62,7 @@ def frame_metrics(frames: torch.Tensor, ref: torch.Tensor | None = None, te: boo
         capi.check(capi.lib().spk_frame_metrics(
             g, f2.data_ptr() if t else None, _FTYPE[frames.dtype], int(f2.stride(0)) if t else w * h,
             r2.data_ptr() if r2 is not None and t else None,
+            _FTYPE[ref.dtype] if ref is not None else capi.SPK_OUT_U8,
             int(r2.stride(0)) if r2 is not None and t else w * h,
             te_out.data_ptr() if te_out is not None and t else None,
             mse_out.data_ptr() if mse_out is not None and t else None, _stream(stream)))
@@ -75,7 +76,7 @@ def two_dimensional_entropy(frame: torch.Tensor) -> float:
 
 
 def mse(image: torch.Tensor, reference: torch.Tensor) -> float:
-    """metrics.cpp:45-55 of one [H, W] image against a uint8 reference image."""
+    """metrics.cpp:45-55 of one [H, W] image against a reference image."""
     if image.shape != reference.shape:
         raise ValueError("mse: dimension mismatch")
     _, m = frame_metrics(image.unsqueeze(0), reference.unsqueeze(0), te=False)
@@ -91,8 +92,8 @@ def psnr(image: torch.Tensor, reference: torch.Tensor) -> float:
 def compare(volume: PackedVolume, methods=("fsr", "ssr", "tfi", "tfp"), ref=None,
             warmup: int = 0, dtype: torch.dtype = torch.float64) -> list[dict]:
     """The CLI's `compare` (spikecam_main.cpp:263-299): per method, the mean
-    entropy over frames [first, T) and, with reference images (uint8 [T, H,
-    W]; frames without one are skipped the way a missing PGM is, via a
+    entropy over frames [first, T) and, with reference images ([T, H, W];
+    frames without one are skipped the way a missing PGM is, via a
     boolean `ref_mask`), the mean mse and its psnr.  `ref` may be a tensor or
     a (tensor, mask) pair."""
     t = volume.frames

@@ -8,6 +8,7 @@
 //
 // `rows` / `vol` only dump results; the Python side compares them with the
 // reference's golden outputs (tests/golden/).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -310,6 +311,64 @@ static void vol(const fs::path& spk, const fs::path& dir) {
     }
 }
 
+// ------------------------------------------------------ metrics / stab ----
+static void put_report(std::ofstream& o, const StabilityReport& r) {
+    put<int32_t>(o, r.first_violation ? r.first_violation->depth : 0);
+    put<int64_t>(o, r.first_violation ? (int64_t)r.first_violation->index : 0);
+    put<int32_t>(o, r.verified_order);
+    put<int32_t>(o, r.absolute ? 1 : 0);
+    const std::string path = r.first_violation ? r.first_violation->path : std::string();
+    put<uint32_t>(o, (uint32_t)path.size());
+    o.write(path.data(), (std::streamsize)path.size());
+}
+
+static void stab_rows(const fs::path& in, const fs::path& out, int depth) {
+    std::ifstream i(in, std::ios::binary);
+    std::ofstream o(out, std::ios::binary);
+    uint32_t ncase = 0;
+    i.read(reinterpret_cast<char*>(&ncase), 4);
+    for (uint32_t c = 0; c < ncase; ++c) {
+        uint32_t t = 0;
+        i.read(reinterpret_cast<char*>(&t), 4);
+        std::vector<uint8_t> b(t);
+        i.read(reinterpret_cast<char*>(b.data()), t);
+        put_report(o, stability_order(SpikeLikeStream(std::vector<int>(b.begin(), b.end()), 1, 0), depth));
+    }
+}
+
+// compare-style metrics of FSR frames against TFI frames, and the per-pixel
+// stability of the volume (verify-stability --in)
+static void metrics(const fs::path& spk, const fs::path& dir) {
+    auto [v, fps] = read_spk(spk);
+    (void)fps;
+    const auto fsr = reconstruct(v, ReconMethod::parse("fsr"));
+    const auto tfi = reconstruct(v, ReconMethod::parse("tfi"));
+    std::vector<IntensityImage> ref;
+    for (const auto& im : tfi) {  // reference images as PGM round trips them
+        IntensityImage q(im.width, im.height);
+        for (size_t k = 0; k < im.values.size(); ++k)
+            q.values[k] = std::round(std::clamp(im.values[k], 0.0, 255.0));
+        ref.push_back(std::move(q));
+    }
+    const auto te = two_dimensional_entropy(fsr);
+    std::ofstream f(dir / "te.f64", std::ios::binary);
+    f.write(reinterpret_cast<const char*>(te.data()), (std::streamsize)(te.size() * 8));
+    std::ofstream g(dir / "single.f64", std::ios::binary);
+    for (size_t n = 0; n < fsr.size(); n += 37) {
+        put<double>(g, two_dimensional_entropy(fsr[n]));
+        put<double>(g, mse(fsr[n], ref[n]));
+        put<double>(g, psnr(fsr[n], ref[n]));
+    }
+    for (int depth : {4, 8}) {
+        std::ofstream o(dir / ("stab_d" + std::to_string(depth) + ".bin"), std::ios::binary);
+        for (const auto& r : stability_order(v, depth)) put_report(o, r);
+    }
+    EXPECT(throws<std::invalid_argument>([&] { two_dimensional_entropy(IntensityImage(2, 7)); }));
+    EXPECT(throws<std::invalid_argument>([&] { mse(IntensityImage(3, 3), IntensityImage(3, 4)); }));
+    EXPECT(throws<std::invalid_argument>([&] { stability_order(pixel_stream(v, 0, 0), 0); }));
+    EXPECT(std::isinf(psnr(fsr[0], fsr[0])));
+}
+
 int main(int argc, char** argv) {
     const std::string mode = argc > 1 ? argv[1] : "";
     try {
@@ -321,8 +380,13 @@ int main(int argc, char** argv) {
             rows(argv[2], argv[3]);
         } else if (mode == "vol" && argc == 4) {
             vol(argv[2], argv[3]);
+        } else if (mode == "stab" && argc == 5) {
+            stab_rows(argv[2], argv[3], std::atoi(argv[4]));
+        } else if (mode == "metrics" && argc == 4) {
+            metrics(argv[2], argv[3]);
         } else {
-            std::fprintf(stderr, "usage: dropin_test selftest DIR | gpucheck | rows IN OUT | vol SPK DIR\n");
+            std::fprintf(stderr, "usage: dropin_test selftest DIR | gpucheck | rows IN OUT | vol SPK DIR | "
+                                 "stab IN OUT DEPTH | metrics SPK DIR\n");
             return 2;
         }
     } catch (const std::exception& e) {

@@ -41,7 +41,9 @@ def test_cpp_dropin_exports(exe):
                  "spikecam::segment_ssr(", "spikecam::fsr_events(", "spikecam::reconstruct_pixel(",
                  "spikecam::read_spk(", "spikecam::write_spk(", "spikecam::read_raw(",
                  "spikecam::write_image(", "spikecam::read_image(", "spikecam::reconstruct_u8(",
-                 "spikecam::SpikeVolume::SpikeVolume(", "spikecam::ReconMethod::parse("]:
+                 "spikecam::SpikeVolume::SpikeVolume(", "spikecam::ReconMethod::parse(",
+                 "spikecam::two_dimensional_entropy(", "spikecam::mse(", "spikecam::psnr(",
+                 "spikecam::stability_order("]:
         assert name in demangled, name
 
 
@@ -125,3 +127,67 @@ def test_cpp_dropin_volume_matches_reference(exe, golden_dir, tmp_path, name):
         if t > 1:
             pgm = (tmp_path / f"{tag}_mid.pgm").read_bytes()
             assert np.array_equal(np.frombuffer(pgm[-w * h:], np.uint8), g[f"{tag}/u8"][t // 2]), tag
+
+
+def _reports(buf):
+    out, off = [], 0
+    while off < len(buf):
+        d, = np.frombuffer(buf, np.int32, 1, off)
+        i, = np.frombuffer(buf, np.int64, 1, off + 4)
+        vo, ab = np.frombuffer(buf, np.int32, 2, off + 12)
+        n, = np.frombuffer(buf, np.uint32, 1, off + 20)
+        path = buf[off + 24: off + 24 + int(n)].decode()
+        out.append(([int(d), int(i), int(vo), int(ab)], path))
+        off += 24 + int(n)
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("depth", [1, 3, 8])
+def test_cpp_dropin_stability_rows(exe, golden_dir, tmp_path, depth):
+    """stability_order(SpikeLikeStream, depth) against the reference's reports."""
+    rows = np.load(golden_dir / "rows.npz")
+    gm = np.load(golden_dir / "metrics.npz")
+    names = list(gm["rows/names"])
+    with open(tmp_path / "in.bin", "wb") as f:
+        f.write(np.uint32(len(names)).tobytes())
+        for n in names:
+            b = rows[f"{n}/bits"].astype(np.uint8)
+            f.write(np.uint32(b.size).tobytes())
+            f.write(b.tobytes())
+    run(exe, "stab", tmp_path / "in.bin", tmp_path / "out.bin", depth)
+    got = _reports((tmp_path / "out.bin").read_bytes())
+    for i, n in enumerate(names):
+        assert got[i][0] == [int(x) for x in gm[f"rows/d{depth}"][i]], n
+        assert got[i][1] == str(gm[f"rows/d{depth}/path"][i]), n
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_metrics_and_volume_stability(exe, golden_dir, tmp_path):
+    """two_dimensional_entropy / mse / psnr and stability_order(SpikeVolume)
+    through the C++ drop-in on the moving-bar volume."""
+    g = np.load(golden_dir / "vol_bar64x48.npz")
+    gm = np.load(golden_dir / "metrics.npz")
+    w, h, t = (int(x) for x in g["geom"])
+    head = np.zeros(16, np.uint8)
+    head[:4] = np.frombuffer(b"SPK1", np.uint8)
+    head[4:8] = np.frombuffer(np.array([w, h], "<u2").tobytes(), np.uint8)
+    head[8:16] = np.frombuffer(np.array([20000, t], "<u4").tobytes(), np.uint8)
+    spk = tmp_path / "v.spk"
+    spk.write_bytes(head.tobytes() + g["planes"].tobytes())
+    run(exe, "metrics", spk, tmp_path)
+    te = np.fromfile(tmp_path / "te.f64", np.float64)
+    want = gm["bar/te_fsr"]
+    assert np.allclose(te, want, rtol=1e-12, atol=0)
+    single = np.fromfile(tmp_path / "single.f64", np.float64).reshape(-1, 3)
+    for k, n in enumerate(range(0, t, 37)):
+        assert np.isclose(single[k, 0], want[n], rtol=1e-12, atol=0)
+        assert np.isclose(single[k, 1], gm["bar/mse_fsr_tfi"][n], rtol=1e-12, atol=0)
+        p = gm["bar/psnr_fsr_tfi"][n]
+        assert (np.isinf(p) and np.isinf(single[k, 2])) or np.isclose(single[k, 2], p, rtol=1e-12)
+    rep = _reports((tmp_path / "stab_d8.bin").read_bytes())
+    wd = gm["vol/bar64x48/d8"]
+    wp = gm["vol/bar64x48/d8/path"]
+    assert len(rep) == w * h
+    for p in range(w * h):
+        assert rep[p][0] == [int(x) for x in wd[p]] and rep[p][1] == str(wp[p]), p
