@@ -23,3 +23,22 @@ for m in ("fsr", "ssr"):
     pxf = W * H * T
     print(f"{m}: {ms:.2f} ms/step  {T / ms * 1e3 / 1e6:.3f} M fps  "
           f"{pxf * 1.125 / ms / 1e6 / 6553.3:.3f} of HBM roofline", flush=True)
+
+# per-phase device times (timing mode runs the volume as one pixel part)
+import ctypes as C  # noqa: E402
+
+from paper_2412_11639_b200 import _capi as capi  # noqa: E402
+
+lib = capi.lib()
+for m in ("fsr", "ssr"):
+    v = [C.c_float() for _ in range(4)]
+    lib.spk_set_timing(1)
+    acc = []
+    for _ in range(4):
+        spk.reconstruct(vol, m, out=out)
+        torch.cuda.synchronize()
+        capi.check(lib.spk_last_timing(*(C.byref(x) for x in v)))
+        acc.append([x.value for x in v])
+    lib.spk_set_timing(0)
+    ph = [sum(a[i] for a in acc[1:]) / 3 for i in range(4)]
+    print(f"{m} phases (seg, fin, exp, fix) ms: " + ", ".join(f"{p:.2f}" for p in ph), flush=True)
