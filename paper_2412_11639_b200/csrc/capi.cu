@@ -29,7 +29,6 @@ thread_local int64_t g_launches = 0;
 thread_local bool g_timing = false;
 thread_local cudaEvent_t g_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 thread_local int g_ev_used = 0;  // events recorded by the last call
-thread_local bool g_no_split = false;  // pipelined host batches: one pixel part per call
 
 // phase marker k (0..4) on stream s when timing is enabled: 0 before K2,
 // 1 after K2, 2 after K2b/scan/K2c, 3 after K3, 4 after the fixup
@@ -116,27 +115,6 @@ void ensure_pool(int dev) {
     done.fetch_or(bit);
 }
 
-constexpr int kParts = 2;
-// only volumes large enough to keep every SM busy with half the pixels
-constexpr int64_t kSplitPixels = 1 << 19;
-
-// per (thread, device) auxiliary stream and events for the pipelined path
-int aux_resources(int dev, cudaStream_t& aux, cudaEvent_t* ev) {
-    struct Res {
-        cudaStream_t s = nullptr;
-        cudaEvent_t e[kParts + 2] = {};
-    };
-    thread_local Res res[16];
-    if (dev < 0 || dev >= 16) return fail(SPK_EINVAL, "spk: device index >= 16");
-    Res& r = res[dev];
-    if (!r.s) {
-        SPK_CK(cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking));
-        for (auto& e : r.e) SPK_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
-    aux = r.s;
-    for (int i = 0; i < kParts + 2; ++i) ev[i] = r.e[i];
-    return SPK_OK;
-}
 
 // RAII stream-ordered scratch
 struct Scratch {
@@ -344,49 +322,18 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
     a.counts = static_cast<uint32_t*>(counts.p);
     a.last = static_cast<int32_t*>(last.p);
 
-    // K2 is issue-bound, K2b..K3 are latency/HBM-bound: with enough pixels
-    // the volume is cut into pixel parts (multiples of 512 pixels) and the
-    // expand of part k runs on an auxiliary stream while K2 scans part k+1.
-    const int nparts = (npix >= kSplitPixels && !g_timing && !g_no_split) ? kParts : 1;
-    if (nparts == 1) {
-        ExpandWork<OUT> w(s);
-        if ((rc = prepare_expand<OUT>(a, w, s))) return rc;
-        mark(0, s);
-        if ((rc = launch_segment(method, a, s))) return rc;
-        if ((rc = launch_expand<OUT>(a, w, out, out_pitch, s))) return rc;
-        mark(3, s);
-        rc = launch_fixup<OUT>(method, a, out, out_pitch, s);
-        mark(4, s);
-        return rc;
-    }
-    cudaStream_t aux;
-    cudaEvent_t ev[kParts + 2];
-    if ((rc = aux_resources(dev, aux, ev))) return rc;
-    SPK_CK(cudaEventRecord(ev[0], s));  // fork: aux sees the allocations above
-    SPK_CK(cudaStreamWaitEvent(aux, ev[0], 0));
-    for (int k = 0; k < nparts; ++k) {
-        const int64_t b0 = std::min(npix, ((npix * k / nparts) + 511) / 512 * 512);
-        const int64_t b1 = k + 1 == nparts ? npix : std::min(npix, ((npix * (k + 1) / nparts) + 511) / 512 * 512);
-        if (b1 <= b0) continue;
-        SegArgs ak = a;
-        ak.planes = static_cast<const char*>(planes) + b0 / 8;
-        ak.npix = b1 - b0;
-        ak.runs = a.runs + b0 * a.cap;
-        ak.counts = a.counts + b0;
-        ak.last = a.last + b0;
-        ExpandWork<OUT> w(aux);
-        if ((rc = prepare_expand<OUT>(ak, w, aux))) return rc;
-        SPK_CK(cudaEventRecord(ev[k + 1], aux));  // workspaces ready -> K2 may fill bins
-        SPK_CK(cudaStreamWaitEvent(s, ev[k + 1], 0));
-        if ((rc = launch_segment(method, ak, s))) return rc;
-        SPK_CK(cudaEventRecord(ev[k + 1], s));
-        SPK_CK(cudaStreamWaitEvent(aux, ev[k + 1], 0));
-        if ((rc = launch_expand<OUT>(ak, w, out + b0, out_pitch, aux))) return rc;
-        if ((rc = launch_fixup<OUT>(method, ak, out + b0, out_pitch, aux))) return rc;
-    }
-    SPK_CK(cudaEventRecord(ev[kParts + 1], aux));  // join before the frees on s
-    SPK_CK(cudaStreamWaitEvent(s, ev[kParts + 1], 0));
-    return SPK_OK;
+    // One pass: pipelining pixel parts of K2 with K3 was measured slower at
+    // every size (K2 fills the SMs, so K3 of part k only runs in the gaps of
+    // part k+1: C3 FSR 9.72 vs 9.34 ms, SSR 25.5 vs 24.5 ms).
+    ExpandWork<OUT> w(s);
+    if ((rc = prepare_expand<OUT>(a, w, s))) return rc;
+    mark(0, s);
+    if ((rc = launch_segment(method, a, s))) return rc;
+    if ((rc = launch_expand<OUT>(a, w, out, out_pitch, s))) return rc;
+    mark(3, s);
+    rc = launch_fixup<OUT>(method, a, out, out_pitch, s);
+    mark(4, s);
+    return rc;
 }
 
 template <typename OUT>
@@ -782,7 +729,6 @@ int spk_reconstruct_host_batch(const spk_geom* g, int32_t count, const void* con
     constexpr int kLanes = 2;
     cudaStream_t st[kLanes] = {nullptr, nullptr};
     for (auto& x : st) SPK_CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
-    g_no_split = true;
     rc = [&]() -> int {
         Scratch planes0(st[0]), planes1(st[1]), out0(st[0]), out1(st[1]);
         Scratch* planes[kLanes] = {&planes0, &planes1};
@@ -811,7 +757,6 @@ int spk_reconstruct_host_batch(const spk_geom* g, int32_t count, const void* con
         }
         return SPK_OK;
     }();
-    g_no_split = false;
     cudaError_t se = cudaSuccess;
     for (auto& x : st) {
         const cudaError_t e = cudaStreamSynchronize(x);

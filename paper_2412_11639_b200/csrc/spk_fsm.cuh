@@ -458,21 +458,24 @@ SPK_HD int fsr_batch4(SC& sc, uint32_t W0, uint32_t W1, uint32_t W2, uint32_t W3
                       int& cpos, EMIT&& emit) {
     const int lo = sc.lo;
     const uint32_t hw = sc.hw;
-    const bool two = lo >= 2;
+    // per-window constants: a second shift by lo when the pair is single
+    // (OR-idempotent, no select per word), the adjacency mask when lo >= 2
+    const uint32_t sh1 = (uint32_t)lo, sh2 = (uint32_t)lo + hw;
+    const uint32_t twom = lo >= 2 ? 0xffffffffu : 0u;
     const uint32_t r0 = W0 & bit_shr_clamp(0xffffffffu, 0u, (uint32_t)cpos);
-    int pv = sc.last;  // last spike before the word under test
+    int pv = sc.last + lo;  // last spike before the word under test, plus lo
     int p0v, p1v, p2v, p3v;
     uint32_t V0, V1, V2, V3;
     auto test = [&](uint32_t w, uint32_t r, int base, int& prev_out, uint32_t& V) {
         prev_out = pv;
-        const uint32_t Q = bit_shr_clamp(w, 0u, (uint32_t)lo) |
-                           bit_sel(hw != 0u, bit_shr_clamp(w, 0u, (uint32_t)lo + 1u), 0u);
-        const uint32_t G1 = w & (w >> 1);
+        const uint32_t Q = bit_shr_clamp(w, 0u, sh1) | bit_shr_clamp(w, 0u, sh2);
         const int f = bit_clz(r | 1u);
-        const uint32_t fb = r ? (0x80000000u >> f) : 0u;
-        const bool bad0 = (r != 0u) & ((uint32_t)(base + f - pv - lo) > hw);
-        V = (r & ~(Q | fb)) | bit_sel(two, r & G1, 0u) | bit_sel(bad0, fb, 0u);
-        pv = r ? base + 32 - bit_ffs(r) : pv;
+        const uint32_t fb = (0x80000000u >> f) & r;  // r's first spike (0 if none)
+        const uint32_t bad0 = (uint32_t)(base + f - pv) > hw ? fb : 0u;
+        V = (r & ~(Q | fb)) | (r & (w >> 1) & w & twom) | bad0;
+        // r's last spike is its lowest set bit: frame base + clz(r & -r)
+        const int lastr = base + bit_clz(r & (0u - r)) + lo;
+        pv = r ? lastr : pv;
     };
     test(W0, r0, base0, p0v, V0);
     test(W1, W1, base0 + 32, p1v, V1);
@@ -489,8 +492,8 @@ SPK_HD int fsr_batch4(SC& sc, uint32_t W0, uint32_t W1, uint32_t W2, uint32_t W3
     const bool s0 = kk == 0, s1 = kk == 1, s2 = kk == 2;
     const uint32_t Vk = bit_sel(s0, V0, bit_sel(s1, V1, bit_sel(s2, V2, V3)));
     const uint32_t rk = bit_sel(s0, r0, bit_sel(s1, W1, bit_sel(s2, W2, W3)));
-    const int prevk = (int)bit_sel(s0, (uint32_t)p0v,
-                                   bit_sel(s1, (uint32_t)p1v, bit_sel(s2, (uint32_t)p2v, (uint32_t)p3v)));
+    const int prevk = -lo + (int)bit_sel(s0, (uint32_t)p0v,
+                                        bit_sel(s1, (uint32_t)p1v, bit_sel(s2, (uint32_t)p2v, (uint32_t)p3v)));
     const uint32_t before = bit_sel(kk > 0, c0, 0u) + bit_sel(kk > 1, c1, 0u) + bit_sel(kk > 2, c2, 0u);
     const int basek = base0 + 32 * kk;
     const int p = bit_clz(Vk);
