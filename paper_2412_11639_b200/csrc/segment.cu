@@ -103,8 +103,8 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         if (lane == 0) vprog[wid] = lowest;
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
-            const uint32_t w = transpose32(nxt[j], lane);
-            rg[(produced + j) & (kRing - 1)][lane] = valid ? w : 0u;
+            const uint32_t t = transpose32(nxt[j], lane);  // every lane shuffles
+            rg[(produced + j) & (kRing - 1)][lane] = valid ? t : 0u;
         }
         produced += kBatch;
         throttle(produced);
@@ -194,23 +194,22 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     // back word by word; the ring bounds how far lanes may drift apart.
     int wi = 0;    // first word of this lane's window
     int cpos = 0;  // frames of word wi already consumed
+    // Groups past the end are produced as zero words, so a window never
+    // needs a bounds check.
     for (;;) {
         const bool more = wi < ngroups;
-        const bool ready = min(wi + 4, ngroups) <= produced;
+        const bool ready = wi + 4 <= produced;
         // refill only when a lane is starved, and only into slots no lane can
         // still read (lowest = the earliest window start)
         if (__any_sync(kFull, more & !ready)) {
             const int lowest = (int)__reduce_min_sync(kFull, (unsigned)(more ? wi : 0x7fffffff));
-            if (produced < ngroups && produced + kBatch <= lowest + kRing) produce(lowest);
+            if (produced < ngroups + 3 && produced + kBatch <= lowest + kRing) produce(lowest);
         }
         if (!__any_sync(kFull, more)) break;
-        if (more & (min(wi + 4, ngroups) <= produced)) {
-            const uint32_t w0 = rg[wi & (kRing - 1)][lane];
-            const uint32_t w1 = wi + 1 < ngroups ? rg[(wi + 1) & (kRing - 1)][lane] : 0u;
-            const uint32_t w2 = wi + 2 < ngroups ? rg[(wi + 2) & (kRing - 1)][lane] : 0u;
-            const uint32_t w3 = wi + 3 < ngroups ? rg[(wi + 3) & (kRing - 1)][lane] : 0u;
-            wi += fsr_batch4(sc, w0, w1, w2, w3, wi * 32, cpos, emit);
-        }
+        if (more & ready)
+            wi += fsr_batch4(sc, rg[wi & (kRing - 1)][lane], rg[(wi + 1) & (kRing - 1)][lane],
+                             rg[(wi + 2) & (kRing - 1)][lane], rg[(wi + 3) & (kRing - 1)][lane],
+                             wi * 32, cpos, emit);
     }
     }
     if (lane == 0) vprog[wid] = 0x7fffffff;  // done: never hold the others back

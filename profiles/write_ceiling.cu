@@ -36,6 +36,26 @@ __global__ void wseg(char* p, size_t pitch, int rows, int groups, uint32_t v) {
     }
 }
 
+// block b writes its own contiguous range (whole rows), 16-B stores
+__global__ void wblocked(char* p, size_t bytes, uint32_t v) {
+    const size_t per = (bytes / gridDim.x) & ~(size_t)4095;
+    char* q = p + (size_t)blockIdx.x * per;
+    const size_t n = blockIdx.x + 1 == gridDim.x ? bytes - (size_t)blockIdx.x * per : per;
+    for (size_t i = threadIdx.x * 16; i < n; i += blockDim.x * 16)
+        *reinterpret_cast<uint4*>(q + i) = make_uint4(v, v, v, (uint32_t)i);
+}
+
+// K3-like tiles but a block covers RW contiguous bytes of each row (warps side by side)
+template <int RW>
+__global__ void wwide(char* p, size_t pitch, int rows, uint32_t v) {
+    const int c = blockIdx.y;
+    char* q = p + (size_t)c * 1024 * pitch + (size_t)blockIdx.x * RW;
+    const int w = min(RW, (int)(pitch - (size_t)blockIdx.x * RW));
+    for (int f = 0; f < 1024 && c * 1024 + f < rows; ++f)
+        for (int i = threadIdx.x * 16; i < w; i += blockDim.x * 16)
+            *reinterpret_cast<uint4*>(q + (size_t)f * pitch + i) = make_uint4(v, v, v, f);
+}
+
 template <int SEG>
 void run_seg(char* d, cudaEvent_t a, cudaEvent_t b, int wpb) {
     const int groups = 100000 / SEG;
@@ -90,6 +110,33 @@ int main() {
         run_seg<1024>(d, a, b, wpb);
         run_seg<2048>(d, a, b, wpb);
         run_seg<4096>(d, a, b, wpb);
+    }
+    for (int blocks : {148, 296, 592, 1184}) {
+        wblocked<<<blocks, 512>>>(d, bytes, 1);
+        cudaEventRecord(a);
+        for (int r = 0; r < 10; ++r) wblocked<<<blocks, 512>>>(d, bytes, r);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        printf("wblocked %5d blocks x 512: %.3f ms  %.0f GB/s\n", blocks, ms / 10, bytes / (ms / 10) / 1e6);
+    }
+    {
+        dim3 grid((100000 + 8191) / 8192, 40);
+        wwide<8192><<<grid, 512>>>(d, 100000, 40000, 1);
+        cudaEventRecord(a);
+        for (int r = 0; r < 10; ++r) wwide<8192><<<grid, 512>>>(d, 100000, 40000, r);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        printf("wwide 8192 B/row x 1024 rows per block: %.3f ms  %.0f GB/s\n", ms / 10, bytes / (ms / 10) / 1e6);
+        dim3 grid2((100000 + 2047) / 2048, 40);
+        wwide<2048><<<grid2, 128>>>(d, 100000, 40000, 1);
+        cudaEventRecord(a);
+        for (int r = 0; r < 10; ++r) wwide<2048><<<grid2, 128>>>(d, 100000, 40000, r);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        printf("wwide 2048 B/row x 1024 rows per block: %.3f ms  %.0f GB/s\n", ms / 10, bytes / (ms / 10) / 1e6);
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
