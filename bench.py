@@ -208,6 +208,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--frames", type=int, default=T)
     ap.add_argument("--no-long", action="store_true", help="skip the configs[4] long-stream leg")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the configs[0], [2] and [3] legs (static, large sensor, batch of 64)")
     ap.add_argument("--long-frames", type=int, default=LONG_T)
     args = ap.parse_args()
     if args.warmup < 3:
@@ -382,17 +384,98 @@ def main():
                                 "kind": kind,
                                 "sample": f"frames [0,{tcpu}) of the same stream, reference "
                                           f"bench() median of 3, {cores} workers"}
-    if not args.no_long:
+    if not args.no_long or not args.no_configs:
         del vol, out
         if not args.no_e2e:
             del payload, houts
         torch.cuda.empty_cache()
+    if not args.no_configs:
+        line["configs"] = other_configs(args, rank, world, dev)
+        torch.cuda.empty_cache()
+    if not args.no_long:
         line["long_stream"] = long_stream(args, rank, world, dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _device_ms(fn, dev, world, steps=5, warmup=3):
+    """mean ms of fn() over `steps` (CUDA events on the current stream; fn
+    joins any side streams it uses), max over ranks"""
+    import torch
+    import torch.distributed as dist
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def other_configs(args, rank, world, dev):
+    """The other BASELINE configs, device-resident like `value`:
+    configs[0] static 400x250x20,000 and configs[2] sensor 1000x1000x20,000
+    (single-GPU configs: rank 0), and configs[3] -- 64 independent 400x250
+    streams of 4,000 frames, seeds 0..63 alternating the static and moving
+    generators -- sharded across the ranks (64/N streams each, no exchange;
+    volumes issued round-robin on two streams so one volume's segmentation
+    overlaps another's expand)."""
+    import torch
+
+    import paper_2412_11639_b200 as spk
+    res = {}
+    methods = ("fsr", "ssr")
+    for key, scene, w, h, t in (("configs[0]", "static", 400, 250, 20000),
+                                ("configs[2]", "sensor", 1000, 1000, 20000)):
+        if rank != 0:
+            continue
+        vol = spk.synth(scene, 0, w, h, t, device=dev)
+        out = torch.empty((t, w * h), dtype=torch.uint8, device=dev)
+        r = {"workload": f"{key} {scene} {w}x{h}x{t}", "unit": "frames/s"}
+        for m in methods:
+            ms = _device_ms(lambda: spk.reconstruct(vol, m, out=out), dev, 1)
+            r[m] = {"value": t / (ms * 1e-3), "ms_per_step": ms,
+                    "step_frac": w * h * t * BYTES_PER_PXF / (ms * 1e-3) / 1e9 / peaks()[0]}
+        res[key] = r
+        del vol, out
+        torch.cuda.empty_cache()
+    nvol, t4 = 64, 4000
+    mine = list(range(rank * nvol // world, (rank + 1) * nvol // world))
+    vols = [spk.synth("static" if i % 2 == 0 else "moving", i, W, H, t4, device=dev) for i in mine]
+    outs = [torch.empty((t4, W * H), dtype=torch.uint8, device=dev) for _ in mine]
+    lanes = [torch.cuda.Stream(dev) for _ in range(2)]
+    cur = torch.cuda.current_stream(dev)
+    r = {"workload": f"configs[3] {nvol} x {W}x{H}x{t4} (static/moving by seed parity)",
+         "unit": "frames/s", "scaling": "strong", "streams_per_rank": len(mine),
+         "parallelism": f"streams x{world}"}
+    for m in methods:
+        def batch():
+            for ln in lanes:
+                ln.wait_stream(cur)
+            for k, (v, o) in enumerate(zip(vols, outs)):
+                spk.reconstruct(v, m, out=o, stream=lanes[k % 2])
+            for ln in lanes:
+                cur.wait_stream(ln)
+        ms = _device_ms(batch, dev, world, steps=3, warmup=2)
+        r[m] = {"value": nvol * t4 / (ms * 1e-3), "ms_per_step": ms,
+                "step_frac": nvol * W * H * t4 * BYTES_PER_PXF / (ms * 1e-3) / 1e9 / peaks()[0]}
+    res["configs[3]"] = r
+    return res
 
 
 def long_stream(args, rank, world, dev):
