@@ -294,7 +294,7 @@ def main():
     fps = world * frames / (ms_step * 1e-3)
     gpxf = world * pxf / (ms_step * 1e-3) / 1e9
 
-    def roofline(ph, ms_step):
+    def roofline(ph, ms_step, method):
         """Dominant kernel (largest share of the step): algorithmic bytes per
         launch / its mean CUDA-event duration.  K2 (segment) reads 0.125 B/px-frame
         and is issue-bound (integer ALU; profiles/), K3 (expand) writes 1 B/px-frame
@@ -307,15 +307,22 @@ def main():
         else:
             kern, achieved, dur = "k_segment", k2_gbs, seg
         traffic = None
-        tf = ROOT / "profiles" / f"traffic_{kern}_{args.method}.json"
+        tf = ROOT / "profiles" / f"traffic_{kern}_{method}.json"
         if tf.exists():
             traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+        alu = None
+        af = ROOT / "profiles" / f"alu_{kern}_{method}.json"
+        if kern == "k_segment" and af.exists():
+            alu = json.loads(af.read_text())
         return {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_kind": peak_kind, "kernel_ms": dur,
-                "kernel_note": ("k_segment is issue-bound (integer ALU), not HBM-bound: its "
-                                "HBM fraction is low by construction" if kern == "k_segment" else
-                                "HBM write-bound"),
+                "kernel_note": (f"k_segment is bound by the integer ALU pipe, not HBM (ncu: ALU pipe "
+                                f"{alu['alu_pipe_frac']:.0%} of peak, FMA pipe {alu['fma_pipe_frac']:.0%}); "
+                                "its HBM fraction is low by construction" if alu else
+                                "k_segment is issue-bound (integer ALU), not HBM-bound"
+                                if kern == "k_segment" else "HBM write-bound"),
+                "alu_pipe_frac": alu["alu_pipe_frac"] if alu else None,
                 "step_frac": pxf * BYTES_PER_PXF / (ms_step * 1e-3) / 1e9 / peak,
                 "phases_ms": {"segment": seg, "finalize": fin, "expand": exp, "fixup": fix},
                 "expand_hbm_gbs": k3_gbs, "expand_hbm_frac": k3_gbs / peak}
@@ -330,12 +337,12 @@ def main():
                    "l2": "no flush: 0.5 GB in + 4 GB out per step > 126 MB L2",
                    "vs_baseline_ref": "FPGA 20,000 FPS (BASELINE.md, PAPER.md:199)"},
         "gpx_frames_per_s": gpxf,
-        "roofline": roofline(phases, ms_step),
+        "roofline": roofline(phases, ms_step, args.method),
         "gpu_launches": int(launches),
         "clocks": clocks,
         other: {"value": world * frames / (ms2 / k2 * 1e-3),
                 "ms_per_step": ms2 / k2,
-                "roofline": roofline(phases2, ms2 / k2)},
+                "roofline": roofline(phases2, ms2 / k2, other)},
     }
 
     # end to end through the C-ABI host boundary (pinned host buffers): the
