@@ -205,7 +205,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--frames", type=int, default=T)
     ap.add_argument("--no-long", action="store_true", help="skip the configs[4] long-stream leg")
     ap.add_argument("--no-configs", action="store_true",
@@ -361,7 +361,7 @@ def main():
         def e2e_batch(count):
             capi.check(lib.spk_reconstruct_host_batch(g, count, pin, kind, 32, capi.SPK_OUT_U8,
                                                       pout, W * H))
-        e2e_batch(1)  # warm
+        e2e_batch(2)  # warm: both lanes' device buffers come from the pool afterwards
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
@@ -373,14 +373,27 @@ def main():
             el = float(t.item())
         step(args.method)  # device-path result of the same method for the check
         assert torch.equal(houts[(n - 1) % 2][-64:], out[-64:].cpu()), "e2e result differs from device path"
+        # the PCIe ceiling of this box: one plain device -> pinned-host copy of a step's frames
+        d2h_ms = []
+        for _ in range(2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            houts[0].copy_(out, non_blocking=True)
+            e1.record()
+            e1.synchronize()
+            d2h_ms.append(e0.elapsed_time(e1))
+        d2h_gbs = houts[0].numel() / (min(d2h_ms) * 1e-3) / 1e9
         line["e2e"] = {"value": world * frames * n / el, "unit": "frames/s",
                        "h2d_bytes_per_step": int(payload.numel()),
                        "d2h_bytes_per_step": int(houts[0].numel()),
                        "steps": n,
                        "path": "spk_reconstruct_host_batch (C-ABI, pinned host in/out, "
                                "H2D + kernels of step i+1 overlap the D2H of step i)",
-                       "pcie_note": "4 GB of uint8 frames per step over PCIe (~52 GB/s D2H measured, "
-                                    "profiles/pcie_probe.py)"}
+                       "pcie_d2h_gbs": d2h_gbs,
+                       "pcie_frac": houts[0].numel() * n / el / 1e9 / d2h_gbs,
+                       "pcie_note": "4 GB of uint8 frames per step over PCIe: e2e is bound by the "
+                                    "device-to-host copy (pcie_d2h_gbs = one plain 4 GB copy on "
+                                    "this box; profiles/pcie_probe.py)"}
 
     if rank == 0 and not args.no_cpu:
         tcpu = min(CPU_SAMPLE_FRAMES, frames)
