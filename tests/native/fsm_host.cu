@@ -210,3 +210,34 @@ extern "C" void batch_iters(const uint8_t* bits, long frames, long* iters, long*
     *iters = it;
     *events = ev;
 }
+
+// SSR bulk words (ssr_word) leave exactly the automaton state of the
+// per-spike steps after every word: returns the first word whose state
+// differs, or -1.
+extern "C" long ssr_state_check(const uint8_t* bits, long frames) {
+    const long ng = (frames + 31) / 32;
+    std::vector<uint32_t> w(ng + 1, 0u);
+    for (long f = 0; f < frames; ++f)
+        if (bits[f]) w[f / 32] |= 0x80000000u >> (f % 32);
+    spk::Scan<spk::kSSR> a, b;
+    a.init();
+    b.init();
+    auto put = [&](bool, int, int) {};
+    for (long i = 0; i < ng; ++i) {
+        const int base = (int)(i * 32);
+        spk::ssr_word(a, w[i], base, put);
+        for (uint32_t s = w[i]; s;) {
+            const int c = spk::bit_clz(s);
+            s ^= 0x80000000u >> c;
+            int rs, cnt;
+            b.step(base + c, rs, cnt);
+        }
+        const int32_t va[] = {a.last, a.lo, a.rs, a.cnt, (int32_t)a.hw, a.ii, a.sub0, a.l0, a.l1,
+                              a.g0, a.g1, (int32_t)a.h0, (int32_t)a.h1, a.fl0, a.fl1, a.sf};
+        const int32_t vb[] = {b.last, b.lo, b.rs, b.cnt, (int32_t)b.hw, b.ii, b.sub0, b.l0, b.l1,
+                              b.g0, b.g1, (int32_t)b.h0, (int32_t)b.h1, b.fl0, b.fl1, b.sf};
+        for (int k = 0; k < 16; ++k)
+            if (va[k] != vb[k]) return i * 100 + k;
+    }
+    return -1;
+}

@@ -36,6 +36,8 @@ def fsm():
     h.word_runs.argtypes = h.fsm_runs.argtypes
     h.batch_runs.restype = C.c_long
     h.batch_runs.argtypes = h.fsm_runs.argtypes
+    h.ssr_state_check.restype = C.c_long
+    h.ssr_state_check.argtypes = [C.c_void_p, C.c_long]
     h.ssrword_runs.restype = C.c_long
     h.ssrword_runs.argtypes = h.fsm_runs.argtypes
 
@@ -48,7 +50,7 @@ def fsm():
             return s[:n], e[:n], c[:n]
         return run
     return {"fsm": make(h.fsm_runs), "scan": make(h.scan_runs), "word": make(h.word_runs),
-            "batch": make(h.batch_runs), "ssrword": make(h.ssrword_runs)}
+            "batch": make(h.batch_runs), "ssrword": make(h.ssrword_runs), "_h": h}
 
 
 def if_stream(rng, t, segs, flips):
@@ -140,3 +142,32 @@ def test_bulk_drivers_long_streams(fsm, oracle, kind):
         for m in (0, 1):
             got, want = run(b, m), oracle.runs(b, m)
             assert all(np.array_equal(x, y) for x, y in zip(got, want)), (m, t)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_ssr_bulk_state_equals_exact_steps(fsm, seed):
+    """After every word, the SSR bulk driver (ssr_flags / ssr_accept) holds
+    exactly the automaton state of the per-spike steps (all 16 fields)."""
+    rng = np.random.default_rng(seed)
+    for _ in range(300):
+        t = int(rng.integers(1, 3000))
+        kind = rng.integers(0, 3)
+        if kind == 0:  # piecewise-constant rates (runs of regular spikes)
+            bits = np.zeros(t, np.uint8)
+            acc, q = rng.uniform(0, 1), rng.uniform(0.02, 1.0)
+            for f in range(t):
+                if rng.random() < 0.003:
+                    q = rng.uniform(0.02, 1.0)
+                acc += q
+                if acc >= 1.0:
+                    acc -= 1.0
+                    bits[f] = 1
+            bits ^= (rng.random(t) < rng.choice([0.0, 0.002, 0.01])).astype(np.uint8)
+        elif kind == 1:
+            bits = (rng.random(t) < rng.uniform(0.05, 0.9)).astype(np.uint8)
+        else:  # slowly varying rate
+            q = 0.05 + 0.4 * (1 + np.sin(np.arange(t) / rng.uniform(50, 900)))
+            c = np.cumsum(q) + rng.uniform(0, 1)
+            bits = (np.floor(c) != np.floor(c - q)).astype(np.uint8)
+        r = fsm["_h"].ssr_state_check(bits.ctypes.data, t)
+        assert r == -1, (seed, t, int(kind), divmod(r, 100))
