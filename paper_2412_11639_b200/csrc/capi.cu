@@ -1293,15 +1293,16 @@ int spk_stability(const spk_geom* g, const void* d_planes, int max_depth, spk_st
     SPK_CK(cudaMemcpyAsync(hc.data(), cnt.p, (size_t)npix * sizeof(uint32_t),
                            cudaMemcpyDeviceToHost, s));
     SPK_CK(cudaStreamSynchronize(s));
-    // per-pixel stack of sequences: a child is at most its parent's length,
-    // and the deepest level is max_depth, so max_depth * |S1| ints suffice
-    constexpr int64_t kBudget = (int64_t)1 << 30;  // scratch ints per batch (4 GB)
+    // per-pixel stack of bit-packed sequences: a child is at most its
+    // parent's length and the deepest level is max_depth, so max_depth *
+    // ceil(|S1| / 32) words suffice
+    constexpr int64_t kBudget = (int64_t)1 << 30;  // scratch words per batch (4 GB)
     for (int64_t p0 = 0; p0 < npix;) {
         std::vector<int64_t> offs;
         int64_t tot = 0, p1 = p0;
         while (p1 < npix) {
             const int64_t len = hc[(size_t)p1] > 1 ? (int64_t)hc[(size_t)p1] - 1 : 0;
-            const int64_t need = (int64_t)max_depth * len + 1;
+            const int64_t need = (int64_t)max_depth * ((len + 31) / 32) + 1;
             if (p1 > p0 && tot + need > kBudget) break;
             offs.push_back(tot);
             tot += need;

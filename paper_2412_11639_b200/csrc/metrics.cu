@@ -11,10 +11,11 @@
 //           double rounding).
 // K_stab    one thread per pixel: stability_order (proj/src/stability.cpp:
 //           61-128) -- the depth-first tree of interval streams, '-' first,
-//           with the reference's pruning -- over the pixel's S1 kept in a
-//           per-pixel global scratch region (a stack of one sequence per
-//           depth; a child is never longer than its parent, so depth * |S1|
-//           ints always suffice).
+//           with the reference's pruning.  Only stable sequences (two values
+//           differing by one) are explored further, so each level of the
+//           pixel's depth-first stack is kept as one bit per element in a
+//           per-pixel global scratch region; a child is never longer than
+//           its parent, so depth * ceil(|S1| / 32) words always suffice.
 #include <cmath>
 
 #include "spk_common.cuh"
@@ -130,23 +131,86 @@ __global__ void k_stab_count(StabArgs a) {
 
 namespace {
 
+// A stable sequence (stability.cpp:41-59: at most two values, differing by
+// one) is stored as one bit per element: value = lo + (raw ^ flip), raw bit e
+// at bit (e & 31) of word e >> 5.  Only stable sequences are ever explored
+// further, so every level of the depth-first stack fits in |S1| bits.
 struct StabLevel {
-    int64_t off;  // first element in the pixel's region
+    int64_t off;  // first word in the pixel's region
     int32_t len;
     int32_t lo, hi;
-    int32_t state;  // 0: not evaluated, 1: '-' child explored, 2: both explored
+    uint32_t flip;   // 0xffffffff when raw bit 1 stands for lo
+    int32_t state;   // 0: not evaluated, 1: '-' child explored, 2: both explored
+    int32_t bad;     // first_violation_index of the level (-1: stable)
 };
 
-// interval_stream(seq, firing) (stability.cpp:93-106): gaps between
-// successive occurrences of `firing`, written at dst; returns the count
-__device__ int32_t gaps_of(const int32_t* seq, int32_t len, int32_t firing, int32_t* dst) {
-    int32_t last = -1, m = 0;
-    for (int32_t i = 0; i < len; ++i) {
-        if (seq[i] != firing) continue;
-        if (last >= 0) dst[m++] = i - last;
-        last = i;
+// Appends the values of a sequence one by one, applying first_violation_index
+// (a = first value, b = the first +-1 neighbour) and min/max, and writing the
+// raw bits (value != a) to `dst` -- stops at the first violation.
+struct SeqBuilder {
+    uint32_t* dst;
+    int32_t m = 0, a = 0, b = 0, lo = 0, hi = 0, bad = -1;
+    bool hb = false;
+    uint32_t acc = 0;
+    __device__ bool push(int32_t v) {  // false once a violation was found
+        uint32_t raw = 0;
+        if (m == 0) {
+            a = lo = hi = v;
+        } else if (v == a) {
+        } else if (hb && v == b) {
+            raw = 1;
+        } else if (!hb && abs(v - a) == 1) {
+            b = v;
+            hb = true;
+            raw = 1;
+            lo = min(lo, v);
+            hi = max(hi, v);
+        } else {
+            bad = m;
+            return false;
+        }
+        acc |= raw << (m & 31);
+        if ((m & 31) == 31) {
+            dst[m >> 5] = acc;
+            acc = 0;
+        }
+        ++m;
+        return true;
     }
-    return m;
+    __device__ void finish(StabLevel& L) {
+        if (bad < 0 && (m & 31)) dst[m >> 5] = acc;
+        L.len = m;
+        L.lo = lo;
+        L.hi = hi;
+        L.flip = hb && b < a ? 0xffffffffu : 0u;
+        L.bad = bad;
+        L.state = 0;
+    }
+};
+
+// interval_stream(seq, firing) (stability.cpp:93-106) of a stored stable
+// sequence: the gaps between successive elements equal to `firing` (hi_bit:
+// the larger value), written as the next level
+__device__ void child_of(const uint32_t* reg, const StabLevel& P, bool hi_bit, StabLevel& C) {
+    SeqBuilder sb;
+    sb.dst = const_cast<uint32_t*>(reg) + C.off;
+    int32_t last = -1;
+    const int32_t nw = (P.len + 31) >> 5;
+    for (int32_t wi = 0; wi < nw; ++wi) {
+        uint32_t w = reg[P.off + wi] ^ P.flip;  // bit 1 = the larger value
+        if (!hi_bit) w = ~w;
+        if (wi == nw - 1 && (P.len & 31)) w &= (1u << (P.len & 31)) - 1u;
+        while (w) {
+            const int32_t pos = wi * 32 + __ffs(w) - 1;
+            w &= w - 1;
+            if (last >= 0 && !sb.push(pos - last)) {
+                sb.finish(C);
+                return;
+            }
+            last = pos;
+        }
+    }
+    sb.finish(C);
 }
 
 }  // namespace
@@ -158,19 +222,23 @@ __global__ void __launch_bounds__(128) k_stab(StabArgs a) {
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= a.nbatch) return;
     const int64_t p = a.pix0 + q;
-    int32_t* reg = a.scratch + a.offs[q] - a.offs[0];
-    // S1 of the pixel stream (pixel_stream, core.cpp:109-118: firing value 1)
-    const uint8_t* col = reinterpret_cast<const uint8_t*>(a.planes) + (p >> 3);
-    const int bit = (int)(p & 7);
-    int32_t m = 0;
-    int64_t last = -1;
-    for (int64_t n = 0; n < a.frames; ++n) {
-        if (!((col[n * (int64_t)a.pitch] >> bit) & 1u)) continue;
-        if (last >= 0) reg[m++] = (int32_t)(n - last);
-        last = n;
-    }
+    uint32_t* reg = reinterpret_cast<uint32_t*>(a.scratch) + (a.offs[q] - a.offs[0]);
     StabLevel L[kStabMaxDepth + 2];
-    L[1] = StabLevel{0, m, 0, 0, 0};
+    // level 1: S1 of the pixel stream (pixel_stream, core.cpp:109-118: firing value 1)
+    {
+        const uint8_t* col = reinterpret_cast<const uint8_t*>(a.planes) + (p >> 3);
+        const int bit = (int)(p & 7);
+        SeqBuilder sb;
+        sb.dst = reg;
+        int64_t last = -1;
+        for (int64_t n = 0; n < a.frames; ++n) {
+            if (!((col[n * (int64_t)a.pitch] >> bit) & 1u)) continue;
+            if (last >= 0 && !sb.push((int32_t)(n - last))) break;
+            last = n;
+        }
+        L[1].off = 0;
+        sb.finish(L[1]);
+    }
     int k = 1;
     int vdepth = 0, deepest = 0, trunc = 0;
     int64_t vindex = 0;
@@ -178,59 +246,39 @@ __global__ void __launch_bounds__(128) k_stab(StabArgs a) {
     const int maxd = a.max_depth;
     while (k >= 1) {
         StabLevel& c = L[k];
-        const int32_t* seq = reg + c.off;
         if (c.state == 0) {
             if (vdepth && vdepth <= k) { --k; continue; }
-            if (c.len == 0) {
+            if (c.len == 0 && c.bad < 0) {
                 deepest = max(deepest, k);
                 --k;
                 continue;
             }
-            // first_violation_index (stability.cpp:41-59) and min/max in one pass
-            int32_t va = seq[0], vb = 0, lo = seq[0], hi = seq[0];
-            bool hb = false;
-            int32_t bad = -1;
-            for (int32_t i = 1; i < c.len; ++i) {
-                const int32_t x = seq[i];
-                lo = min(lo, x);
-                hi = max(hi, x);
-                if (x == va || (hb && x == vb)) continue;
-                if (!hb && abs(x - va) == 1) {
-                    vb = x;
-                    hb = true;
-                    continue;
-                }
-                bad = i;
-                break;
-            }
-            if (bad >= 0) {
+            if (c.bad >= 0) {
                 if (!vdepth || k < vdepth) {
                     vdepth = k;
-                    vindex = bad;
+                    vindex = c.bad;
                     vpath = path;
                 }
                 --k;
                 continue;
             }
             deepest = max(deepest, k);
-            if (lo == hi) { --k; continue; }
+            if (c.lo == c.hi) { --k; continue; }
             if (k >= maxd) {
                 trunc = 1;
                 --k;
                 continue;
             }
-            c.lo = lo;
-            c.hi = hi;
             c.state = 1;
-            const int64_t off = c.off + c.len;
-            L[k + 1] = StabLevel{off, gaps_of(seq, c.len, lo, reg + off), 0, 0, 0};
+            L[k + 1].off = c.off + ((c.len + 31) >> 5);
+            child_of(reg, c, false, L[k + 1]);  // '-': the smaller firing value
             path &= ~(1ull << (k - 1));
             ++k;
         } else if (c.state == 1) {
             c.state = 2;
             if (vdepth && vdepth <= k + 1) { --k; continue; }  // the '+' child returns at once
-            const int64_t off = c.off + c.len;
-            L[k + 1] = StabLevel{off, gaps_of(seq, c.len, c.hi, reg + off), 0, 0, 0};
+            L[k + 1].off = c.off + ((c.len + 31) >> 5);
+            child_of(reg, c, true, L[k + 1]);
             path |= 1ull << (k - 1);
             ++k;
         } else {
