@@ -412,6 +412,9 @@ def main():
     if not args.no_configs:
         line["configs"] = other_configs(args, rank, world, dev)
         torch.cuda.empty_cache()
+        if rank == 0:
+            line["metrics"] = metrics_leg(dev, not args.no_cpu)
+            torch.cuda.empty_cache()
     if not args.no_long:
         line["long_stream"] = long_stream(args, rank, world, dev)
     if rank == 0:
@@ -445,6 +448,57 @@ def _device_ms(fn, dev, world, steps=5, warmup=3):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     return ms
+
+
+def metrics_leg(dev, with_cpu):
+    """SURVEY 8(f) row 4 on the device: the CLI's `compare` metrics (per-frame
+    two_dimensional_entropy + mse against uint8 reference frames) over a
+    configs[1] reconstruction, and `verify-stability --in` (stability_order of
+    every pixel, depth 8) over configs[0] and configs[1]; beside them the
+    reference's own functions on the host (single thread, bounded samples)."""
+    import torch
+
+    import paper_2412_11639_b200 as spk
+    res = {}
+    vol = spk.synth("moving", 0, W, H, T, device=dev)
+    f64 = spk.reconstruct(vol, "fsr", dtype=torch.float64)
+    ref = spk.reconstruct(vol, "tfi")
+    ms = _device_ms(lambda: spk.frame_metrics(f64, ref), dev, 1, steps=3, warmup=1)
+    res["compare"] = {"workload": f"configs[1] FSR f64 frames vs TFI uint8 frames, {T} frames",
+                      "value": T / (ms * 1e-3), "unit": "frames/s", "ms": ms}
+    if with_cpu:
+        from oracle.oracle import Reference, ref_available
+        if ref_available():
+            r = Reference()
+            sample = f64[:20].cpu().numpy()
+            rs = ref[:20].cpu().numpy().astype(np.float64)
+            t0 = time.perf_counter()
+            for n in range(20):
+                r.te(sample[n].reshape(H, W))
+                r.mse(sample[n].reshape(H, W), rs[n].reshape(H, W))
+            el = time.perf_counter() - t0
+            res["compare"]["cpu_baseline"] = {"value": 20 / el, "unit": "frames/s", "cores": 1,
+                                              "kind": "reference", "sample": "frames [0,20)"}
+    del f64, ref
+    for key, scene, t in (("configs[0]", "static", 20000), ("configs[1]", "moving", T)):
+        v = spk.synth(scene, 0, W, H, t, device=dev)
+        ms = _device_ms(lambda: spk.stability(v, 8), dev, 1, steps=2, warmup=1)
+        rr = {"workload": f"verify-stability --in, depth 8, {key} {scene} {W}x{H}x{t}",
+              "value": W * H / (ms * 1e-3), "unit": "pixels/s", "ms": ms}
+        if with_cpu:
+            from oracle.oracle import Reference, ref_available
+            if ref_available():
+                r = Reference()
+                pl = v.planes[:, :8].cpu().numpy()  # pixels 0..63
+                t0 = time.perf_counter()
+                for p in range(64):
+                    r.stability(((pl[:, p >> 3] >> (p & 7)) & 1).astype(np.uint8), 8)
+                el = time.perf_counter() - t0
+                rr["cpu_baseline"] = {"value": 64 / el, "unit": "pixels/s", "cores": 1,
+                                      "kind": "reference", "sample": "pixels [0,64)"}
+        res[f"stability {key}"] = rr
+        del v
+    return res
 
 
 def other_configs(args, rank, world, dev):

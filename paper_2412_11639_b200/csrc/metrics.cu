@@ -3,10 +3,11 @@
 //
 // K_te/mse  one block per frame: two_dimensional_entropy (proj/src/metrics.cpp:
 //           12-43) and mse against a reference image (45-55).  The
-//           256x256 (gray, rounded 3x3 mean) histogram is built in shared
-//           memory in two halves of 128 gray levels (128 KB each, 32-bit
-//           counts: a 1000x1000 frame has ~1M interior pixels); each half is
-//           reduced to its -p*log2(p) sum in a fixed order, so the result is
+//           256x256 (gray, rounded 3x3 mean) histogram is built in 128 KB of
+//           shared memory: at once with 16-bit counts when the frame has
+//           fewer than 65,536 interior pixels, else in two halves of 128 gray
+//           levels with 32-bit counts (a 1000x1000 frame has ~1M); the
+//           -p*log2(p) terms are reduced in a fixed order, so the result is
 //           deterministic (equal to the reference's sequential sum up to
 //           double rounding).
 // K_stab    one thread per pixel: stability_order (proj/src/stability.cpp:
@@ -80,6 +81,42 @@ __global__ void __launch_bounds__(kMetThreads) k_frame_metrics(MetArgs a) {
     const int iw = w - 2;
     const int64_t interior = (int64_t)iw * (h - 2);
     double te = 0.0;
+    if (interior < 65536) {
+        // every bin fits 16 bits: the whole 256x256 histogram at once, two
+        // bins per 32-bit word
+        for (int i = threadIdx.x; i < kMetHalf; i += blockDim.x) hist[i] = 0u;
+        __syncthreads();
+        for (int64_t i = threadIdx.x; i < interior; i += blockDim.x) {
+            const int x = 1 + (int)(i % iw), y = 1 + (int)(i / iw);
+            const IN* c = f + (int64_t)y * w + x;
+            int sum = 0;
+#pragma unroll
+            for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                for (int dx = -1; dx <= 1; ++dx) sum += qv(c[(int64_t)dy * w + dx]);
+            const int bin = qv(c[0]) * 256 + (2 * sum + 9) / 18;  // lround(sum / 9.0), no ties
+            atomicAdd(&hist[bin >> 1], 1u << ((bin & 1) * 16));
+        }
+        __syncthreads();
+        double acc = 0.0;
+        const double tot = (double)interior;
+        for (int i = threadIdx.x; i < kMetHalf; i += blockDim.x) {
+            const uint32_t c2 = hist[i];
+            if (c2) {
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const uint32_t c = (c2 >> (16 * k)) & 0xffffu;
+                    if (c) {
+                        const double p = (double)c / tot;
+                        acc -= p * log2(p);
+                    }
+                }
+            }
+        }
+        te = block_sum(acc, red);
+        if (threadIdx.x == 0) a.te[n] = te;
+        return;
+    }
     for (int half = 0; half < 2; ++half) {
         for (int i = threadIdx.x; i < kMetHalf; i += blockDim.x) hist[i] = 0u;
         __syncthreads();
