@@ -233,9 +233,11 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     if (smem > 48 * 1024)
         SPK_CK(cudaFuncSetAttribute(k_expand<OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
-    for (int c0 = 0; c0 < sa.nchunks; c0 += 65535) {
+    e.pieces = w.ngroups <= kPieceMaxGroups ? kPieces : 1;
+    const int per_launch = 65535 / e.pieces;  // grid.y = chunks x pieces
+    for (int c0 = 0; c0 < sa.nchunks; c0 += per_launch) {
         e.chunk0 = c0;
-        const unsigned by = (unsigned)std::min(65535, sa.nchunks - c0);
+        const unsigned by = (unsigned)(std::min(per_launch, sa.nchunks - c0) * e.pieces);
         k_expand<OUT><<<dim3(bx, by), warps * 32, smem, s>>>(e);
         SPK_LAUNCHED("k_expand");
     }

@@ -19,7 +19,7 @@
 //       the exact round-half-away integer form.
 //   (K2b/K2c: block = pixel group x chunk window, warp = one pixel, 32 runs
 //   per coalesced load, shared-memory counters.)
-//   K3  k_expand      one warp per (group, chunk): per sub-tile of kSub
+//   K3  k_expand      one warp per (group, chunk, 64-frame piece): per sub-tile of kSub
 //       frames, the warp reads that sub-tile's changes (contiguous, coalesced)
 //       into per-frame value/mask buckets in shared memory, then every lane
 //       walks the frames merging its bucket and storing its P values per frame
@@ -202,10 +202,17 @@ __global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
     uint32_t* B = reinterpret_cast<uint32_t*>(D + kSub * 32 * G::DE);
 
     const int g = blockIdx.x * Geo<OUT>::WARPS + warp;
-    const int c = a.chunk0 + (int)blockIdx.y;
+    // tile = (group, chunk, piece of kPieceSubs sub-tiles): blocks of one
+    // piece row run together, so the rows being written at any time stay
+    // within a narrow band of frames (DRAM page locality: 64-row tiles write
+    // at 6.8 TB/s in the probe, 1024-row tiles at 5.7)
+    const int c = a.chunk0 + (int)blockIdx.y / a.pieces;
+    const int sub0 = ((int)blockIdx.y % a.pieces) * kPieceSubs;
     if (g >= a.ngroups) return;  // warp-uniform; lanes only exchange via __syncwarp
-    const int f0 = c << kChunkLog2;
-    const int f1 = min(a.frames, f0 + kChunk);
+    const int fc = c << kChunkLog2;       // chunk start
+    const int f0 = fc + sub0 * kSub;      // piece start
+    const int f1 = min(a.frames, fc + kChunk);
+    if (f0 >= f1) return;
     const int64_t p0 = (int64_t)g * GP + (int64_t)lane * P;
     const int np = (int)max((int64_t)0, min((int64_t)P, a.npix - p0));
 
@@ -244,6 +251,54 @@ __global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
     const uint32_t off_lo = a.offs[b0 + lane], off_hi = a.offs[b0 + 32 + lane];
     const uint32_t cnt_lo = a.bins[b0 + lane], cnt_hi = a.bins[b0 + 32 + lane];
     const Change<OUT>* st = reinterpret_cast<const Change<OUT>*>(a.stream);
+    // Dense tiles (many changes per pixel in the chunk) are written whole by
+    // the piece-0 warp: the piece prefix would re-read too many changes.
+    const uint32_t tile_changes = __shfl_sync(kFull, off_hi + cnt_hi, 31) - __shfl_sync(kFull, off_lo, 0);
+    const bool whole = a.pieces == 1 || tile_changes > (uint32_t)(kPieceDensity * GP);
+    if (whole && sub0 > 0) return;  // warp-uniform
+    const int sub1 = whole ? kBins : sub0 + kPieceSubs;
+    if (sub0 > 0) {
+        // values at the piece start: the chunk-start values updated by the
+        // latest change of each pixel in the sub-tiles before the piece (one
+        // contiguous range of the stream; a shared-memory max over
+        // (frame offset, index) per pixel picks it)
+        uint32_t* K = reinterpret_cast<uint32_t*>(D);
+        for (int i = lane; i < GP; i += 32) K[i] = 0u;
+        __syncwarp();
+        const uint32_t pb = __shfl_sync(kFull, off_lo, 0);
+        const uint32_t pe = __shfl_sync(kFull, sub0 < 32 ? off_lo : off_hi, sub0 & 31);
+        for (uint32_t k = lane; k < pe - pb; k += 32) {
+            const Change<OUT> ch = st[pb + k];
+            uint32_t fo, pix;
+            if constexpr (sizeof(OUT) == 1) {
+                fo = ch.w >> 17;
+                pix = (ch.w >> 8) & 0x1ffu;
+            } else {
+                fo = ch.key >> 16;
+                pix = ch.key & 0xffffu;
+            }
+            atomicMax(&K[pix], (fo + 1u) << 20 | k);  // k < 2^20: at most 512 x 1024 changes
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            const uint32_t key = K[lane * P + i];
+            if (key) {
+                const Change<OUT> ch = st[pb + (key & 0xfffffu)];
+                if constexpr (sizeof(OUT) == 1) {
+                    const int sh = (i & 3) * 8;
+                    words[i >> 2] = (words[i >> 2] & ~(0xffu << sh)) | ((ch.w & 0xffu) << sh);
+                } else if constexpr (sizeof(OUT) == 4) {
+                    words[i] = ch.bits;
+                } else {
+                    const unsigned long long bits = __double_as_longlong(ch.v);
+                    words[2 * i] = (uint32_t)bits;
+                    words[2 * i + 1] = (uint32_t)(bits >> 32);
+                }
+            }
+        }
+        __syncwarp();  // K (in D) is reused for the buckets below
+    }
 #pragma unroll
     for (int f = 0; f < kSub; ++f) B[f * 32 + lane] = 0u;
 
@@ -259,7 +314,7 @@ __global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
     // loaded while the previous sub-tile's frames are being stored
     constexpr int R = sizeof(OUT) == 8 ? 2 : 4;
     uint32_t off, n;
-    bin_of(0, off, n);
+    bin_of(sub0, off, n);
     Change<OUT> pre[R];
 #pragma unroll
     for (int i = 0; i < R; ++i)
@@ -286,12 +341,12 @@ __global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
         atomicOr(&B[fs * 32 + own], pend_bit<OUT>(i));
     };
 
-    for (int sub = 0; sub < kBins; ++sub) {
-        const int t0 = f0 + sub * kSub;
+    for (int sub = sub0; sub < sub1; ++sub) {
+        const int t0 = fc + sub * kSub;
         if (t0 >= f1) break;
         // ---- phase A: this sub-tile's changes -> owners' buckets
         uint32_t noff = 0, nn = 0;
-        if (sub + 1 < kBins) bin_of(sub + 1, noff, nn);
+        if (sub + 1 < sub1) bin_of(sub + 1, noff, nn);
 #pragma unroll
         for (int i = 0; i < R; ++i)
             if ((uint32_t)(lane + 32 * i) < n) bucket(pre[i], sub);

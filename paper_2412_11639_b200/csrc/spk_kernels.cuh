@@ -80,6 +80,13 @@ struct ShardArgs {
 // in sub-tiles of kSub frames (kBins sub-tiles per chunk).
 constexpr int kSub = 16;
 constexpr int kBins = kChunk / kSub;
+constexpr int kPieceSubs = 4;                // K3 tile height: 64 frames
+constexpr int kPieces = kBins / kPieceSubs;  // K3 tiles per (group, chunk)
+constexpr int kPieceDensity = 12;            // changes per pixel per chunk above which
+                                             // K3 writes the chunk as one tile
+constexpr int kPieceMaxGroups = 512;         // pieces only for narrow frames (few groups
+                                             // per row: wide rows already keep the
+                                             // concurrently written rows close)
 template <typename OUT>
 struct Geo;
 template <>
@@ -145,6 +152,7 @@ struct ExpArgs {
     int nchunks;
     int ngroups;
     int chunk0;  // first chunk of this launch (blockIdx.y offset)
+    int pieces;  // tiles per (group, chunk): kPieces, or 1 (whole chunks)
     void* out;
     size_t pitch;  // elements between frames
     int vec_ok;    // out base / pitch allow 16-B vector stores

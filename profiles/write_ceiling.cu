@@ -56,6 +56,42 @@ __global__ void wwide(char* p, size_t pitch, int rows, uint32_t v) {
             *reinterpret_cast<uint4*>(q + (size_t)f * pitch + i) = make_uint4(v, v, v, f);
 }
 
+// K3 tile pattern with RT rows per tile (warp = 512 B of a row, 4 warps per block)
+template <int RT>
+__global__ void wtile(char* p, size_t pitch, int rows, int groups, uint32_t v) {
+    const int lane = threadIdx.x & 31;
+    const int g = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int c = blockIdx.y;
+    if (g >= groups) return;
+    char* q = p + (size_t)c * RT * pitch + (size_t)g * 512 + lane * 16;
+    for (int f = 0; f < RT && c * RT + f < rows; ++f)
+        *reinterpret_cast<uint4*>(q + (size_t)f * pitch) = make_uint4(v, v, v, f);
+}
+
+template <int RT>
+void run_tile(char* d, cudaEvent_t a, cudaEvent_t b) {
+    dim3 grid((196 + 3) / 4, (40000 + RT - 1) / RT);
+    wtile<RT><<<grid, 128>>>(d, 100000, 40000, 196, 1);
+    cudaEventRecord(a);
+    for (int r = 0; r < 10; ++r) wtile<RT><<<grid, 128>>>(d, 100000, 40000, 196, r);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("wtile %4d rows per tile: %.3f ms  %.0f GB/s\n", RT, ms / 10, 4e9 / (ms / 10) / 1e6);
+}
+
+// transposed launch order: chunk fastest (a wave covers few groups, many chunks)
+__global__ void wtileT(char* p, size_t pitch, int rows, int groups, uint32_t v) {
+    const int lane = threadIdx.x & 31;
+    const int g = blockIdx.y * (blockDim.x / 32) + threadIdx.x / 32;
+    const int c = blockIdx.x;
+    if (g >= groups) return;
+    char* q = p + (size_t)c * 1024 * pitch + (size_t)g * 512 + lane * 16;
+    for (int f = 0; f < 1024 && c * 1024 + f < rows; ++f)
+        *reinterpret_cast<uint4*>(q + (size_t)f * pitch) = make_uint4(v, v, v, f);
+}
+
 template <int SEG>
 void run_seg(char* d, cudaEvent_t a, cudaEvent_t b, int wpb) {
     const int groups = 100000 / SEG;
@@ -110,6 +146,20 @@ int main() {
         run_seg<1024>(d, a, b, wpb);
         run_seg<2048>(d, a, b, wpb);
         run_seg<4096>(d, a, b, wpb);
+    }
+    run_tile<64>(d, a, b);
+    run_tile<256>(d, a, b);
+    run_tile<1024>(d, a, b);
+    run_tile<4096>(d, a, b);
+    {
+        dim3 grid(40, 49);
+        wtileT<<<grid, 128>>>(d, 100000, 40000, 196, 1);
+        cudaEventRecord(a);
+        for (int r = 0; r < 10; ++r) wtileT<<<grid, 128>>>(d, 100000, 40000, 196, r);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        printf("wtileT (chunk-fastest order): %.3f ms  %.0f GB/s\n", ms / 10, bytes / (ms / 10) / 1e6);
     }
     for (int blocks : {148, 296, 592, 1184}) {
         wblocked<<<blocks, 512>>>(d, bytes, 1);
