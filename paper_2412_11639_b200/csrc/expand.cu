@@ -253,10 +253,16 @@ __global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
     const Change<OUT>* st = reinterpret_cast<const Change<OUT>*>(a.stream);
     // Dense tiles (many changes per pixel in the chunk) are written whole by
     // the piece-0 warp: the piece prefix would re-read too many changes.
+    // Tile height by the tile's change density: the denser, the longer the
+    // prefix a piece re-reads, so pieces merge (64 -> 128 frames) and dense
+    // tiles are written whole; the merged-away pieces exit at once.
     const uint32_t tile_changes = __shfl_sync(kFull, off_hi + cnt_hi, 31) - __shfl_sync(kFull, off_lo, 0);
-    const bool whole = a.pieces == 1 || tile_changes > (uint32_t)(kPieceDensity * GP);
-    if (whole && sub0 > 0) return;  // warp-uniform
-    const int sub1 = whole ? kBins : sub0 + kPieceSubs;
+    const int span = a.pieces == 1 ? kBins
+                   : tile_changes <= (uint32_t)(kPieceSparse * GP) ? kPieceSubs
+                   : tile_changes <= (uint32_t)(kPieceDensity * GP) ? 2 * kPieceSubs
+                                                                    : kBins;
+    if (sub0 % span) return;  // warp-uniform
+    const int sub1 = min(sub0 + span, kBins);
     if (sub0 > 0) {
         // values at the piece start: the chunk-start values updated by the
         // latest change of each pixel in the sub-tiles before the piece (one

@@ -82,8 +82,9 @@ constexpr int kSub = 16;
 constexpr int kBins = kChunk / kSub;
 constexpr int kPieceSubs = 4;                // K3 tile height: 64 frames
 constexpr int kPieces = kBins / kPieceSubs;  // K3 tiles per (group, chunk)
-constexpr int kPieceDensity = 12;            // changes per pixel per chunk above which
-                                             // K3 writes the chunk as one tile
+constexpr int kPieceSparse = 2;              // changes per pixel per chunk up to which
+                                             // K3 tiles are 64 frames high (else 128)
+constexpr int kPieceDensity = 12;            // ... above which K3 writes the chunk whole
 constexpr int kPieceMaxGroups = 512;         // pieces only for narrow frames (few groups
                                              // per row: wide rows already keep the
                                              // concurrently written rows close)
