@@ -260,7 +260,8 @@ __global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
     const int span = a.pieces == 1 ? kBins
                    : tile_changes <= (uint32_t)(kPieceSparse * GP) ? kPieceSubs
                    : tile_changes <= (uint32_t)(kPieceDensity * GP) ? 2 * kPieceSubs
-                                                                    : kBins;
+                   : tile_changes <= (uint32_t)(kPieceDense * GP) ? 4 * kPieceSubs
+                                                                  : kBins;
     if (sub0 % span) return;  // warp-uniform
     const int sub1 = min(sub0 + span, kBins);
     if (sub0 > 0) {

@@ -84,7 +84,8 @@ constexpr int kPieceSubs = 4;                // K3 tile height: 64 frames
 constexpr int kPieces = kBins / kPieceSubs;  // K3 tiles per (group, chunk)
 constexpr int kPieceSparse = 2;              // changes per pixel per chunk up to which
                                              // K3 tiles are 64 frames high (else 128)
-constexpr int kPieceDensity = 12;            // ... above which K3 writes the chunk whole
+constexpr int kPieceDensity = 12;            // ... up to which 128 frames high (else 256)
+constexpr int kPieceDense = 48;              // ... above which K3 writes the chunk whole
 constexpr int kPieceMaxGroups = 512;         // pieces only for narrow frames (few groups
                                              // per row: wide rows already keep the
                                              // concurrently written rows close)
