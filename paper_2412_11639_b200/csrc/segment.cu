@@ -96,6 +96,8 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         const int f = j * 32 + rev;
         nxt[j] = f < frames ? __ldg(reinterpret_cast<const uint32_t*>(col + (size_t)f * pitch)) : 0u;
     }
+    Transpose32 tp;
+    tp.init(lane);
     int produced = 0;  // groups transposed into the ring
     // `lowest`: this warp's earliest group still to be read (published for the
     // other warps of the block), then the next batch's loads wait for them
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         if (lane == 0) vprog[wid] = lowest;
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
-            const uint32_t t = transpose32(nxt[j], lane);  // every lane shuffles
+            const uint32_t t = tp(nxt[j]);  // every lane shuffles
             rg[(produced + j) & (kRing - 1)][lane] = valid ? t : 0u;
         }
         produced += kBatch;

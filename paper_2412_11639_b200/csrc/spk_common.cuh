@@ -23,25 +23,52 @@ constexpr int kNoSpike = -(1 << 29);
 
 // 32x32 bit-matrix transpose across a warp.  On entry lane i holds row i
 // (bit j = column j); on exit lane j holds column j (bit i = row i).
-// Five butterfly stages of (funnel rotate, shuffle, bit-select): 15 issue
-// slots per lane per 32x32 block.  Lane i's partner at stage s is i^s; the
+// Five butterfly stages of shuffles.  Lane i's partner at stage s is i^s; the
 // lower lane keeps the columns with (j & s) == 0 and receives the partner's
 // same columns moved up by s, the upper lane the mirror image.
-__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
-#pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) {
-        const uint32_t m = s == 16 ? 0x0000ffffu
-                         : s == 8  ? 0x00ff00ffu
-                         : s == 4  ? 0x0f0f0f0fu
-                         : s == 2  ? 0x33333333u
-                                   : 0x55555555u;
-        const bool lo = (lane & s) == 0;
-        const uint32_t send = __funnelshift_r(x, x, lo ? s : 32 - s);
-        const uint32_t y = __shfl_xor_sync(kFull, send, s);
-        const uint32_t keep = lo ? m : ~m;
-        x = (x & keep) | (y & ~keep);
+// Implementation with the per-lane constants computed once (hoisted out of
+// the caller's loop): the two byte stages (s = 16, 8) are one PRMT each on
+// the unrotated partner word, the three bit stages one funnel rotate and one
+// 3-input bit-select (LOP3 0xE4) each -- 8 integer-ALU instructions per word
+// instead of 20 with a lane-dependent mask per stage (K2 is bound by the
+// integer ALU pipe).
+struct Transpose32 {
+    uint32_t sel16, sel8;        // PRMT selectors of the byte stages
+    uint32_t keep4, keep2, keep1;  // bits this lane keeps at stages 4, 2, 1
+    uint32_t rot4, rot2, rot1;     // rotate of the word this lane sends
+
+    __device__ __forceinline__ void init(int lane) {
+        const bool l16 = (lane & 16) == 0, l8 = (lane & 8) == 0;
+        // lower lane: [x.b0, x.b1, y.b0, y.b1], upper: [y.b2, y.b3, x.b2, x.b3]
+        sel16 = l16 ? 0x5410u : 0x3276u;
+        // lower lane: [x.b0, y.b0, x.b2, y.b2], upper: [y.b1, x.b1, y.b3, x.b3]
+        sel8 = l8 ? 0x6240u : 0x3715u;
+        keep4 = (lane & 4) == 0 ? 0x0f0f0f0fu : 0xf0f0f0f0u;
+        keep2 = (lane & 2) == 0 ? 0x33333333u : 0xccccccccu;
+        keep1 = (lane & 1) == 0 ? 0x55555555u : 0xaaaaaaaau;
+        rot4 = (lane & 4) == 0 ? 4u : 28u;
+        rot2 = (lane & 2) == 0 ? 2u : 30u;
+        rot1 = (lane & 1) == 0 ? 1u : 31u;
     }
-    return x;
+    __device__ __forceinline__ static uint32_t bitsel(uint32_t x, uint32_t y, uint32_t keep) {
+        uint32_t r;  // (x & keep) | (y & ~keep)
+        asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(x), "r"(y), "r"(keep));
+        return r;
+    }
+    __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+        x = __byte_perm(x, __shfl_xor_sync(kFull, x, 16), sel16);
+        x = __byte_perm(x, __shfl_xor_sync(kFull, x, 8), sel8);
+        x = bitsel(x, __shfl_xor_sync(kFull, __funnelshift_r(x, x, rot4), 4), keep4);
+        x = bitsel(x, __shfl_xor_sync(kFull, __funnelshift_r(x, x, rot2), 2), keep2);
+        x = bitsel(x, __shfl_xor_sync(kFull, __funnelshift_r(x, x, rot1), 1), keep1);
+        return x;
+    }
+};
+
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+    Transpose32 t;  // loop-invariant: the compiler hoists init out of callers' loops
+    t.init(lane);
+    return t(x);
 }
 
 // The reference's uint8 rule for a run value: round-half-away(255*N/span)
