@@ -68,6 +68,83 @@ __global__ void wtile(char* p, size_t pitch, int rows, int groups, uint32_t v) {
         *reinterpret_cast<uint4*>(q + (size_t)f * pitch) = make_uint4(v, v, v, f);
 }
 
+// fused-K2 pattern: one wave of 8-warp blocks, warp = 32 pixels (32 B of each
+// row), per 32-row word every lane stores 8 u32 (lane = pixel quad q x row
+// phase j: rows 4k + j, k = 0..7); ALU work between words simulates the scan
+template <int SPIN>
+__global__ void wk2(char* p, size_t pitch, int rows, int warps, uint32_t v) {
+    const int lane = threadIdx.x & 31;
+    const int w = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (w >= warps) return;
+    const int q = lane & 7, j = lane >> 3;
+    char* base = p + (size_t)w * 32 + q * 4 + (size_t)j * pitch;
+    uint32_t x = v + lane;
+    for (int g = 0; g * 32 < rows; ++g) {
+#pragma unroll
+        for (int s = 0; s < SPIN; ++s) x = x * 1664525u + 1013904223u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<uint32_t*>(base + (size_t)(32 * g + 4 * k) * pitch) = x + k;
+    }
+    if (x == 0x12345678u) p[0] = 1;
+}
+
+// variants: MODE 1 = per lane 16 B of one row (2 x STG.128 per lane-word,
+// rows l and l+... 32 B per row per warp); MODE 2 = block-cooperative: the 8
+// warps of a block write 256 contiguous bytes of each row (warp w: rows
+// 32g + 4w .. 4w+3, lane 8 B)
+template <int MODE>
+__global__ void wk2v(char* p, size_t pitch, int rows, int warps, uint32_t v) {
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x / 32;
+    const int w = blockIdx.x * (blockDim.x / 32) + wib;
+    if (w >= warps) return;
+    if (MODE == 1) {
+        // lane l: rows 32g + l (16 B = pixels 0..15) -- half rows: lanes 0..15 pixels 0..15 of rows
+        // 2k + (l>>4)?  simpler: lane l covers row 32g + (l>>1) + 16 * i, pixel half (l & 1)
+        char* base = p + (size_t)w * 32 + (lane & 1) * 16;
+        for (int g = 0; g * 32 < rows; ++g)
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+                *reinterpret_cast<uint4*>(base + (size_t)(32 * g + 16 * i + (lane >> 1)) * pitch) =
+                    make_uint4(v, g, i, lane);
+    } else {
+        const int b0 = blockIdx.x * 256;
+        if (b0 + 8 * lane + 8 > 100000) return;
+        char* base = p + (size_t)b0 + 8 * lane;
+        for (int g = 0; g * 32 < rows; ++g)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                *reinterpret_cast<uint2*>(base + (size_t)(32 * g + 4 * wib + k) * pitch) = make_uint2(v, g);
+    }
+}
+
+template <int MODE>
+void run_k2v(char* d, cudaEvent_t a, cudaEvent_t b) {
+    const int warps = 100000 / 32;
+    wk2v<MODE><<<(warps + 7) / 8, 256>>>(d, 100000, 40000, warps, 1);
+    cudaEventRecord(a);
+    for (int r = 0; r < 10; ++r) wk2v<MODE><<<(warps + 7) / 8, 256>>>(d, 100000, 40000, warps, r);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("wk2v mode %d: %.3f ms  %.0f GB/s\n", MODE, ms / 10, 4e9 / (ms / 10) / 1e6);
+}
+
+template <int SPIN>
+void run_k2(char* d, cudaEvent_t a, cudaEvent_t b) {
+    const int warps = 100000 / 32;
+    wk2<SPIN><<<(warps + 7) / 8, 256>>>(d, 100000, 40000, warps, 1);
+    cudaEventRecord(a);
+    for (int r = 0; r < 10; ++r) wk2<SPIN><<<(warps + 7) / 8, 256>>>(d, 100000, 40000, warps, r);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("wk2 (fused-K2 pattern, spin %d): %.3f ms  %.0f GB/s\n", SPIN, ms / 10, 4e9 / (ms / 10) / 1e6);
+}
+
 template <int RT>
 void run_tile(char* d, cudaEvent_t a, cudaEvent_t b) {
     dim3 grid((196 + 3) / 4, (40000 + RT - 1) / RT);
@@ -147,6 +224,11 @@ int main() {
         run_seg<2048>(d, a, b, wpb);
         run_seg<4096>(d, a, b, wpb);
     }
+    run_k2v<1>(d, a, b);
+    run_k2v<2>(d, a, b);
+    run_k2<0>(d, a, b);
+    run_k2<64>(d, a, b);
+    run_k2<256>(d, a, b);
     run_tile<64>(d, a, b);
     run_tile<256>(d, a, b);
     run_tile<1024>(d, a, b);
