@@ -57,6 +57,18 @@ SPK_HD int fsub(int a, int b) {  // a - b
 #endif
 }
 
+// k ? a : b for an integer k in {0, 1}, as b + k * (a - b): two IMADs on the
+// FMA pipe instead of a SEL on the (saturated) integer ALU pipe.
+SPK_HD int fsel(int k, int a, int b) {
+#ifdef __CUDA_ARCH__
+    int r;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(k), "r"(fsub(a, b)), "r"(b));
+    return r;
+#else
+    return k ? a : b;
+#endif
+}
+
 enum { kFSR = 0, kSSR = 1, kTFI = 2, kTFP = 3 };
 
 template <int METHOD>
@@ -275,10 +287,12 @@ struct Scan {
         bool brk = fbrk;
         bool emit = fbrk & (lo < kLim);
         if (METHOD == kSSR) {
-            const bool k = (t & 1) != 0;
-            const int l = k ? l1 : l0;
-            const int glo = k ? g1 : g0;
-            const uint32_t ghw = k ? h1 : h0;
+            // parity-slot selects on the FMA pipe (the SSR scan saturates the ALU pipe)
+            const int ki = t & 1, kn = ki ^ 1;
+            const bool k = ki != 0;
+            const int l = fsel(ki, l1, l0);
+            const int glo = fsel(ki, g1, g0);
+            const uint32_t ghw = (uint32_t)fsel(ki, (int)h1, (int)h0);
             const bool stale = l < sub0;
             const int gap = fsub(ii, l);
             const int gd = fsub(gap, glo);
@@ -293,14 +307,14 @@ struct Scan {
             const int keep = gext ? min(glo, gap) : glo;
             const int nglo = fresh ? kNoPair : (gnone ? gap : keep);
             const uint32_t nghw = (fresh | gnone) ? 0u : (ghw | (uint32_t)gext);
-            l0 = k ? l0 : ii;
-            l1 = k ? ii : l1;
-            fl0 = k ? fl0 : n;
-            fl1 = k ? n : fl1;
-            g0 = k ? g0 : nglo;
-            g1 = k ? nglo : g1;
-            h0 = k ? h0 : nghw;
-            h1 = k ? nghw : h1;
+            l0 = fsel(kn, ii, l0);
+            l1 = fsel(ki, ii, l1);
+            fl0 = fsel(kn, n, fl0);
+            fl1 = fsel(ki, n, fl1);
+            g0 = fsel(kn, nglo, g0);
+            g1 = fsel(ki, nglo, g1);
+            h0 = (uint32_t)fsel(kn, (int)nghw, (int)h0);
+            h1 = (uint32_t)fsel(ki, (int)nghw, (int)h1);
             sub0 = brk ? ii : sub0;
             sf = brk ? n : sf;
             ii = fadd(ii, 1);
