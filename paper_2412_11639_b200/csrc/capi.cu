@@ -211,7 +211,8 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     SPK_CK(cudaMemcpyAsync(w.cursor.p, w.offs.p, (size_t)w.nbins * sizeof(uint32_t),
                            cudaMemcpyDeviceToDevice, s));
     f.cursor = static_cast<uint32_t*>(w.cursor.p);
-    k_fin_scatter<OUT><<<(unsigned)((sa.npix + 255) / 256), 256, 0, s>>>(f);
+    const unsigned nseg = (unsigned)((sa.cap + kFinSeg - 1) / kFinSeg);
+    k_fin_scatter<OUT><<<dim3((unsigned)((sa.npix + 255) / 256), nseg), 256, 0, s>>>(f);
     SPK_LAUNCHED("k_fin_scatter");
     mark(2, s);
 

@@ -106,12 +106,19 @@ __global__ void __launch_bounds__(256) k_fin_scatter(FinArgs a) {
     const uint32_t cnt = a.counts[p];
     const bool over = cnt > (uint32_t)a.cap;  // k_fixup rewrites it: values don't matter
     const int n = (int)min(cnt, (uint32_t)a.cap);
+    // blockIdx.y: this thread's segment of kFinSeg runs (runs are independent
+    // here -- a value needs only the next run's start -- so a pixel's list is
+    // spread over several threads: enough loads and atomics in flight even
+    // for sensors with few pixels)
+    const int kb = (int)blockIdx.y * kFinSeg;
+    if (kb >= n) return;
+    const int ke = min(n, kb + kFinSeg);
     const spk_run_t* rp = a.runs + p * a.cap;
     const uint32_t lastp = (uint32_t)a.last[p];
     Change<OUT>* stp = reinterpret_cast<Change<OUT>*>(a.stream);
     OUT* tb = reinterpret_cast<OUT*>(a.tblv);
     const int64_t total_frames = (int64_t)a.nchunks << kChunkLog2;
-    for (int k0 = 0; k0 < n; k0 += B) {
+    for (int k0 = kb; k0 < ke; k0 += B) {
         spk_run_t r[B + 1];
 #pragma unroll
         for (int j = 0; j <= B; ++j)
@@ -119,7 +126,7 @@ __global__ void __launch_bounds__(256) k_fin_scatter(FinArgs a) {
         uint32_t pos[B];
 #pragma unroll
         for (int j = 0; j < B; ++j) {
-            if (k0 + j < n) {
+            if (k0 + j < ke) {
                 const int st = max((int)r[j].start, 0);  // see K2b: starts before frame 0
                 const int c = st >> kChunkLog2;
                 const int bi = (st & (kChunk - 1)) / kSub;
@@ -128,7 +135,7 @@ __global__ void __launch_bounds__(256) k_fin_scatter(FinArgs a) {
         }
 #pragma unroll
         for (int j = 0; j < B; ++j) {
-            if (k0 + j < n) {
+            if (k0 + j < ke) {
                 const int st = max((int)r[j].start, 0);
                 const uint32_t fo = (uint32_t)(st & (kChunk - 1));
                 const OUT val = over ? OUT(0) : OutVal<OUT>::run(r[j].intervals, r[j + 1].start - r[j].start);

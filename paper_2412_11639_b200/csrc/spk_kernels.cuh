@@ -141,6 +141,7 @@ struct FinArgs {
     uint32_t* cursor;      // K2c: running copy of offs (claimed with atomics)
     void* stream;          // Change<OUT>[total] (K2c)
 };
+constexpr int kFinSeg = 64;       // K2c: runs per thread (a pixel's list spans cap / kFinSeg threads)
 constexpr int kFinWarps = 16;     // K2b/K2c: warps per block (block = one pixel group)
 constexpr int kFinWindow = 128;   // chunks per shared-memory window (32 KB of counters)
 
