@@ -289,7 +289,6 @@ struct Scan {
         if (METHOD == kSSR) {
             // parity-slot selects on the FMA pipe (the SSR scan saturates the ALU pipe)
             const int ki = t & 1, kn = ki ^ 1;
-            const bool k = ki != 0;
             const int l = fsel(ki, l1, l0);
             const int glo = fsel(ki, g1, g0);
             const uint32_t ghw = (uint32_t)fsel(ki, (int)h1, (int)h0);

@@ -11,5 +11,5 @@ cmd = [b.nvcc(), *b.NVCC_FLAGS, *os.environ['NVCC_EXTRA'].split(), '-I' + str(b.
 subprocess.run(cmd, check=True)
 " || { echo "build failed: $v"; continue; }
   echo "== variant: ${v:-default}"
-  python profiles/quickbench.py
+  python profiles/${PROBE:-quickbench.py}
 done
