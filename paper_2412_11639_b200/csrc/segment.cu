@@ -90,31 +90,46 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     };
 
     // Producer (warp-uniform): kBatch groups per refill, loads one batch ahead.
+    // The loads walk a running pointer (one 64-bit add per group instead of a
+    // 64-bit multiply-add per load); a batch's ring slots never wrap
+    // (kBatch divides kRing and `produced` is a multiple of kBatch).
+    static_assert(kRing % kBatch == 0, "a batch must not wrap the ring");
+    const size_t gstride = (size_t)32 * pitch;  // bytes between a lane's rows of consecutive groups
+    const char* lp = col + (size_t)rev * pitch;  // this lane's row of the next group to load
+    int lf = rev;                                // its frame
     uint32_t nxt[kBatch];
+    int produced = 0;  // groups transposed into the ring
+    // (SSR keeps per-load addressing: its spike loop schedules better with
+    // the pointer state out of the registers -- SSR K2 5.94 vs 6.54 ms)
+    auto load_batch = [&]() {
 #pragma unroll
-    for (int j = 0; j < kBatch; ++j) {
-        const int f = j * 32 + rev;
-        nxt[j] = f < frames ? __ldg(reinterpret_cast<const uint32_t*>(col + (size_t)f * pitch)) : 0u;
-    }
+        for (int j = 0; j < kBatch; ++j) {
+            if constexpr (METHOD == kFSR) {
+                nxt[j] = lf < frames ? __ldg(reinterpret_cast<const uint32_t*>(lp)) : 0u;
+                lp += gstride;
+                lf += 32;
+            } else {
+                const int f = (produced + j) * 32 + rev;
+                nxt[j] = f < frames ? __ldg(reinterpret_cast<const uint32_t*>(col + (size_t)f * pitch)) : 0u;
+            }
+        }
+    };
+    load_batch();
     Transpose32 tp;
     tp.init(lane);
-    int produced = 0;  // groups transposed into the ring
     // `lowest`: this warp's earliest group still to be read (published for the
     // other warps of the block), then the next batch's loads wait for them
     auto produce = [&](int lowest) {
         if (lane == 0) vprog[wid] = lowest;
+        uint32_t* slot = &rg[produced & (kRing - 1)][lane];
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
             const uint32_t t = tp(nxt[j]);  // every lane shuffles
-            rg[(produced + j) & (kRing - 1)][lane] = valid ? t : 0u;
+            slot[32 * j] = valid ? t : 0u;
         }
         produced += kBatch;
         throttle(produced);
-#pragma unroll
-        for (int j = 0; j < kBatch; ++j) {
-            const int f = (produced + j) * 32 + rev;
-            nxt[j] = f < frames ? __ldg(reinterpret_cast<const uint32_t*>(col + (size_t)f * pitch)) : 0u;
-        }
+        load_batch();
         __syncwarp();
     };
 
