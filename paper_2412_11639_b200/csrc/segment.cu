@@ -82,10 +82,14 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     // The stored pair lives in its own registers (written only on an emit), so
     // the automaton's next update does not wait for the store to read them.
     int o_rs = 0, o_cnt = 0;
+    // `wp` = rp + nrun while nrun < cap (a running store pointer: no 64-bit
+    // address arithmetic per emit); past the capacity nothing is stored
+    spk_run_t* wp = rp;
     auto emit = [&](bool e, int rs, int cnt) {
         o_rs = e ? rs : o_rs;
         o_cnt = e ? cnt : o_cnt;
-        st_run_if(e & (nrun <= capm1), rp + min(nrun, capm1), o_rs, o_cnt);
+        st_run_if(e & (nrun <= capm1), wp, o_rs, o_cnt);
+        wp += (int)e;
         nrun += (int)e;
     };
 
