@@ -4,17 +4,21 @@
 // 358-390) and the column->row gather of reconstruct_into (416-419).
 //
 // Mapping: one thread per pixel, one warp per 32-bit plane word (32
-// consecutive pixels).  For every group of 32 frames lane i loads the warp's
-// word from plane 32g + (31 - i); a 5-stage shuffle transpose turns the 32x32
-// bit block into one 32-frame word per pixel with the earliest frame in bit
-// 31, and the lane walks its spikes with clz, one spike per warp iteration
-// through the branch-free Scan automaton (spk_fsm.cuh).  Plane loads run one
-// batch (kBatch groups = 256 frames) ahead of the scan.
+// consecutive pixels), 8 warps per block (one 32-byte sector of every plane
+// row, shared through L2 under a drift throttle).  For every group of 32
+// frames lane i loads the warp's word from plane 32g + (31 - i); a 5-stage
+// shuffle transpose (Transpose32) turns the 32x32 bit block into one 32-frame
+// word per pixel with the earliest frame in bit 31, kept in a per-warp ring
+// in shared memory.  FSR: every lane walks its own pixel four words per
+// iteration (fsr_batch4: bit-parallel acceptance up to the next event, one
+// exact automaton step for the event); SSR: bulk (ssr_flags) or word-lockstep
+// spike mode per warp.  Plane loads run one batch (kBatch groups = 256
+// frames) ahead of the scan.
 //
 // Output per pixel p: runs[p*cap + k] = {start frame, intervals} (k < cap),
 // counts[p] (may exceed cap: overflow) and last[p] (last spike, -1 if none).
-// k_finalize (K2b) turns them into run values + the run table for K3;
-// overflowed pixels are rewritten exactly by k_fixup after K3.
+// K2b/K2c (expand.cu) turn them into values and a frame-sorted change stream
+// for K3; overflowed pixels are rewritten exactly by k_fixup after K3.
 #include "spk_fsm.cuh"
 #include "spk_kernels.cuh"
 

@@ -8,9 +8,8 @@ namespace spk {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-// Frames per table chunk: the expand kernel (K3) tiles time in chunks of
-// kChunk frames and the segment kernel (K2) records, for every pixel and chunk
-// boundary, which run covers that frame ("run table").
+// Frames per chunk: the expand kernel (K3) tiles time in chunks of kChunk
+// frames, and K2c records every pixel's value at each chunk start.
 constexpr int kChunkLog2 = 10;
 constexpr int kChunk = 1 << kChunkLog2;
 

@@ -242,7 +242,7 @@ struct Fsm {
 // spikes some lane takes one in most iterations.  Every case is therefore a
 // select, and a closed run is a single predicated 8-byte store of
 // (start frame, intervals); its end is the next run's start (or the pixel's
-// last spike) and its value is computed later by k_finalize.
+// last spike) and its value is computed later by K2c (expand.cu).
 //
 // Encodings (frames < 2^29):
 //   lo >= kLim          no interval yet (kNoPair initially; after the first
