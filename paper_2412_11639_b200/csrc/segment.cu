@@ -217,24 +217,45 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     // own pace -- a window of four words per iteration, stopping at the first
     // event (fsr_batch4) -- so a lane with many breaks does not hold the others
     // back word by word; the ring bounds how far lanes may drift apart.
+    // After an iteration in which no lane met an event, the warp tries kQuiet
+    // words at once (fsr_quiet: the test alone, no selection across words);
+    // lanes whose window holds an event take the 4-word batch in the same
+    // iteration.  Moving scenes rarely have such an iteration, static scenes
+    // and long quiet stretches almost always.
+    static_assert(kQuiet + kBatch <= kRing, "a quiet window must fit the ring beside a batch");
     int wi = 0;    // first word of this lane's window
     int cpos = 0;  // frames of word wi already consumed
+    bool quiet = false;  // warp-uniform: the last iteration had no event
     // Groups past the end are produced as zero words, so a window never
     // needs a bounds check.
     for (;;) {
         const bool more = wi < ngroups;
         const bool ready = wi + 4 <= produced;
-        // refill only when a lane is starved, and only into slots no lane can
-        // still read (lowest = the earliest window start)
-        if (__any_sync(kFull, more & !ready)) {
+        // refill only when a lane is starved (or, when quiet, short of a quiet
+        // window), and only into slots no lane can still read (lowest = the
+        // earliest window start)
+        if (__any_sync(kFull, more & (quiet ? wi + kQuiet > produced : !ready))) {
             const int lowest = (int)__reduce_min_sync(kFull, (unsigned)(more ? wi : 0x7fffffff));
-            if (produced < ngroups + 3 && produced + kBatch <= lowest + kRing) produce(lowest);
+            if (produced < ngroups + kQuiet - 1 && produced + kBatch <= lowest + kRing) produce(lowest);
         }
         if (!__any_sync(kFull, more)) break;
-        if (more & ready)
-            wi += fsr_batch4(sc, rg[wi & (kRing - 1)][lane], rg[(wi + 1) & (kRing - 1)][lane],
-                             rg[(wi + 2) & (kRing - 1)][lane], rg[(wi + 3) & (kRing - 1)][lane],
-                             wi * 32, cpos, emit);
+        bool tookq = false;
+        if (quiet && __all_sync(kFull, !more | (wi + kQuiet <= produced))) {
+            if (more) {
+                tookq = fsr_quiet<kQuiet>(sc, [&](int k) { return rg[(wi + k) & (kRing - 1)][lane]; },
+                                          wi * 32, cpos);
+                wi += tookq ? kQuiet : 0;
+            }
+        }
+        bool ev = false;
+        if (more & !tookq & (wi + 4 <= produced)) {
+            const int k = fsr_batch4(sc, rg[wi & (kRing - 1)][lane], rg[(wi + 1) & (kRing - 1)][lane],
+                                     rg[(wi + 2) & (kRing - 1)][lane], rg[(wi + 3) & (kRing - 1)][lane],
+                                     wi * 32, cpos, emit);
+            ev = k < 4;
+            wi += k;
+        }
+        quiet = !__any_sync(kFull, ev);
     }
     }
     if (lane == 0) vprog[wid] = 0x7fffffff;  // done: never hold the others back

@@ -253,6 +253,12 @@ struct Fsm {
 //   violation resets both slots by moving sub0 only; glo >= kLim = no gap yet.
 constexpr int kLim = 1 << 29;
 
+// FSR quiet windows: words accepted at once by fsr_quiet (segment kernel)
+#ifndef SPK_QUIET
+#define SPK_QUIET 8
+#endif
+constexpr int kQuiet = SPK_QUIET;
+
 template <int METHOD>
 struct Scan {
     int last, lo, rs, cnt, nrun;
@@ -545,6 +551,43 @@ SPK_HD int fsr_batch4(SC& sc, uint32_t W0, uint32_t W1, uint32_t W2, uint32_t W3
         emit(e, rs, cnt);
     }
     return ev ? kk : 4;
+}
+
+// FSR over N consecutive words when the window holds no event at all: the
+// fsr_batch4 test on every word (each word's first remaining spike against
+// the last spike before it), OR-ed.  With no violation anywhere the whole
+// window is accepted at once (cnt += spikes, last = the latest spike,
+// cpos = 0) and true is returned; otherwise nothing changes and the caller
+// takes the exact fsr_batch4 path.  No selection across words is needed, so
+// a quiet window costs about half a 4-word batch per word (static scenes,
+// long streams).  word(k) returns word k of the window; words past the end
+// of the stream must read as 0.
+template <int N, class SC, class WORD>
+SPK_HD bool fsr_quiet(SC& sc, WORD&& word, int base0, int& cpos) {
+    const int lo = sc.lo;
+    const uint32_t hw = sc.hw;
+    const uint32_t sh1 = (uint32_t)lo, sh2 = (uint32_t)lo + hw;
+    const uint32_t twom = lo >= 2 ? 0xffffffffu : 0u;
+    int pv = sc.last + lo;  // last spike before the word under test, plus lo
+    uint32_t bad = 0u, n = 0u;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const uint32_t w = word(k);
+        const uint32_t r = k == 0 ? w & bit_shr_clamp(0xffffffffu, 0u, (uint32_t)cpos) : w;
+        const int base = base0 + 32 * k;
+        const uint32_t Q = bit_shr_clamp(w, 0u, sh1) | bit_shr_clamp(w, 0u, sh2);
+        const int f = bit_clz(r | 1u);
+        const uint32_t fb = (0x80000000u >> f) & r;
+        const uint32_t bad0 = (uint32_t)(base + f - pv) > hw ? fb : 0u;
+        bad |= (r & ~(Q | fb)) | (r & (w >> 1) & w & twom) | bad0;
+        n += (uint32_t)bit_popc(r);
+        pv = r ? base + bit_clz(r & (0u - r)) + lo : pv;
+    }
+    if (bad) return false;
+    sc.cnt += (int)n;
+    sc.last = pv - lo;
+    cpos = 0;
+    return true;
 }
 
 // FSR: the remaining spikes S of word So (first frame in bit 31, frames

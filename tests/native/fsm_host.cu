@@ -184,6 +184,52 @@ extern "C" long batch_runs(const uint8_t* bits, long frames, int method, long* s
     return n;
 }
 
+// The FSR driver of the segment kernel with quiet windows: after an
+// iteration without an event, kQuiet words are tried at once (fsr_quiet),
+// and the 4-word batch runs when they hold an event.
+extern "C" long quiet_runs(const uint8_t* bits, long frames, int method, long* start, long* end,
+                           long* cnt, long cap) {
+    if (method != 0) return word_runs(bits, frames, method, start, end, cnt, cap);
+    long n = 0, last = -1;
+    auto put = [&](bool e, int rs, int c) {
+        if (e) {
+            if (n < cap) {
+                start[n] = rs;
+                cnt[n] = c;
+            }
+            ++n;
+        }
+    };
+    const long ngroups = (frames + 31) / 32;
+    std::vector<uint32_t> words(ngroups + spk::kQuiet, 0u);
+    for (long f = 0; f < frames; ++f)
+        if (bits[f]) {
+            words[f / 32] |= 0x80000000u >> (f % 32);
+            last = f;
+        }
+    spk::Scan<spk::kFSR> sc;
+    sc.init();
+    long wi = 0;
+    int cpos = 0;
+    bool quiet = false;
+    while (wi < ngroups) {
+        if (quiet && spk::fsr_quiet<spk::kQuiet>(sc, [&](int k) { return words[wi + k]; }, (int)(wi * 32),
+                                                 cpos)) {
+            wi += spk::kQuiet;
+            continue;
+        }
+        const int k = spk::fsr_batch4(sc, words[wi], words[wi + 1], words[wi + 2], words[wi + 3],
+                                      (int)(wi * 32), cpos, put);
+        quiet = k == 4;
+        wi += k;
+    }
+    int rs, c;
+    const bool e = sc.tail(rs, c);
+    put(e, rs, c);
+    for (long k = 0; k < n && k < cap; ++k) end[k] = (k + 1 < n) ? start[k + 1] : last;
+    return n;
+}
+
 // the u8 run-value rule as compiled for the kernels
 extern "C" void host_run_u8(const uint32_t* n, const uint32_t* span, uint32_t* out, long m) {
     for (long i = 0; i < m; ++i) out[i] = spk::run_u8(n[i], span[i]);

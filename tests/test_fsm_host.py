@@ -36,6 +36,8 @@ def fsm():
     h.word_runs.argtypes = h.fsm_runs.argtypes
     h.batch_runs.restype = C.c_long
     h.batch_runs.argtypes = h.fsm_runs.argtypes
+    h.quiet_runs.restype = C.c_long
+    h.quiet_runs.argtypes = h.fsm_runs.argtypes
     h.ssr_state_check.restype = C.c_long
     h.ssr_state_check.argtypes = [C.c_void_p, C.c_long]
     h.ssrword_runs.restype = C.c_long
@@ -50,7 +52,8 @@ def fsm():
             return s[:n], e[:n], c[:n]
         return run
     return {"fsm": make(h.fsm_runs), "scan": make(h.scan_runs), "word": make(h.word_runs),
-            "batch": make(h.batch_runs), "ssrword": make(h.ssrword_runs), "_h": h}
+            "batch": make(h.batch_runs), "quiet": make(h.quiet_runs),
+            "ssrword": make(h.ssrword_runs), "_h": h}
 
 
 def if_stream(rng, t, segs, flips):
@@ -66,7 +69,7 @@ def if_stream(rng, t, segs, flips):
     return b ^ (rng.random(t) < flips).astype(np.uint8)
 
 
-@pytest.mark.parametrize("kind", ["fsm", "scan", "word", "batch", "ssrword"])
+@pytest.mark.parametrize("kind", ["fsm", "scan", "word", "batch", "quiet", "ssrword"])
 @pytest.mark.parametrize("family", ["noise", "if", "if_noisy", "if_rare_flips"])
 def test_fsm_matches_oracle(fsm, oracle, family, kind):
     run = fsm[kind]
@@ -83,7 +86,7 @@ def test_fsm_matches_oracle(fsm, oracle, family, kind):
             assert all(np.array_equal(x, y) for x, y in zip(got, want)), (family, m, t)
 
 
-@pytest.mark.parametrize("kind", ["fsm", "scan", "word", "batch", "ssrword"])
+@pytest.mark.parametrize("kind", ["fsm", "scan", "word", "batch", "quiet", "ssrword"])
 def test_fsm_golden_rows(fsm, golden_dir, kind):
     z = np.load(golden_dir / "rows.npz")
     for name in sorted({k.split("/")[0] for k in z.files}):
@@ -122,7 +125,7 @@ def test_run_u8_exact_vs_integer_rule(fsm):
     assert np.array_equal(out, np.floor(np.clip(v, 0, 255) + 0.5).astype(np.uint32))
 
 
-@pytest.mark.parametrize("kind", ["batch", "ssrword"])
+@pytest.mark.parametrize("kind", ["batch", "quiet", "ssrword"])
 def test_bulk_drivers_long_streams(fsm, oracle, kind):
     """long stable runs (rates near integer reciprocals, slow drifts, rare
     flips): the bit-parallel tests accept many words in a row"""
