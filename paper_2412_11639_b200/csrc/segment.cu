@@ -110,10 +110,12 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     // (SSR keeps per-load addressing: its spike loop schedules better with
     // the pointer state out of the registers -- SSR K2 5.94 vs 6.54 ms)
     auto load_batch = [&]() {
+        const bool full = lf + 32 * (kBatch - 1) < frames;  // warp-uniform (lf - rev is)
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
             if constexpr (METHOD == kFSR) {
-                nxt[j] = lf < frames ? __ldg(reinterpret_cast<const uint32_t*>(lp)) : 0u;
+                // (a batch wholly inside the stream needs no per-row check)
+                nxt[j] = full || lf < frames ? __ldg(reinterpret_cast<const uint32_t*>(lp)) : 0u;
                 lp += gstride;
                 lf += 32;
             } else {
@@ -136,7 +138,9 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
             slot[32 * j] = valid ? t : 0u;
         }
         produced += kBatch;
-        throttle(produced);
+        // the drift bound is checked every other batch (the block's warps
+        // stay within kDrift + kBatch groups)
+        if ((produced & kBatch) == 0) throttle(produced);
         load_batch();
         __syncwarp();
     };
