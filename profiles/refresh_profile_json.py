@@ -28,6 +28,8 @@ for r in rows[2:]:
     seen[k] = r  # the last (warm) launch of each kernel
 here = Path(__file__).resolve().parent
 for kern in ("k_segment", "k_expand"):
+    if kern not in seen:  # capture restricted to other kernels: keep the file
+        continue
     r = seen[kern]
     rd, wr = num(r[col("dram__bytes_read.sum")]), num(r[col("dram__bytes_write.sum")])
     unit_r, unit_w = rows[1][col("dram__bytes_read.sum")], rows[1][col("dram__bytes_write.sum")]
