@@ -153,7 +153,9 @@ private:
     int width_, height_;
 };
 
-// `workers` is accepted for signature compatibility: one call = one GPU.
+// `workers` > 1 splits the pixels into that many bands over the visible GPUs
+// (round-robin; spk_reconstruct_host_multi); the result is identical for any
+// worker count, as in the reference (reconstruct.hpp:70-72).
 std::vector<IntensityImage> reconstruct(const SpikeVolume& volume, ReconMethod method,
                                         int workers = 0);
 void reconstruct(const SpikeVolume& volume, ReconMethod method, int workers,

@@ -202,6 +202,19 @@ int spk_upload_planes(const spk_geom* g, const void* h_payload, size_t src_pitch
 int spk_reconstruct_host(const spk_geom* g, const void* h_payload, int method, int tfp_window,
                          int out_type, void* h_out, size_t out_pitch);
 
+/* reconstruct() with `workers` GPUs (SURVEY.md 8(b) spk_reconstruct_sharded;
+ * the reference's parallel split, proj/src/reconstruct.cpp:456-466, is a
+ * pixel range per OpenMP thread, "identical for any worker count",
+ * proj/include/spikecam/reconstruct.hpp:70-72): the pixels are cut into
+ * nbands bands on 128-pixel boundaries and band i runs on CUDA device
+ * devices[i] (a device may take several bands), each from its own host
+ * thread: upload of its plane columns, reconstruction, download into its
+ * columns of h_out.  Arguments otherwise as spk_reconstruct_host; the output
+ * is identical for any band count.  Synchronous. */
+int spk_reconstruct_host_multi(const spk_geom* g, const void* h_payload, int method, int tfp_window,
+                               int out_type, void* h_out, size_t out_pitch, const int32_t* devices,
+                               int32_t nbands);
+
 /* Many volumes of one geometry through the host boundary, pipelined: the
  * upload and reconstruction of volume i+1 overlap the download of volume i
  * (two stream lanes), so a sequence is bound by the slower PCIe direction.
@@ -281,6 +294,9 @@ int64_t spk_launch_count(int reset);
 int spk_set_timing(int enable);
 int spk_last_timing(float* segment_ms, float* finalize_ms, float* expand_ms, float* fixup_ms);
 const char* spk_last_error(void);
+/* number of visible CUDA devices (the C++ drop-in spreads `workers` bands
+ * over them); -1 when the CUDA runtime reports an error */
+int spk_device_count(void);
 int spk_version(void);
 
 /* ---- quality metrics and the stability check ------- */

@@ -19,6 +19,7 @@ from .recon import (  # noqa: F401
     reconstruct,
     reconstruct_host,
     reconstruct_host_batch,
+    reconstruct_host_multi,
     segments,
     synth,
     write_spk,

@@ -112,15 +112,26 @@ std::vector<uint8_t> stream_payload(const SpikeLikeStream& s) {
     return pay;  // 1 pixel -> one byte per plane, bit 0
 }
 
+// workers > 1: that many pixel bands, spread round-robin over the visible
+// CUDA devices (spk_reconstruct_host_multi); otherwise one call on the
+// current device.  The result is the same for any worker count.
 template <typename T>
-std::vector<T> recon_host(const PackedSpikes& sp, ReconMethod m, int out_type) {
+std::vector<T> recon_host(const PackedSpikes& sp, ReconMethod m, int out_type, int workers = 1) {
     const size_t npix = static_cast<size_t>(sp.width) * sp.height;
     std::vector<T> out(npix * sp.frames);
     const spk_geom g = geom(sp.width, sp.height, sp.frames);
     if (sp.payload.size() != plane_bytes(sp.width, sp.height) * sp.frames)
         throw std::invalid_argument("PackedSpikes: payload size does not match the geometry");
-    ck(spk_reconstruct_host(&g, sp.payload.data(), static_cast<int>(m.kind), m.tfp_window, out_type,
-                            out.data(), npix));
+    if (workers > 1) {
+        const int ndev = std::max(1, spk_device_count());
+        std::vector<int32_t> devs(static_cast<size_t>(workers));
+        for (int i = 0; i < workers; ++i) devs[static_cast<size_t>(i)] = i % ndev;
+        ck(spk_reconstruct_host_multi(&g, sp.payload.data(), static_cast<int>(m.kind), m.tfp_window,
+                                      out_type, out.data(), npix, devs.data(), workers));
+    } else {
+        ck(spk_reconstruct_host(&g, sp.payload.data(), static_cast<int>(m.kind), m.tfp_window,
+                                out_type, out.data(), npix));
+    }
     return out;
 }
 
@@ -297,14 +308,14 @@ std::vector<double> reconstruct_pixel(const SpikeLikeStream& stream, ReconMethod
 
 void reconstruct(const SpikeVolume& volume, ReconMethod method, int workers,
                  std::vector<IntensityImage>& out) {
-    (void)workers;  // one GPU per call; the result does not depend on it
+    // workers <= 0: the default (one GPU); the result does not depend on it
     check_method(method);
     const int W = volume.width(), H = volume.height();
     const size_t T = static_cast<size_t>(volume.frames());
     if (out.size() != T || (T > 0 && (out[0].width != W || out[0].height != H)))
         out.assign(T, IntensityImage(W, H));  // reuse rule of reconstruct.cpp:452-455
     if (T == 0) return;
-    const std::vector<double> frames = reconstruct_f64(pack(volume), method);
+    const std::vector<double> frames = recon_host<double>(pack(volume), method, SPK_OUT_F64, workers);
     const size_t npix = static_cast<size_t>(W) * H;
     for (size_t n = 0; n < T; ++n)
         std::copy_n(frames.begin() + n * npix, npix, out[n].values.begin());

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "spk_common.cuh"
@@ -660,6 +661,49 @@ size_t spk_plane_pitch(int32_t width, int32_t height) {
     return (min_pitch(npix) + 15) & ~(size_t)15;  // 16-B rows: vector/TMA friendly
 }
 
+namespace {
+
+// One pixel band (a bn x 1 volume) through the host boundary on the current
+// device: its plane columns are read from a payload of src_pitch bytes per
+// frame, its frames written to columns [0, bn) of h_out (out_pitch elements
+// per frame).  Synchronous.
+int spk_reconstruct_host_band(const spk_geom* bg, const uint8_t* h_payload, size_t src_pitch,
+                              int method, int tfp_window, int out_type, uint8_t* h_out,
+                              size_t out_pitch, int64_t bn) {
+    spk_geom dg = *bg;
+    dg.plane_pitch = spk_plane_pitch(bg->width, bg->height);
+    const size_t esz = out_type == SPK_OUT_U8 ? 1 : out_type == SPK_OUT_F32 ? 4 : 8;
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    cudaStream_t s;
+    SPK_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    int rc = [&]() -> int {
+        Scratch planes(s), out(s);
+        SPK_CK(planes.alloc(dg.plane_pitch * (size_t)bg->frames));
+        SPK_CK(out.alloc((size_t)bn * esz * (size_t)bg->frames));
+        int r = spk_upload_planes(&dg, h_payload, src_pitch, 0, planes.p, s);
+        if (r) return r;
+        if (out_type == SPK_OUT_U8)
+            r = spk_reconstruct_u8(&dg, planes.p, method, tfp_window, static_cast<uint8_t*>(out.p), (size_t)bn, s);
+        else if (out_type == SPK_OUT_F32)
+            r = spk_reconstruct_f32(&dg, planes.p, method, tfp_window, static_cast<float*>(out.p), (size_t)bn, s);
+        else
+            r = spk_reconstruct_f64(&dg, planes.p, method, tfp_window, static_cast<double*>(out.p), (size_t)bn, s);
+        if (r) return r;
+        SPK_CK(cudaMemcpy2DAsync(h_out, out_pitch * esz, out.p, (size_t)bn * esz, (size_t)bn * esz,
+                                 (size_t)bg->frames, cudaMemcpyDeviceToHost, s));
+        return SPK_OK;
+    }();
+    cudaError_t se = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (rc) return rc;
+    if (se != cudaSuccess) return cuda_fail(se, "cudaStreamSynchronize");
+    return SPK_OK;
+}
+
+}  // namespace
+
 int spk_reconstruct_host(const spk_geom* g, const void* h_payload, int method, int tfp_window,
                          int out_type, void* h_out, size_t out_pitch) {
     spk_geom dg = *g;
@@ -703,6 +747,68 @@ int spk_reconstruct_host(const spk_geom* g, const void* h_payload, int method, i
     cudaStreamDestroy(s);
     if (rc) return rc;
     if (se != cudaSuccess) return cuda_fail(se, "cudaStreamSynchronize");
+    return SPK_OK;
+}
+
+int spk_reconstruct_host_multi(const spk_geom* g, const void* h_payload, int method, int tfp_window,
+                               int out_type, void* h_out, size_t out_pitch, const int32_t* devices,
+                               int32_t nbands) {
+    spk_geom dg = *g;
+    dg.plane_pitch = spk_plane_pitch(g->width, g->height);
+    int rc = check_geom(&dg, true);
+    if (rc) return rc;
+    if ((rc = check_method(method, tfp_window))) return rc;
+    if (out_type < SPK_OUT_U8 || out_type > SPK_OUT_F64)
+        return fail(SPK_EINVAL, "spk_reconstruct_host_multi: bad out_type");
+    if (nbands < 1 || !devices) return fail(SPK_EINVAL, "spk_reconstruct_host_multi: no devices");
+    const int64_t npix = npix_of(g);
+    if (out_pitch < (size_t)npix) return fail(SPK_EINVAL, "spk: out_pitch must be >= W*H");
+    if (g->frames == 0) return SPK_OK;
+    if (!h_payload || !h_out) return fail(SPK_EINVAL, "spk: null host buffer");
+    int ndev = 0;
+    SPK_CK(cudaGetDeviceCount(&ndev));
+    for (int i = 0; i < nbands; ++i)
+        if (devices[i] < 0 || devices[i] >= ndev)
+            return fail(SPK_EINVAL, "spk_reconstruct_host_multi: no such device");
+    const size_t esz = out_type == SPK_OUT_U8 ? 1 : out_type == SPK_OUT_F32 ? 4 : 8;
+    // pixel bands on 128-pixel boundaries (16-byte aligned plane columns and
+    // output columns), one host thread and one device each; every band is an
+    // independent (p1-p0) x 1 volume: pixels never interact
+    const int64_t units = (npix + 127) / 128;
+    struct Band {
+        int rc = SPK_OK;
+        std::string err;
+        int64_t launches = 0;
+    };
+    std::vector<Band> res((size_t)nbands);
+    std::vector<std::thread> th;
+    for (int i = 0; i < nbands; ++i) {
+        const int64_t p0 = std::min(npix, units * i / nbands * 128);
+        const int64_t p1 = std::min(npix, units * (i + 1) / nbands * 128);
+        if (p1 <= p0) continue;
+        th.emplace_back([&, i, p0, p1]() {
+            Band& b = res[(size_t)i];
+            b.rc = [&]() -> int {
+                SPK_CK(cudaSetDevice(devices[i]));
+                spk_geom bg;
+                bg.width = (int32_t)(p1 - p0);
+                bg.height = 1;
+                bg.frames = g->frames;
+                bg.plane_pitch = 0;
+                const int64_t bn = p1 - p0;
+                return spk_reconstruct_host_band(&bg, static_cast<const uint8_t*>(h_payload) + p0 / 8,
+                                                 plane_bytes(g), method, tfp_window, out_type,
+                                                 static_cast<uint8_t*>(h_out) + p0 * esz, out_pitch, bn);
+            }();
+            if (b.rc) b.err = g_err;
+            b.launches = g_launches;
+        });
+    }
+    for (auto& t : th) t.join();
+    for (const Band& b : res) {
+        g_launches += b.launches;
+        if (b.rc) return fail(b.rc, b.err);
+    }
     return SPK_OK;
 }
 
@@ -1223,6 +1329,11 @@ int spk_last_timing(float* segment_ms, float* finalize_ms, float* expand_ms, flo
 }
 
 const char* spk_last_error(void) { return g_err.c_str(); }
+
+int spk_device_count(void) {
+    int n = 0;
+    return cudaGetDeviceCount(&n) == cudaSuccess ? n : -1;
+}
 
 int spk_version(void) { return 100; }
 

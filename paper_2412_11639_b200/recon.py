@@ -260,6 +260,27 @@ def reconstruct_host(payload: np.ndarray, width: int, height: int, frames: int, 
     return out
 
 
+def reconstruct_host_multi(payload: np.ndarray, width: int, height: int, frames: int, method="fsr",
+                           dtype=np.uint8, devices=(0,), out: np.ndarray | None = None) -> np.ndarray:
+    """reconstruct_host() over several GPUs: the pixels are cut into
+    len(devices) bands (128-pixel boundaries), band i on CUDA device
+    devices[i] (spk_reconstruct_host_multi).  Identical output for any band
+    count, as the reference's `workers` (reconstruct.hpp:70-72)."""
+    m = _method(method)
+    code = {np.dtype(np.uint8): capi.SPK_OUT_U8, np.dtype(np.float32): capi.SPK_OUT_F32,
+            np.dtype(np.float64): capi.SPK_OUT_F64}[np.dtype(dtype)]
+    npix = width * height
+    if out is None:
+        out = np.empty((frames, npix), dtype=dtype)
+    buf = np.ascontiguousarray(payload.reshape(-1))
+    devs = np.ascontiguousarray(np.asarray(devices, dtype=np.int32))
+    g = capi.geom(width, height, frames, 0)
+    capi.check(capi.lib().spk_reconstruct_host_multi(g, buf.ctypes.data, int(m.kind),
+                                                     int(m.tfp_window), code, out.ctypes.data,
+                                                     out.shape[1], devs.ctypes.data, int(devs.size)))
+    return out
+
+
 def reconstruct_host_batch(payloads, width: int, height: int, frames: int, method="fsr",
                            dtype=np.uint8, outs=None) -> list:
     """Many volumes of one geometry through spk_reconstruct_host_batch: the

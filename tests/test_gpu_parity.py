@@ -228,6 +228,32 @@ def test_host_boundary_matches_device_path():
     assert np.array_equal(f64, host2d(run(v, "ssr", torch.float64), w * h))
 
 
+@pytest.mark.parametrize("w,h", [(400, 250), (333, 7), (5, 3)])
+def test_host_multi_bands_match_single(w, h):
+    """reconstruct() with `workers` bands (spk_reconstruct_host_multi): every
+    band on its own host thread, here all on device 0 (one GPU on the test
+    box); identical to the one-call path for any band count, empty bands
+    included (more bands than 128-pixel units)."""
+    t = 700
+    v = spk.synth("moving", 8, w, h, t)
+    payload = v.payload()
+    for m in ("fsr", "ssr", "tfi", "tfp"):
+        one = spk.reconstruct_host(payload, w, h, t, m)
+        for nb in (1, 2, 3, 7):
+            got = spk.reconstruct_host_multi(payload, w, h, t, m, devices=[0] * nb)
+            assert np.array_equal(got, one), (m, nb)
+    for dtype in (np.float32, np.float64):
+        one = spk.reconstruct_host(payload, w, h, t, "ssr", dtype=dtype)
+        got = spk.reconstruct_host_multi(payload, w, h, t, "ssr", dtype=dtype, devices=[0, 0, 0])
+        assert np.array_equal(got.view(np.uint8), one.view(np.uint8)), dtype
+    with pytest.raises(ValueError):
+        spk.reconstruct_host_multi(payload, w, h, t, "fsr", devices=[spk_device_count()])
+
+
+def spk_device_count():
+    return capi.lib().spk_device_count()
+
+
 def test_launch_count_and_determinism():
     v = spk.synth("static", 1, 400, 250, 2000)
     capi.lib().spk_launch_count(1)
