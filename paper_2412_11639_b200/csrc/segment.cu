@@ -53,13 +53,13 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     if (word * 32 >= a.npix) return;  // warp-uniform
     uint32_t(*rg)[32] = reinterpret_cast<uint32_t(*)[32]>(seg_smem + (size_t)wid * kRing * 32);
     volatile int* vprog = prog;
-    // stay within kDrift groups of the block's slowest warp (L2 sector sharing)
+    // stay within the drift bound of the block's slowest warp (L2 sector sharing)
     auto throttle = [&](int front) {
         for (;;) {
             int mn = 0x7fffffff;
 #pragma unroll
             for (int i = 0; i < kSegWarps; ++i) mn = min(mn, vprog[i]);
-            if (front - mn <= kDrift) break;
+            if (front - mn <= (METHOD == kFSR ? kDriftFsr : kDriftSsr)) break;
             __nanosleep(256);
         }
     };
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         }
         produced += kBatch;
         // the drift bound is checked every other batch (the block's warps
-        // stay within kDrift + kBatch groups)
+        // stay within the bound + kBatch groups)
         if ((produced & kBatch) == 0) throttle(produced);
         load_batch();
         __syncwarp();

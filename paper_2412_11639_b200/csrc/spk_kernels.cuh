@@ -16,12 +16,16 @@ using spk_event_t = ::spk_event;
 using spk_stab_t = ::spk_stab;
 
 // K2 block = 8 warps = 256 pixels = one 32-byte sector of every plane row;
-// the warps share each sector through L2, so they are kept within kDrift
-// groups of each other (otherwise every 4-byte load pulls its own sector from
+// the warps share each sector through L2, so they are kept within a drift
+// bound (kDriftFsr / kDriftSsr groups) of each other (otherwise every 4-byte load pulls its own sector from
 // DRAM on long streams)
 constexpr int kSegThreads = 256;
 constexpr int kSegWarps = kSegThreads / 32;
-constexpr int kDrift = 96;       // max groups a warp may produce ahead of its block's slowest
+// max groups a warp may produce ahead of its block's slowest warp, per
+// method (measured: FSR 48 vs 96 -- C5 K2 -3%, C3 -2%; SSR 160 vs 96 --
+// C3 SSR K2 -1%)
+constexpr int kDriftFsr = 48;
+constexpr int kDriftSsr = 160;
 constexpr int kBatch = 8;        // 32-frame groups per prefetch batch
 constexpr int kSsrProbe = 64;    // SSR: words scanned in bulk mode before choosing the mode
 constexpr int kSsrDense = 2;     // SSR: events per lane-word above which spike mode wins
