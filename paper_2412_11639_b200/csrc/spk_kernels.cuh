@@ -33,6 +33,11 @@ constexpr int kSsrDense = 2;     // SSR: events per lane-word above which spike 
 // at 32 KB per block, which leaves L1 room for the plane sectors the block's
 // warps share (64: C3 K2 4.01 vs 3.82 ms)
 constexpr int kRing = 32;
+// A warp's own front is at most kRing + kBatch groups past its published
+// lowest group, so a smaller bound would make it wait on itself (measured:
+// a bound of 16 hangs).
+static_assert(kDriftFsr >= kRing + kBatch && kDriftSsr >= kRing + kBatch,
+              "the drift bound must exceed a warp's own ring span");
 constexpr int kCausalWarps = 2;  // warps per TFI/TFP block
 
 struct SegArgs {
