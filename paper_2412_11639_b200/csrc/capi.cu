@@ -204,7 +204,10 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     f.tblv = w.tblv.p;
     f.offs = static_cast<const uint32_t*>(w.offs.p);
     f.stream = w.stream.p;
-    const dim3 fgrid((unsigned)w.ngroups, (unsigned)((sa.nchunks + kFinWindow - 1) / kFinWindow));
+    // few groups (narrow sensors): split each group's pixels over 4 blocks
+    const unsigned fsplit = w.ngroups < 1024 ? 4u : 1u;
+    const dim3 fgrid((unsigned)w.ngroups, (unsigned)((sa.nchunks + kFinWindow - 1) / kFinWindow), fsplit);
+    if (fsplit > 1) SPK_CK(cudaMemsetAsync(w.bins.p, 0, (size_t)w.nbins * sizeof(uint32_t), s));
     k_fin_bins<GP><<<fgrid, kFinWarps * 32, 0, s>>>(f);
     SPK_LAUNCHED("k_fin_bins");
     int rc = launch_scan(f.bins, static_cast<uint32_t*>(w.offs.p), w.nbins, s);

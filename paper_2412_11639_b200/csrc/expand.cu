@@ -55,9 +55,14 @@ __global__ void __launch_bounds__(kFinWarps * 32, 2) k_fin_bins(FinArgs a) {
     const int cw0 = blockIdx.y * kFinWindow;
     const int cw1 = min(a.nchunks, cw0 + kFinWindow);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // blockIdx.z: this block's share of the group's pixels (gridDim.z > 1
+    // for sensors with few groups: more blocks in flight; the shares' counts
+    // meet in global memory, zeroed beforehand)
+    const int share = GP / (int)gridDim.z;
+    const int pl0 = (int)blockIdx.z * share, pl1 = pl0 + share;
     for (int i = threadIdx.x; i < kFinWindow * kBins; i += blockDim.x) hist[i] = 0;
     __syncthreads();
-    for (int pl = warp; pl < GP; pl += kFinWarps) {
+    for (int pl = pl0 + warp; pl < pl1; pl += kFinWarps) {
         const int64_t p = (int64_t)g * GP + pl;
         if (p >= a.npix) break;
         const int n = (int)min(a.counts[p], (uint32_t)a.cap);
@@ -82,7 +87,11 @@ __global__ void __launch_bounds__(kFinWarps * 32, 2) k_fin_bins(FinArgs a) {
     __syncthreads();
     for (int i = threadIdx.x; i < (cw1 - cw0) * kBins; i += blockDim.x) {
         const int c = cw0 + i / kBins;
-        a.bins[((int64_t)c * a.ngroups + g) * kBins + (i % kBins)] = hist[i];
+        uint32_t* b = &a.bins[((int64_t)c * a.ngroups + g) * kBins + (i % kBins)];
+        if (gridDim.z == 1)
+            *b = hist[i];
+        else if (hist[i])
+            atomicAdd(b, hist[i]);
     }
 }
 
