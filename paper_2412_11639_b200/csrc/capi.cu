@@ -147,7 +147,7 @@ int launch_segment(int method, const SegArgs& a, cudaStream_t s) {
 
 // exclusive scan of n uint32 counts into T (three small launches)
 template <typename T>
-int launch_scan(const uint32_t* in, T* out, int64_t n, cudaStream_t s) {
+int launch_scan(const uint32_t* in, T* out, int64_t n, cudaStream_t s, T* out2 = nullptr) {
     const int64_t nb = (n + kScanBlock - 1) / kScanBlock;
     Scratch sums(s);
     SPK_CK(sums.alloc((size_t)nb * sizeof(T)));
@@ -156,7 +156,7 @@ int launch_scan(const uint32_t* in, T* out, int64_t n, cudaStream_t s) {
     SPK_LAUNCHED("k_scan_blocks");
     k_scan_sums<T><<<1, kScanBlock, 0, s>>>(sp, nb);
     SPK_LAUNCHED("k_scan_sums");
-    k_scan_add<T><<<(unsigned)nb, kScanBlock, 0, s>>>(out, sp, n);
+    k_scan_add<T><<<(unsigned)nb, kScanBlock, 0, s>>>(out, sp, n, out2);
     SPK_LAUNCHED("k_scan_add");
     return SPK_OK;
 }
@@ -210,10 +210,10 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     if (fsplit > 1) SPK_CK(cudaMemsetAsync(w.bins.p, 0, (size_t)w.nbins * sizeof(uint32_t), s));
     k_fin_bins<GP><<<fgrid, kFinWarps * 32, 0, s>>>(f);
     SPK_LAUNCHED("k_fin_bins");
-    int rc = launch_scan(f.bins, static_cast<uint32_t*>(w.offs.p), w.nbins, s);
+    // the scan also writes the copy K2c claims slots from
+    int rc = launch_scan(f.bins, static_cast<uint32_t*>(w.offs.p), w.nbins, s,
+                         static_cast<uint32_t*>(w.cursor.p));
     if (rc) return rc;
-    SPK_CK(cudaMemcpyAsync(w.cursor.p, w.offs.p, (size_t)w.nbins * sizeof(uint32_t),
-                           cudaMemcpyDeviceToDevice, s));
     f.cursor = static_cast<uint32_t*>(w.cursor.p);
     const unsigned nseg = (unsigned)((sa.cap + kFinSeg - 1) / kFinSeg);
     k_fin_scatter<OUT><<<dim3((unsigned)((sa.npix + 255) / 256), nseg), 256, 0, s>>>(f);

@@ -508,18 +508,22 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_sums(T* sums, int64_t nb) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kScanBlock) k_scan_add(T* out, const T* sums, int64_t n) {
+__global__ void __launch_bounds__(kScanBlock) k_scan_add(T* out, const T* sums, int64_t n, T* out2) {
     const int64_t i = (int64_t)blockIdx.x * kScanBlock + threadIdx.x;
-    if (i < n) out[i] += sums[blockIdx.x];
+    if (i < n) {
+        const T v = out[i] + sums[blockIdx.x];
+        out[i] = v;
+        if (out2) out2[i] = v;  // a second copy (K2c's running slot cursors)
+    }
 }
 
 template __global__ void k_scan_blocks<uint32_t>(const uint32_t*, uint32_t*, uint32_t*, int64_t);
 template __global__ void k_scan_sums<uint32_t>(uint32_t*, int64_t);
-template __global__ void k_scan_add<uint32_t>(uint32_t*, const uint32_t*, int64_t);
+template __global__ void k_scan_add<uint32_t>(uint32_t*, const uint32_t*, int64_t, uint32_t*);
 template __global__ void k_scan_blocks<unsigned long long>(const uint32_t*, unsigned long long*,
                                                            unsigned long long*, int64_t);
 template __global__ void k_scan_sums<unsigned long long>(unsigned long long*, int64_t);
 template __global__ void k_scan_add<unsigned long long>(unsigned long long*, const unsigned long long*,
-                                                        int64_t);
+                                                        int64_t, unsigned long long*);
 
 }  // namespace spk

@@ -242,7 +242,7 @@ __global__ void k_scan_blocks(const uint32_t* in, T* out, T* sums, int64_t n);
 template <typename T>
 __global__ void k_scan_sums(T* sums, int64_t nb);
 template <typename T>
-__global__ void k_scan_add(T* out, const T* sums, int64_t n);
+__global__ void k_scan_add(T* out, const T* sums, int64_t n, T* out2);
 constexpr int kScanBlock = 1024;
 template <int METHOD, typename OUT>
 __global__ void k_causal(CausalArgs a);
