@@ -12,10 +12,12 @@ zero-copy view of the full planes (byte offset p0/8, same pitch, 16-B
 aligned) and its output columns stay 16-B aligned for the vector stores.
 A band is handed to the C-ABI as a (p1-p0) x 1 volume.
 
-Time sharding (needed only when one stream's planes exceed a GPU; C5's
-12.5 GB fits in 180 GB) is not exact with a halo alone -- a run's set of
-accepted intervals depends on its whole history (reconstruct.cpp:17-36) --
-and is documented in DESIGN.md, not implemented.
+Time shards (configs[4]: one long stream cut in frame ranges, one per
+rank) are below (`TimeShard`, `reconstruct_time_sharded`,
+`reconstruct_time_sharded_dist`).  A halo alone is not exact -- a run's set
+of accepted intervals depends on its whole history (reconstruct.cpp:17-36)
+-- so every shard is scanned speculatively from a fresh state and the true
+boundary state is resolved exactly (csrc/shard.cu).
 """
 from __future__ import annotations
 

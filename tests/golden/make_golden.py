@@ -147,6 +147,29 @@ def save_volume(name, bits, w, h, methods):
     print(f"vol_{name}.npz", w, h, t)
 
 
+def save_crit9():
+    """proj/tests/acceptance.cpp:231-236 (criterion 9, the benchmark floor):
+    400x250x320, static rates 0.05 + 0.9*((31x + 17y) mod 20)/19, default
+    simulate options (threshold 1, residual 0) -- 20 distinct pixel streams.
+    Stored: the planes and SHA-256 of the reference's FSR/SSR outputs (f64
+    doubles and quantised uint8 frames; the frames themselves are 32 MB)."""
+    w, h, t = 400, 250, 320
+    streams = [REF.simulate_pixel(np.full(t, 0.05 + 0.9 * c / 19.0)) for c in range(20)]
+    bits = np.zeros((t, w * h), np.uint8)
+    for y in range(h):
+        for x in range(w):
+            bits[:, y * w + x] = streams[(x * 31 + y * 17) % 20]
+    planes = pack(bits, w, h)
+    fb = planes.shape[1]
+    data = {"planes": planes, "geom": np.array([w, h, t], np.int64)}
+    for m, tag in ((0, "fsr"), (1, "ssr")):
+        f, u = REF.reconstruct(planes, fb, w, h, t, m, 32, workers=4)
+        data[f"{tag}/f64_sha256"] = np.frombuffer(hashlib.sha256(f.tobytes()).digest(), np.uint8)
+        data[f"{tag}/u8_sha256"] = np.frombuffer(hashlib.sha256(u.tobytes()).digest(), np.uint8)
+    np.savez_compressed(OUT / "vol_crit9.npz", **data)
+    print("vol_crit9.npz", w, h, t)
+
+
 def save_records():
     """SPKR images of the golden volumes from the reference's --emit-records
     loop (proj/tools/spikecam_main.cpp:146-172 -> write_spkr), plus a
@@ -223,6 +246,7 @@ def main():
     print("formats.npz")
     save_records()
     save_metrics()
+    save_crit9()
 
 
 def stab_rows(bits_list, depth):
