@@ -1,6 +1,7 @@
 // spikecam/b200.hpp -- C++ drop-in for the reconstruction surface of the
 // reference library (namespace spikecam, proj/include/spikecam/{core,
-// reconstruct,io}.hpp), implemented over the sm_100a C-ABI
+// reconstruct,io,codec,metrics}.hpp -- each of those names is also provided
+// in include/spikecam/ and includes this header), implemented over the sm_100a C-ABI
 // (include/spikecam_b200.h).  Same names, signatures, value semantics and
 // exception classes as the reference, so its callers
 // (proj/tools/spikecam_main.cpp:174,271, proj/src/metrics.cpp:71, the tests)
@@ -153,8 +154,9 @@ private:
     int width_, height_;
 };
 
-// `workers` > 1 splits the pixels into that many bands over the visible GPUs
-// (round-robin; spk_reconstruct_host_multi); the result is identical for any
+// `workers` (the reference's CPU thread count) selects up to that many of the
+// visible GPUs, one pixel band each (spk_reconstruct_host_multi); with one
+// GPU, or workers <= 1, it is one call.  The result is identical for any
 // worker count, as in the reference (reconstruct.hpp:70-72).
 std::vector<IntensityImage> reconstruct(const SpikeVolume& volume, ReconMethod method,
                                         int workers = 0);
@@ -212,6 +214,58 @@ void write_image(const IntensityImage& image, const std::filesystem::path& path,
                  ImageFormat format);
 // P5 PGM back into [0, 255] values (read_image, io.cpp:230-234, PGM branch).
 IntensityImage read_image(const std::filesystem::path& path);
+
+// SPKR container (io.hpp:44-60): "SPKR" magic, the SPK1 geometry header,
+// then per pixel (row-major) a u32 word count and that many u16 words.
+struct RecordVolume {
+    int width = 0;
+    int height = 0;
+    uint32_t fps = kDefaultFps;
+    uint32_t frame_count = 0;
+    std::vector<std::vector<uint16_t>> words;  // per pixel, row-major
+    std::vector<uint16_t>& pixel(int x, int y) { return words[static_cast<size_t>(y) * width + x]; }
+    const std::vector<uint16_t>& pixel(int x, int y) const {
+        return words[static_cast<size_t>(y) * width + x];
+    }
+};
+void write_spkr(const RecordVolume& records, const std::filesystem::path& path);
+RecordVolume read_spkr(const std::filesystem::path& path);
+
+// ---------------------------------------------------------------- codec ----
+// 16-bit records (codec.hpp:11-25): duration in the high byte, intensity
+// (rounded, ties away from zero) in the low byte; durations > 255 split into
+// full 255-frame words with the remainder last.
+inline int duration_of(uint16_t word) { return word >> 8; }
+inline int intensity_of(uint16_t word) { return word & 0xff; }
+void encode_append(std::vector<uint16_t>& words, long duration, double intensity);
+std::vector<uint16_t> encode(long duration, double intensity);
+std::vector<uint16_t> encode_events(std::span<const SegmentEvent> events);
+std::vector<uint8_t> decode(std::span<const uint16_t> words);
+
+// The CLI's --emit-records loop (spikecam_main.cpp:146-172: per pixel
+// fsr_events / segment_ssr -> encode_events) for every pixel at once on the
+// GPU (spk_records_host); method fsr or ssr, else invalid_argument.
+RecordVolume emit_records(const SpikeVolume& volume, ReconMethod method, uint32_t fps = kDefaultFps);
+
+// -------------------------------------------------------------- metrics ----
+struct MetricReport {
+    double te = 0.0;  // two-dimensional entropy, bits
+    std::optional<double> psnr;
+    std::optional<double> mse;
+    std::optional<double> throughput;  // frames / second
+};
+struct BenchResult {
+    std::string method;
+    int width = 0;
+    int height = 0;
+    int frames = 0;
+    int workers = 0;
+    int repeats = 0;
+    double frames_per_second = 0.0;  // median over repeats
+};
+// metrics.cpp:63-82: `repeats` (>= 3) timed reconstruct() calls into one
+// reused output, median frames/s -- here each call is the GPU path.
+BenchResult bench(const SpikeVolume& volume, ReconMethod method, int repeats, int workers = 1);
 
 // ------------------------------------------------ packed fast path (new) ----
 // The SPK1 payload kept bit-packed: no byte-per-bit SpikeVolume in between.

@@ -32,6 +32,9 @@ def build(ref: bool = True) -> None:
     subprocess.run(["make", "-s", "-C", str(HERE), "all"], check=True)
     if ref and REF_SRC.exists():
         subprocess.run(["make", "-s", "-C", str(HERE), "ref"], check=True)
+        # the reference's acceptance gate over the B200 path (integration/);
+        # needs libspikecam_b200.so, so __graft_entry__.build() builds it first
+        subprocess.run(["make", "-s", "-C", str(HERE), "b200"], check=True)
 
 
 def _ptr(a: np.ndarray) -> int:

@@ -8,6 +8,7 @@
 #include "spikecam/b200.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cmath>
 #include <cstring>
@@ -112,9 +113,9 @@ std::vector<uint8_t> stream_payload(const SpikeLikeStream& s) {
     return pay;  // 1 pixel -> one byte per plane, bit 0
 }
 
-// workers > 1: that many pixel bands, spread round-robin over the visible
-// CUDA devices (spk_reconstruct_host_multi); otherwise one call on the
-// current device.  The result is the same for any worker count.
+// workers > 1 with several visible CUDA devices: min(workers, devices)
+// pixel bands, one per device (spk_reconstruct_host_multi); otherwise one
+// call on the current device.  The result is the same for any worker count.
 template <typename T>
 std::vector<T> recon_host(const PackedSpikes& sp, ReconMethod m, int out_type, int workers = 1) {
     const size_t npix = static_cast<size_t>(sp.width) * sp.height;
@@ -122,12 +123,14 @@ std::vector<T> recon_host(const PackedSpikes& sp, ReconMethod m, int out_type, i
     const spk_geom g = geom(sp.width, sp.height, sp.frames);
     if (sp.payload.size() != plane_bytes(sp.width, sp.height) * sp.frames)
         throw std::invalid_argument("PackedSpikes: payload size does not match the geometry");
-    if (workers > 1) {
-        const int ndev = std::max(1, spk_device_count());
-        std::vector<int32_t> devs(static_cast<size_t>(workers));
-        for (int i = 0; i < workers; ++i) devs[static_cast<size_t>(i)] = i % ndev;
+    // one band per GPU, at most `workers` of them (narrow bands on one device
+    // would only add copies: the single call already fills the GPU)
+    const int nbands = std::min(std::max(workers, 1), std::max(1, spk_device_count()));
+    if (nbands > 1) {
+        std::vector<int32_t> devs(static_cast<size_t>(nbands));
+        for (int i = 0; i < nbands; ++i) devs[static_cast<size_t>(i)] = i;
         ck(spk_reconstruct_host_multi(&g, sp.payload.data(), static_cast<int>(m.kind), m.tfp_window,
-                                      out_type, out.data(), npix, devs.data(), workers));
+                                      out_type, out.data(), npix, devs.data(), nbands));
     } else {
         ck(spk_reconstruct_host(&g, sp.payload.data(), static_cast<int>(m.kind), m.tfp_window,
                                 out_type, out.data(), npix));
@@ -636,6 +639,136 @@ IntensityImage read_image(const std::filesystem::path& path) {
     IntensityImage img(w, h);
     std::copy(px.begin(), px.end(), img.values.begin());
     return img;
+}
+
+// ----------------------------------------------------------------- SPKR ----
+// write_spkr / read_spkr (io.cpp:240-292): same layout, checks and messages.
+void write_spkr(const RecordVolume& records, const std::filesystem::path& path) {
+    if (records.words.size() != static_cast<size_t>(records.width) * records.height)
+        throw io_error("SPKR record table does not match geometry");
+    size_t total = 16;
+    for (const auto& w : records.words) total += 4 + 2 * w.size();
+    std::vector<uint8_t> data(total);
+    std::memcpy(data.data(), "SPKR", 4);
+    put_le(data.data() + 4, static_cast<uint32_t>(records.width), 2);
+    put_le(data.data() + 6, static_cast<uint32_t>(records.height), 2);
+    put_le(data.data() + 8, records.fps, 4);
+    put_le(data.data() + 12, records.frame_count, 4);
+    size_t pos = 16;
+    for (const auto& w : records.words) {
+        put_le(data.data() + pos, static_cast<uint32_t>(w.size()), 4);
+        pos += 4;
+        for (uint16_t x : w) {
+            put_le(data.data() + pos, x, 2);
+            pos += 2;
+        }
+    }
+    write_file(path, data.data(), data.size());
+}
+
+namespace {
+
+RecordVolume parse_spkr(const uint8_t* data, size_t size, const std::string& name) {
+    if (size < 16 || std::memcmp(data, "SPKR", 4) != 0) throw io_error("bad SPKR magic in " + name);
+    RecordVolume rv;
+    rv.width = data[4] | data[5] << 8;
+    rv.height = data[6] | data[7] << 8;
+    rv.fps = le32(data + 8);
+    rv.frame_count = le32(data + 12);
+    if (rv.width < 1 || rv.height < 1) throw io_error("empty geometry in " + name);
+    const size_t pixels = static_cast<size_t>(rv.width) * rv.height;
+    rv.words.resize(pixels);
+    size_t pos = 16;
+    for (size_t p = 0; p < pixels; ++p) {
+        if (pos + 4 > size) throw io_error("truncated SPKR record table: " + name);
+        const uint32_t count = le32(data + pos);
+        pos += 4;
+        if (pos + 2ull * count > size) throw io_error("truncated SPKR records: " + name);
+        auto& w = rv.words[p];
+        w.resize(count);
+        for (uint32_t i = 0; i < count; ++i, pos += 2) w[i] = static_cast<uint16_t>(data[pos] | data[pos + 1] << 8);
+    }
+    if (pos != size) throw io_error("trailing bytes after SPKR records in " + name);
+    return rv;
+}
+
+}  // namespace
+
+RecordVolume read_spkr(const std::filesystem::path& path) {
+    const std::vector<uint8_t> data = read_file(path);
+    return parse_spkr(data.data(), data.size(), path.string());
+}
+
+RecordVolume emit_records(const SpikeVolume& volume, ReconMethod method, uint32_t fps) {
+    if (method.kind != Method::fsr && method.kind != Method::ssr)
+        throw std::invalid_argument("--emit-records needs method fsr or ssr");
+    if (volume.width() > 65535 || volume.height() > 65535)
+        throw std::invalid_argument("SPKR geometry is 16-bit: width/height must be <= 65535");
+    const PackedSpikes sp = pack(volume, fps);
+    const spk_geom g = geom(volume.width(), volume.height(), volume.frames());
+    void* img = nullptr;
+    uint64_t bytes = 0;
+    ck(spk_records_host(&g, sp.payload.data(), static_cast<int>(method.kind), fps, &img, &bytes));
+    try {
+        RecordVolume rv = parse_spkr(static_cast<const uint8_t*>(img), static_cast<size_t>(bytes), "device image");
+        spk_free_host(img);
+        return rv;
+    } catch (...) {
+        spk_free_host(img);
+        throw;
+    }
+}
+
+// ---------------------------------------------------------------- codec ----
+// encode_append / encode / encode_events / decode (codec.cpp:8-41): same
+// rules and exceptions.
+void encode_append(std::vector<uint16_t>& words, long duration, double intensity) {
+    if (duration < 1) throw std::invalid_argument("encode: duration must be >= 1");
+    if (!(intensity >= 0.0 && intensity <= 255.0)) throw std::invalid_argument("encode: intensity outside [0, 255]");
+    const uint16_t q = static_cast<uint16_t>(std::lround(intensity));
+    for (; duration > 255; duration -= 255) words.push_back(static_cast<uint16_t>(0xff00u | q));
+    words.push_back(static_cast<uint16_t>(static_cast<uint16_t>(duration) << 8 | q));
+}
+
+std::vector<uint16_t> encode(long duration, double intensity) {
+    std::vector<uint16_t> words;
+    encode_append(words, duration, intensity);
+    return words;
+}
+
+std::vector<uint16_t> encode_events(std::span<const SegmentEvent> events) {
+    std::vector<uint16_t> words;
+    for (const SegmentEvent& e : events) encode_append(words, e.duration, e.intensity);
+    return words;
+}
+
+std::vector<uint8_t> decode(std::span<const uint16_t> words) {
+    size_t n = 0;
+    for (uint16_t w : words) {
+        if (duration_of(w) == 0) throw std::runtime_error("decode: zero-duration record");
+        n += static_cast<size_t>(duration_of(w));
+    }
+    std::vector<uint8_t> frames;
+    frames.reserve(n);
+    for (uint16_t w : words) frames.insert(frames.end(), static_cast<size_t>(duration_of(w)), static_cast<uint8_t>(intensity_of(w)));
+    return frames;
+}
+
+// ---------------------------------------------------------------- bench ----
+BenchResult bench(const SpikeVolume& volume, ReconMethod method, int repeats, int workers) {
+    if (repeats < 3) throw std::invalid_argument("bench: repeats must be >= 3");
+    std::vector<double> fps(static_cast<size_t>(repeats));
+    std::vector<IntensityImage> images;  // reused across repeats, as the reference
+    for (int r = 0; r < repeats; ++r) {
+        const auto t0 = std::chrono::steady_clock::now();
+        reconstruct(volume, method, workers, images);
+        const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        fps[static_cast<size_t>(r)] = volume.frames() / std::max(s, 1e-12);
+    }
+    std::sort(fps.begin(), fps.end());
+    const size_t h = static_cast<size_t>(repeats / 2);
+    const double median = repeats % 2 ? fps[h] : 0.5 * (fps[h - 1] + fps[h]);
+    return {method.name(), volume.width(), volume.height(), volume.frames(), workers, repeats, median};
 }
 
 }  // namespace spikecam

@@ -5,6 +5,7 @@
 //   dropin_test gpucheck             self-consistency of the GPU-backed API
 //   dropin_test rows IN OUT          per-stream API on the golden streams
 //   dropin_test vol IN.spk OUTDIR    volume API on a golden SPK1 file
+//   dropin_test records IN.spk DIR   the CLI's --emit-records loop + emit_records
 //
 // `rows` / `vol` only dump results; the Python side compares them with the
 // reference's golden outputs (tests/golden/).
@@ -15,10 +16,17 @@
 #include <filesystem>
 #include <fstream>
 #include <functional>
+#include <iterator>
 #include <random>
 #include <string>
 
-#include "spikecam/b200.hpp"
+// the reference's header names (include/spikecam/*.hpp forward to b200.hpp)
+#include "spikecam/codec.hpp"
+#include "spikecam/core.hpp"
+#include "spikecam/io.hpp"
+#include "spikecam/metrics.hpp"
+#include "spikecam/reconstruct.hpp"
+#include "spikecam/b200.hpp"  // the additions: EventStream, reconstruct_u8, PackedSpikes
 
 using namespace spikecam;
 namespace fs = std::filesystem;
@@ -130,6 +138,89 @@ static void selftest(const fs::path& dir) {
     EXPECT(r.width == 4 && r.height == 2);
     EXPECT((r.values == std::vector<double>{0, 128, 127, 255, 255, 1, 0, 255}));
     EXPECT(throws<io_error>([&] { write_image(img, dir / "q.png", ImageFormat::png); }));
+
+    // codec (codec.cpp:8-41): word layout, splits past 255 frames, rounding, errors
+    EXPECT((encode(3, 127.5) == std::vector<uint16_t>{static_cast<uint16_t>(3 << 8 | 128)}));
+    const auto split = encode(600, 10.4);
+    EXPECT((split == std::vector<uint16_t>{0xff0a, 0xff0a, static_cast<uint16_t>(90 << 8 | 10)}));
+    EXPECT(duration_of(split[2]) == 90 && intensity_of(split[2]) == 10);
+    EXPECT(decode(split).size() == 600u && decode(split)[599] == 10);
+    EXPECT(throws<std::invalid_argument>([] { encode(0, 1.0); }));
+    EXPECT(throws<std::invalid_argument>([] { encode(5, 255.5); }));
+    EXPECT(throws<std::invalid_argument>([] { encode(5, -0.1); }));
+    const std::vector<uint16_t> zero{0x0005};
+    EXPECT(throws<std::runtime_error>([&] { decode(zero); }));
+    const std::vector<SegmentEvent> evs{{2, 0.4}, {300, 254.6}};
+    EXPECT((encode_events(evs) == std::vector<uint16_t>{0x0200, 0xffff, static_cast<uint16_t>(45 << 8 | 255)}));
+    // SPKR (io.cpp:240-292): round trip, geometry check, truncation / trailing bytes
+    RecordVolume rv;
+    rv.width = 2;
+    rv.height = 1;
+    rv.frame_count = 7;
+    rv.words = {{0x0701}, {0x0300, 0x0402}};
+    write_spkr(rv, dir / "r.spkr");
+    const RecordVolume back = read_spkr(dir / "r.spkr");
+    EXPECT(back.width == 2 && back.height == 1 && back.fps == kDefaultFps && back.frame_count == 7);
+    EXPECT(back.words == rv.words && back.pixel(1, 0).size() == 2u);
+    RecordVolume bad = rv;
+    bad.words.pop_back();
+    EXPECT(throws<io_error>([&] { write_spkr(bad, dir / "bad.spkr"); }));
+    {
+        std::ifstream in(dir / "r.spkr", std::ios::binary);
+        std::string bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+        std::ofstream(dir / "trunc.spkr", std::ios::binary).write(bytes.data(), (std::streamsize)bytes.size() - 1);
+        std::ofstream(dir / "trail.spkr", std::ios::binary).write((bytes + "x").data(), (std::streamsize)bytes.size() + 1);
+    }
+    EXPECT(throws<io_error>([&] { read_spkr(dir / "trunc.spkr"); }));
+    EXPECT(throws<io_error>([&] { read_spkr(dir / "trail.spkr"); }));
+    EXPECT(throws<io_error>([&] { read_spkr(dir / "q.pgm"); }));
+    EXPECT(throws<std::invalid_argument>([&] { bench(SpikeVolume(2, 2, 2), ReconMethod::parse("fsr"), 2); }));
+}
+
+// ------------------------------------------------------------- records ----
+// The CLI's --emit-records loop (spikecam_main.cpp:146-172) compiled against
+// the drop-in (per pixel: pixel_stream -> fsr_events / segment_ssr ->
+// encode_events -> write_spkr), and the whole-sensor GPU form emit_records;
+// both files are compared with the reference's SPKR bytes by test_dropin.py.
+static void records(const fs::path& spk, const fs::path& dir) {
+    const auto [volume, fps] = read_spk(spk);
+    for (const char* name : {"fsr", "ssr"}) {
+        const ReconMethod method = ReconMethod::parse(name);
+        RecordVolume rv;
+        rv.width = volume.width();
+        rv.height = volume.height();
+        rv.fps = fps;
+        rv.frame_count = static_cast<uint32_t>(volume.frames());
+        rv.words.resize(static_cast<size_t>(rv.width) * rv.height);
+        for (int y = 0; y < rv.height; ++y) {
+            for (int x = 0; x < rv.width; ++x) {
+                SpikeLikeStream stream = pixel_stream(volume, x, y);
+                std::vector<SegmentEvent> events;
+                if (method.kind == Method::fsr) {
+                    events = fsr_events(stream);
+                } else {
+                    for (const Segment& sg : segment_ssr(stream)) events.push_back({sg.duration(), sg.intensity});
+                }
+                rv.pixel(x, y) = encode_events(events);
+            }
+        }
+        write_spkr(rv, dir / (std::string(name) + "_loop.spkr"));
+        const RecordVolume gpu = emit_records(volume, method, fps);
+        write_spkr(gpu, dir / (std::string(name) + "_gpu.spkr"));
+        EXPECT(gpu.words == rv.words);
+        // decode of every pixel's words == its uint8 frames (codec.hpp:23-25)
+        const auto u8 = reconstruct_u8(volume, method);
+        bool eq = true;
+        for (int p = 0; eq && p < rv.width * rv.height; ++p) {
+            const auto d = decode(gpu.words[static_cast<size_t>(p)]);
+            eq = d.size() == static_cast<size_t>(volume.frames());
+            for (int n = 0; eq && n < volume.frames(); ++n) eq = d[static_cast<size_t>(n)] == u8[static_cast<size_t>(n)][static_cast<size_t>(p)];
+        }
+        EXPECT(eq);
+    }
+    EXPECT(throws<std::invalid_argument>([&] { emit_records(volume, ReconMethod::parse("tfi")); }));
+    const BenchResult b = bench(volume, ReconMethod::parse("ssr"), 3, 1);
+    EXPECT(b.method == "ssr" && b.repeats == 3 && b.frames == volume.frames() && b.frames_per_second > 0.0);
 }
 
 // ------------------------------------------------------------ gpucheck ----
@@ -384,9 +475,11 @@ int main(int argc, char** argv) {
             stab_rows(argv[2], argv[3], std::atoi(argv[4]));
         } else if (mode == "metrics" && argc == 4) {
             metrics(argv[2], argv[3]);
+        } else if (mode == "records" && argc == 4) {
+            records(argv[2], argv[3]);
         } else {
             std::fprintf(stderr, "usage: dropin_test selftest DIR | gpucheck | rows IN OUT | vol SPK DIR | "
-                                 "stab IN OUT DEPTH | metrics SPK DIR\n");
+                                 "stab IN OUT DEPTH | metrics SPK DIR | records SPK DIR\n");
             return 2;
         }
     } catch (const std::exception& e) {

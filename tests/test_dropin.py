@@ -191,3 +191,34 @@ def test_cpp_dropin_metrics_and_volume_stability(exe, golden_dir, tmp_path):
     assert len(rep) == w * h
     for p in range(w * h):
         assert rep[p][0] == [int(x) for x in wd[p]] and rep[p][1] == str(wp[p]), p
+
+
+def _spk_file(path, planes, w, h, t):
+    head = np.zeros(16, np.uint8)
+    head[:4] = np.frombuffer(b"SPK1", np.uint8)
+    head[4:8] = np.frombuffer(np.array([w, h], "<u2").tobytes(), np.uint8)
+    head[8:16] = np.frombuffer(np.array([20000, t], "<u4").tobytes(), np.uint8)
+    path.write_bytes(head.tobytes() + planes.tobytes())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", VOLS + ["sparse7x3"])
+def test_cpp_dropin_emit_records_match_reference(exe, golden_dir, tmp_path, name):
+    """The CLI's --emit-records loop (spikecam_main.cpp:146-172) compiled
+    against the drop-in headers, and the whole-sensor emit_records (GPU),
+    write the reference's SPKR bytes (tests/golden/records.npz); decode() of
+    every pixel equals its uint8 frames; bench() runs."""
+    rec = np.load(golden_dir / "records.npz")
+    if name == "sparse7x3":
+        planes, geom = rec["sparse7x3/planes"], rec["sparse7x3/geom"]
+    else:
+        g = np.load(golden_dir / f"vol_{name}.npz")
+        planes, geom = g["planes"], g["geom"]
+    w, h, t = (int(x) for x in geom)
+    spk = tmp_path / "v.spk"
+    _spk_file(spk, planes, w, h, t)
+    run(exe, "records", spk, tmp_path)
+    for tag in ("fsr", "ssr"):
+        want = rec[f"{name}/{tag}"].tobytes()
+        assert (tmp_path / f"{tag}_loop.spkr").read_bytes() == want, tag
+        assert (tmp_path / f"{tag}_gpu.spkr").read_bytes() == want, tag
