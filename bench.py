@@ -46,6 +46,24 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def build_sha16() -> str:
+    """SHA-256 (16 hex) of the sm_100a library this run loads."""
+    import hashlib
+    lib = ROOT / "paper_2412_11639_b200" / "libspikecam_b200.so"
+    return hashlib.sha256(lib.read_bytes()).hexdigest()[:16] if lib.exists() else "missing"
+
+
+def step_profile(lib_sha: str):
+    """Per-kernel ncu figures of one C2 step (profiles/ncu_step.json, written
+    by profiles/ncu_step_profile.py from an ncu --set full capture), only when
+    they were captured from this very build."""
+    f = ROOT / "profiles" / "ncu_step.json"
+    if not f.exists():
+        return None
+    d = json.loads(f.read_text())
+    return d if d.get("build_sha16") == lib_sha else None
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -105,12 +123,24 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU baseline --
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_fps(planes_host: np.ndarray, pitch: int, w: int, h: int, t: int, method: int,
-                      repeats: int = 3):
-    """The reference's own bench() (proj/src/metrics.cpp:63-82) on the host."""
+                      repeats: int = 3, workers: int | None = None):
+    """The reference's own bench() (proj/src/metrics.cpp:63-82) on the host:
+    median of `repeats` reconstruct() calls with `workers` OpenMP threads
+    (default: every host thread).  Returns (fps, threads used, kind)."""
     from oracle.oracle import Reference, ref_available
 
-    cores = os.cpu_count() or 1
+    cores = workers or os.cpu_count() or 1
     if ref_available():
         fps = Reference().bench_fps(planes_host, pitch, w, h, t, method, 32, repeats, cores)
         return fps, cores, "reference"
@@ -122,11 +152,49 @@ def cpu_reference_fps(planes_host: np.ndarray, pitch: int, w: int, h: int, t: in
     return repeats * t / (time.perf_counter() - t0), cores, "port"
 
 
+def cpu_baseline_block(planes_host: np.ndarray, pitch: int, method: int, source: str,
+                       long_planes: np.ndarray | None = None):
+    """cpu_baseline: the reference on the box's host cores, every thread and
+    one thread, on frames [0, CPU_SAMPLE_FRAMES) of the configs[1] stream
+    (plus a longer sample, when given, for the frames-vs-T scaling)."""
+    tcpu = planes_host.shape[0]
+    fps_all, cores, kind = cpu_reference_fps(planes_host, pitch, W, H, tcpu, method)
+    fps_one, _, _ = cpu_reference_fps(planes_host, pitch, W, H, tcpu, method, workers=1)
+    blk = {"value": fps_all, "unit": "frames/s", "cores": cores, "kind": kind,
+           "workers_1": fps_one, "cpu_model": cpu_model(),
+           "sample": f"frames [0,{tcpu}) of the configs[1] stream ({source}); the reference "
+                     f"bench(): median of 3 reconstruct() calls, {cores} OpenMP workers "
+                     f"(workers_1: one)"}
+    if long_planes is not None:
+        tl = long_planes.shape[0]
+        fps_l, _, _ = cpu_reference_fps(long_planes, pitch, W, H, tl, method)
+        blk["t_scaling"] = {f"T={tcpu}": fps_all, f"T={tl}": fps_l,
+                            "note": "reference frames/s at two sample lengths (all threads)"}
+    return blk
+
+
+def reference_stream(frames: int):
+    """Frames [0, frames) of the configs[1] stream as host SPK planes: the
+    device generator (spk_synth, the GPU arm's exact input) when a GPU is
+    present, else the host port of the same scene construction."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            import paper_2412_11639_b200 as spk
+            v = spk.synth("moving", 0, W, H, frames, device=torch.device("cuda", 0))
+            return v.planes.cpu().numpy(), v.pitch, "device generator, seed 0: the GPU arm's input"
+    except Exception:  # noqa: BLE001 -- no usable GPU: host generator below
+        pass
+    pl = moving_scene_cpu(W, H, frames, 0)
+    return pl, pl.shape[1], "host generator (no GPU visible)"
+
+
 def moving_scene_cpu(w: int, h: int, t: int, seed: int) -> np.ndarray:
-    """Host-only generator of the configs[1] moving scene for the reference arm
-    (same construction as the device generator: 16 seeded sinusoids in
-    [0.01, 0.6] translating at 0.05 px/step, an occluding bar at 0.2 px/step,
-    integrate-and-fire with threshold 1 and uniform initial residual).
+    """Host-only generator of the configs[1] moving scene (fallback for the
+    reference arm on a host without a GPU; same construction as the device
+    generator: 16 seeded sinusoids in [0.01, 0.6] translating at 0.05 px/step,
+    an occluding bar at 0.2 px/step, integrate-and-fire with threshold 1 and
+    uniform initial residual -- a different random draw).
     Returns dense SPK1 planes [t, ceil(w*h/8)]."""
     rng = np.random.default_rng(seed)
     amp = 0.3 + rng.random(16)
@@ -160,34 +228,44 @@ def moving_scene_cpu(w: int, h: int, t: int, seed: int) -> np.ndarray:
     return planes
 
 
+def bench_config(frames: int, method: str, world: int) -> dict:
+    """`config` of both arms (the driver compares them)."""
+    return {"workload": f"configs[1] moving 400x250x{frames}", "method": method,
+            "width": W, "height": H, "frames": frames,
+            "parallelism": f"streams x{world} (one independent stream per GPU)",
+            "l2": "no flush: 0.5 GB in + 4 GB out per step > 126 MB L2",
+            "vs_baseline_ref": "FPGA 20,000 FPS (BASELINE.md, PAPER.md:199)"}
+
+
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     method = {"fsr": 0, "ssr": 1}[args.method]
     tcpu = CPU_SAMPLE_FRAMES
-    planes = moving_scene_cpu(W, H, tcpu, 0)
-    pitch = planes.shape[1]
+    planes, pitch, source = reference_stream(tcpu)
     cores = os.cpu_count() or 1
     for _ in range(args.warmup):
         cpu_reference_fps(planes, pitch, W, H, tcpu, method, repeats=3)
     rates = []
+    kind = "reference"
     for _ in range(args.steps):
         fps_i, cores, kind = cpu_reference_fps(planes, pitch, W, H, tcpu, method, repeats=3)
         rates.append(fps_i)
     fps = float(np.median(rates))
+    fps_one, _, _ = cpu_reference_fps(planes, pitch, W, H, tcpu, method, repeats=3, workers=1)
     total = args.steps * tcpu / fps
-    sample = (f"configs[1] moving scene, frames [0,{tcpu}) of 400x250 (host-generated); per step "
-              f"the reference bench() (median of 3 reconstruct() calls, {cores} workers)")
+    sample = (f"configs[1] moving scene, frames [0,{tcpu}) of the 400x250x{args.frames} stream "
+              f"({source}); per step the reference bench() (median of 3 reconstruct() calls, "
+              f"{cores} OpenMP workers); workers_1 = one worker")
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": fps / FPGA_FPS, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "configs[1] moving 400x250x40000 (bounded CPU sample)",
-                   "method": args.method, "width": W, "height": H, "frames": tcpu},
+        "config": bench_config(args.frames, args.method, world),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": kind,
-                         "sample": sample},
+                         "workers_1": fps_one, "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -294,48 +372,46 @@ def main():
     fps = world * frames / (ms_step * 1e-3)
     gpxf = world * pxf / (ms_step * 1e-3) / 1e9
 
+    lib_sha = build_sha16()
+    prof = step_profile(lib_sha)
+
     def roofline(ph, ms_step, method):
-        """Dominant kernel (largest share of the step): algorithmic bytes per
-        launch / its mean CUDA-event duration.  K2 (segment) reads 0.125 B/px-frame
-        and is issue-bound (integer ALU; profiles/), K3 (expand) writes 1 B/px-frame
-        and is HBM-write-bound; both fractions are reported."""
+        """The path's HBM roofline: algorithmic bytes of one step (1.125 B per
+        px-frame: the packed input bit + the uint8 output byte)
+        over the device-timed step.  `kernels`: each phase's share of the step
+        (CUDA events on the launch stream), its own algorithmic bytes (K2
+        reads 0.125 B/px-frame, the finalize none, K3 writes 1 B/px-frame) over
+        its time, and what binds it -- from the ncu --set full capture of this
+        very build (profiles/ncu_step_<method>.json, matched by the library's
+        SHA-256; null when the capture is of another build)."""
         seg, fin, exp, fix = ph
-        k2_gbs = pxf * 0.125 / (seg * 1e-3) / 1e9
-        k3_gbs = pxf * 1.0 / (exp * 1e-3) / 1e9
-        if exp >= seg:
-            kern, achieved, dur = "k_expand", k3_gbs, exp
-        else:
-            kern, achieved, dur = "k_segment", k2_gbs, seg
-        traffic = None
-        tf = ROOT / "profiles" / f"traffic_{kern}_{method}.json"
-        if tf.exists():
-            traffic = json.loads(tf.read_text()).get("bytes_per_launch")
-        alu = None
-        af = ROOT / "profiles" / f"alu_{kern}_{method}.json"
-        if kern == "k_segment" and af.exists():
-            alu = json.loads(af.read_text())
-        return {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                "peak_kind": peak_kind, "kernel_ms": dur,
-                "kernel_note": (f"k_segment is bound by the integer ALU pipe, not HBM (ncu: ALU pipe "
-                                f"{alu['alu_pipe_frac']:.0%} of peak, FMA pipe {alu['fma_pipe_frac']:.0%}); "
-                                "its HBM fraction is low by construction" if alu else
-                                "k_segment is issue-bound (integer ALU), not HBM-bound"
-                                if kern == "k_segment" else "HBM write-bound"),
-                "alu_pipe_frac": alu["alu_pipe_frac"] if alu else None,
-                "step_frac": pxf * BYTES_PER_PXF / (ms_step * 1e-3) / 1e9 / peak,
-                "phases_ms": {"segment": seg, "finalize": fin, "expand": exp, "fixup": fix},
-                "expand_hbm_gbs": k3_gbs, "expand_hbm_frac": k3_gbs / peak}
+        step_gbs = pxf * BYTES_PER_PXF / (ms_step * 1e-3) / 1e9
+        kp = (prof or {}).get(method, {})
+
+        def kern(name, ms, alg_bytes, note):
+            k = {"name": name, "ms": ms, "share": ms / ms_step,
+                 "hbm_frac_algorithmic": (alg_bytes / (ms * 1e-3) / 1e9 / peak) if ms > 0 and alg_bytes else None,
+                 "bound": note}
+            if name in kp:
+                k["ncu"] = kp[name]
+            return k
+        kernels = [kern("k_segment", seg, pxf * 0.125, "integer ALU pipe (issue), not HBM"),
+                   kern("finalize", fin, 0.0, "latency (scattered 4-B stores)"),
+                   kern("k_expand", exp, pxf * 1.0, "HBM write"),
+                   kern("k_fixup", fix, 0.0, "-")]
+        traffic = sum(v.get("dram_bytes", 0.0) for v in kp.values()) if kp else None
+        return {"bound": "hbm", "scope": "whole step (K2 + finalize + K3 + fixup)",
+                "achieved": step_gbs, "peak": peak, "unit": "GB/s", "frac": step_gbs / peak,
+                "traffic": traffic, "algorithmic_bytes": pxf * BYTES_PER_PXF,
+                "peak_kind": peak_kind, "build_sha16": lib_sha,
+                "traffic_source": (prof or {}).get("source"), "kernels": kernels,
+                "phases_ms": {"segment": seg, "finalize": fin, "expand": exp, "fixup": fix}}
 
     line = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": fps / FPGA_FPS, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"configs[1] moving 400x250x{frames}", "method": args.method,
-                   "width": W, "height": H, "frames": frames,
-                   "parallelism": f"streams x{world} (one independent stream per GPU)",
-                   "l2": "no flush: 0.5 GB in + 4 GB out per step > 126 MB L2",
-                   "vs_baseline_ref": "FPGA 20,000 FPS (BASELINE.md, PAPER.md:199)"},
+        "config": bench_config(frames, args.method, world),
         "gpx_frames_per_s": gpxf,
         "roofline": roofline(phases, ms_step, args.method),
         "gpu_launches": int(launches),
@@ -398,12 +474,10 @@ def main():
     if rank == 0 and not args.no_cpu:
         tcpu = min(CPU_SAMPLE_FRAMES, frames)
         host = vol.planes[:tcpu].cpu().numpy()
-        fps_cpu, cores, kind = cpu_reference_fps(host, vol.pitch, W, H, tcpu,
-                                                 0 if args.method == "fsr" else 1)
-        line["cpu_baseline"] = {"value": fps_cpu, "unit": "frames/s", "cores": cores,
-                                "kind": kind,
-                                "sample": f"frames [0,{tcpu}) of the same stream, reference "
-                                          f"bench() median of 3, {cores} workers"}
+        longp = vol.planes[:min(4 * tcpu, frames)].cpu().numpy() if frames > tcpu else None
+        line["cpu_baseline"] = cpu_baseline_block(host, vol.pitch, 0 if args.method == "fsr" else 1,
+                                                  "device generator, seed 0: this arm's input",
+                                                  longp)
     if not args.no_long or not args.no_configs:
         del vol, out
         if not args.no_e2e:

@@ -117,6 +117,14 @@ void ensure_pool(int dev) {
 }
 
 
+// Test hook (tests/test_limits.py): SPK_TEST_PART_ENTRIES / SPK_TEST_GRID_Y
+// lower the 2^32 change-stream limit and the 65535 grid.y limit so the splits
+// run on small volumes.  Read once; unset in production.
+int64_t test_limit(const char* name, int64_t dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::max<int64_t>(1, std::atoll(v)) : dflt;
+}
+
 // RAII stream-ordered scratch
 struct Scratch {
     void* p = nullptr;
@@ -215,9 +223,14 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
                          static_cast<uint32_t*>(w.cursor.p));
     if (rc) return rc;
     f.cursor = static_cast<uint32_t*>(w.cursor.p);
-    const unsigned nseg = (unsigned)((sa.cap + kFinSeg - 1) / kFinSeg);
-    k_fin_scatter<OUT><<<dim3((unsigned)((sa.npix + 255) / 256), nseg), 256, 0, s>>>(f);
-    SPK_LAUNCHED("k_fin_scatter");
+    const int nseg = (sa.cap + kFinSeg - 1) / kFinSeg;
+    static const int maxy = (int)test_limit("SPK_TEST_GRID_Y", 65535);
+    for (int g0 = 0; g0 < nseg; g0 += maxy) {  // grid.y limit: caps past 4.19M runs
+        f.seg0 = g0;
+        const unsigned ny = (unsigned)std::min(maxy, nseg - g0);
+        k_fin_scatter<OUT><<<dim3((unsigned)((sa.npix + 255) / 256), ny), 256, 0, s>>>(f);
+        SPK_LAUNCHED("k_fin_scatter");
+    }
     mark(2, s);
 
     ExpArgs e;
@@ -245,6 +258,30 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
         const unsigned by = (unsigned)(std::min(per_launch, sa.nchunks - c0) * e.pieces);
         k_expand<OUT><<<dim3(bx, by), warps * 32, smem, s>>>(e);
         SPK_LAUNCHED("k_expand");
+    }
+    return SPK_OK;
+}
+
+// The change stream of one expand is indexed with 32-bit offsets (scan of
+// the bins, K2c slot claims, K3): its length, at most npix * cap, must stay
+// below 2^32.  Larger (pixels x capacity) products are expanded in pixel
+// parts, each a whole number of pixel groups with npix_part * cap < 2^32.
+template <typename OUT>
+int expand_parts(const SegArgs& sa, OUT* out, size_t out_pitch, cudaStream_t s) {
+    constexpr int64_t GP = 32 * Geo<OUT>::P;
+    static const int64_t entries = test_limit("SPK_TEST_PART_ENTRIES", (int64_t)UINT32_MAX);
+    const int64_t limit = entries / std::max(sa.cap, 1);
+    const int64_t part = std::max<int64_t>(GP, limit / GP * GP);
+    for (int64_t p0 = 0; p0 < sa.npix; p0 += part) {
+        SegArgs sub = sa;
+        sub.npix = std::min(part, sa.npix - p0);
+        sub.runs = sa.runs + p0 * sa.cap;
+        sub.counts = sa.counts + p0;
+        sub.last = sa.last + p0;
+        ExpandWork<OUT> w(s);
+        int rc = prepare_expand<OUT>(sub, w, s);
+        if (rc) return rc;
+        if ((rc = launch_expand<OUT>(sub, w, out + p0, out_pitch, s))) return rc;
     }
     return SPK_OK;
 }
@@ -332,11 +369,9 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
     // One pass: pipelining pixel parts of K2 with K3 was measured slower at
     // every size (K2 fills the SMs, so K3 of part k only runs in the gaps of
     // part k+1: C3 FSR 9.72 vs 9.34 ms, SSR 25.5 vs 24.5 ms).
-    ExpandWork<OUT> w(s);
-    if ((rc = prepare_expand<OUT>(a, w, s))) return rc;
     mark(0, s);
     if ((rc = launch_segment(method, a, s))) return rc;
-    if ((rc = launch_expand<OUT>(a, w, out, out_pitch, s))) return rc;
+    if ((rc = expand_parts<OUT>(a, out, out_pitch, s))) return rc;
     mark(3, s);
     rc = launch_fixup<OUT>(method, a, out, out_pitch, s);
     mark(4, s);
@@ -367,9 +402,7 @@ int expand_runs_impl(const spk_geom* g, const spk_run* runs, int64_t cap, const 
     a.runs = const_cast<spk_run*>(runs);
     a.counts = const_cast<uint32_t*>(counts);
     a.last = const_cast<int32_t*>(last);
-    ExpandWork<OUT> w(s);
-    if ((rc = prepare_expand<OUT>(a, w, s))) return rc;
-    return launch_expand<OUT>(a, w, out, out_pitch, s);
+    return expand_parts<OUT>(a, out, out_pitch, s);
 }
 
 }  // namespace

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(256) k_fin_scatter(FinArgs a) {
     // here -- a value needs only the next run's start -- so a pixel's list is
     // spread over several threads: enough loads and atomics in flight even
     // for sensors with few pixels)
-    const int kb = (int)blockIdx.y * kFinSeg;
+    const int kb = (a.seg0 + (int)blockIdx.y) * kFinSeg;
     if (kb >= n) return;
     const int ke = min(n, kb + kFinSeg);
     const spk_run_t* rp = a.runs + p * a.cap;

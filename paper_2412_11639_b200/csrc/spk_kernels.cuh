@@ -149,6 +149,7 @@ struct FinArgs {
     const uint32_t* offs;  // exclusive prefix of bins
     uint32_t* cursor;      // K2c: running copy of offs (claimed with atomics)
     void* stream;          // Change<OUT>[total] (K2c)
+    int seg0 = 0;          // K2c: first run segment of this launch (blockIdx.y offset)
 };
 constexpr int kFinSeg = 64;       // K2c: runs per thread (a pixel's list spans cap / kFinSeg threads)
 constexpr int kFinWarps = 16;     // K2b/K2c: warps per block (block = one pixel group)

@@ -81,8 +81,13 @@ def gather_bands(local: torch.Tensor, npix: int, group=None) -> torch.Tensor:
     if world == 1:
         return local[:, :npix].contiguous()
     t, bmax = local.shape
-    flat = torch.empty((world * t, bmax), dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(flat, local.contiguous(), group=group)
+    if _staged(group) and local.is_cuda:  # gloo: through the host
+        flat_h = torch.empty((world * t, bmax), dtype=local.dtype)
+        dist.all_gather_into_tensor(flat_h, local.contiguous().cpu(), group=group)
+        flat = flat_h.to(local.device)
+    else:
+        flat = torch.empty((world * t, bmax), dtype=local.dtype, device=local.device)
+        dist.all_gather_into_tensor(flat, local.contiguous(), group=group)
     stacked = flat.view(world, t, bmax)
     full = torch.empty((t, npix), dtype=local.dtype, device=local.device)
     for r, (p0, p1) in enumerate(bands):
@@ -122,10 +127,18 @@ def _ptr(t):
 
 class TimeShard:
     """Frames [f0, f1) of a volume: speculative scan, then resolve / junction /
-    stitch / expand through the C-ABI (all asynchronous on `stream`)."""
+    stitch / expand through the C-ABI -- all asynchronous on `stream` (every
+    torch allocation and reduction below runs on that stream too).
+
+    Fast pass (robust=False): no host synchronisation.  The speculative run
+    lists get a fixed capacity and the resolve no fallback re-scan; either
+    overflowing (noise-like pixels) only sets the device flag `overflow`, and
+    the driver re-runs the protocol robustly when any shard's flag is set --
+    one host check after the whole pass.  Robust pass: capacities grown and
+    fallback scans taken as needed (host checks between the launches)."""
 
     def __init__(self, volume: PackedVolume, f0: int, f1: int, method, prefix_cap: int = 64,
-                 stream=None):
+                 stream=None, robust: bool = False):
         from .recon import _method, _stream
         from . import _capi as capi
         self.capi, self.lib = capi, capi.lib()
@@ -140,21 +153,26 @@ class TimeShard:
         self.dev = volume.planes.device
         self.planes = volume.planes[f0:f1]
         self.stream = _stream(stream)
+        self.ts = (torch.cuda.ExternalStream(self.stream, device=self.dev) if self.stream
+                   else torch.cuda.current_stream(self.dev))
+        self.robust = robust
         self.pcap = int(prefix_cap)
         self.g = capi.geom(volume.width, volume.height, self.frames, volume.pitch)
         i32 = dict(dtype=torch.int32, device=self.dev)
-        self.prefix = torch.empty((self.npix, self.pcap, 2), **i32)
-        self.sync = torch.empty((self.npix, SYNC_DT), **i32)
-        self.tstate = torch.empty((STATE_FIELDS, self.npix), **i32)
-        self.exit_state = torch.empty((STATE_FIELDS, self.npix), **i32)
-        self.entry_close = torch.empty((self.npix, CLOSE_DT), **i32)
-        self.tail_close = torch.empty((self.npix, CLOSE_DT), **i32)
+        with torch.cuda.stream(self.ts):
+            self.prefix = torch.empty((self.npix, self.pcap, 2), **i32)
+            self.sync = torch.empty((self.npix, SYNC_DT), **i32)
+            self.tstate = torch.empty((STATE_FIELDS, self.npix), **i32)
+            self.exit_state = torch.empty((STATE_FIELDS, self.npix), **i32)
+            self.entry_close = torch.empty((self.npix, CLOSE_DT), **i32)
+            self.tail_close = torch.empty((self.npix, CLOSE_DT), **i32)
+            self.overflow = torch.zeros((), dtype=torch.bool, device=self.dev)
         self.fb = self.fb_counts = self.fb_state = None
 
     def _segment(self, state_in):
-        """runs of this shard from `state_in` (None = fresh), capacity grown
-        until no pixel overflows"""
-        cap = max(64, self.frames // 64)  # grown below if any pixel needs more
+        """runs of this shard from `state_in` (None = fresh); robust: the
+        capacity grows until no pixel overflows, else overflow is flagged"""
+        cap = max(64, self.frames // 64)
         i32 = dict(dtype=torch.int32, device=self.dev)
         while True:
             runs = torch.empty((self.npix, cap, 2), **i32)
@@ -164,13 +182,18 @@ class TimeShard:
             self.capi.check(self.lib.spk_segment_state(
                 self.g, _ptr(self.planes) if self.frames else None, self.kind, _ptr(runs), cap,
                 _ptr(counts), _ptr(last), _ptr(state_in), _ptr(state), self.stream))
+            if not self.robust:
+                if self.npix:
+                    self.overflow |= counts.max() > cap
+                return runs, counts, last, state, cap
             need = int(counts.max().item()) if self.npix else 0
             if need <= cap:
                 return runs, counts, last, state, cap
             cap = need
 
     def speculate(self):
-        self.spec, self.spec_counts, _, self.spec_state, self.scap = self._segment(None)
+        with torch.cuda.stream(self.ts):
+            self.spec, self.spec_counts, _, self.spec_state, self.scap = self._segment(None)
 
     def fresh_entry(self) -> torch.Tensor:
         """entry state of the first shard (start of the stream)"""
@@ -178,12 +201,19 @@ class TimeShard:
 
     def resolve(self, entry: torch.Tensor):
         """true entry state -> sync records, exit state, entry / tail closes"""
+        with torch.cuda.stream(self.ts):
+            return self._resolve(entry)
+
+    def _resolve(self, entry):
         self.entry = entry
         self.capi.check(self.lib.spk_shard_resolve(
             self.g, _ptr(self.planes) if self.frames else None, self.kind, _ptr(entry),
             _ptr(self.spec), self.scap, _ptr(self.spec_counts), _ptr(self.spec_state),
             _ptr(self.prefix), self.pcap, _ptr(self.sync), _ptr(self.tstate), self.stream))
-        if bool((self.sync[:, 3] == -1).any().item()):  # a prefix overflowed: full re-scan
+        if not self.robust:
+            if self.npix:
+                self.overflow |= (self.sync[:, 3] == -1).any()  # a prefix overflowed
+        elif bool((self.sync[:, 3] == -1).any().item()):  # a prefix overflowed: full re-scan
             self.fb, self.fb_counts, _, self.fb_state, fbcap = self._segment(entry)
             if fbcap != self.scap:  # keep one capacity for both lists
                 pad = torch.empty((self.npix, max(fbcap, self.scap), 2), dtype=torch.int32,
@@ -203,7 +233,8 @@ class TimeShard:
         return self.exit_state
 
     def close_from_next(self, entry_close_next, close_next):
-        close = torch.empty((self.npix, CLOSE_DT), dtype=torch.int32, device=self.dev)
+        with torch.cuda.stream(self.ts):
+            close = torch.empty((self.npix, CLOSE_DT), dtype=torch.int32, device=self.dev)
         self.capi.check(self.lib.spk_shard_close_chain(
             self.npix, _ptr(entry_close_next), _ptr(close_next), self.frames, _ptr(close),
             self.stream))
@@ -212,9 +243,10 @@ class TimeShard:
     def stitch(self, close: torch.Tensor):
         rcap = self.scap + self.pcap + 1
         i32 = dict(dtype=torch.int32, device=self.dev)
-        self.region = torch.empty((self.npix, rcap, 2), **i32)
-        self.region_counts = torch.empty((self.npix,), **i32)
-        self.region_last = torch.empty((self.npix,), **i32)
+        with torch.cuda.stream(self.ts):
+            self.region = torch.empty((self.npix, rcap, 2), **i32)
+            self.region_counts = torch.empty((self.npix,), **i32)
+            self.region_last = torch.empty((self.npix,), **i32)
         self.rcap = rcap
         self.capi.check(self.lib.spk_shard_stitch(
             self.g, self.kind, _ptr(self.entry), _ptr(self.sync), _ptr(self.prefix), self.pcap,
@@ -253,29 +285,57 @@ def reconstruct_time_sharded(volume: PackedVolume, method="fsr", nshards: int = 
                              bounds: list[int] | None = None, dtype: torch.dtype = torch.uint8,
                              prefix_cap: int = 64, out: torch.Tensor | None = None, stream=None):
     """reconstruct() of one volume cut into time shards processed independently
-    (one GPU, all shards in this process); bit-identical to reconstruct()."""
+    (one GPU, all shards in this process); bit-identical to reconstruct().
+    The fast pass issues every launch without a host synchronisation; one
+    check at the end decides whether the robust pass must redo it."""
     bounds = bounds or time_bounds(volume.frames, nshards)
     if bounds[0] != 0 or bounds[-1] != volume.frames or any(b1 <= b0 for b0, b1 in zip(bounds, bounds[1:])):
         raise ValueError("bounds must increase strictly from 0 to the frame count")
     if out is None:
         out = torch.empty((volume.frames, volume.npix), dtype=dtype, device=volume.planes.device)
     with torch.cuda.device(volume.planes.device):
-        shards = [TimeShard(volume, b0, b1, method, prefix_cap, stream)
-                  for b0, b1 in zip(bounds, bounds[1:])]
-        for sh in shards:                      # independent: the speculative scans
-            sh.speculate()
-        entry = fresh_state(volume.npix, volume.planes.device, stream)
-        for sh in shards:                      # forward: true entry states
-            entry = sh.resolve(entry)
-        close = shards[-1].tail_close          # backward: closes of crossing runs
-        closes = [None] * len(shards)
-        closes[-1] = close
-        for r in range(len(shards) - 2, -1, -1):
-            closes[r] = shards[r].close_from_next(shards[r + 1].entry_close, closes[r + 1])
-        for sh, c in zip(shards, closes):      # independent: stitch + frames
-            sh.stitch(c)
-            sh.expand(out[sh.f0:sh.f1])
+        shards = _time_sharded_pass(volume, method, bounds, prefix_cap, out, stream, robust=False)
+        if bool(torch.stack([sh.overflow for sh in shards]).any().item()):
+            _time_sharded_pass(volume, method, bounds, prefix_cap, out, stream, robust=True)
     return out.view(volume.frames, volume.height, volume.width)
+
+
+def _time_sharded_pass(volume, method, bounds, prefix_cap, out, stream, robust):
+    shards = [TimeShard(volume, b0, b1, method, prefix_cap, stream, robust)
+              for b0, b1 in zip(bounds, bounds[1:])]
+    for sh in shards:                      # independent: the speculative scans
+        sh.speculate()
+    entry = fresh_state(volume.npix, volume.planes.device, stream)
+    for sh in shards:                      # forward: true entry states
+        entry = sh.resolve(entry)
+    closes = [None] * len(shards)          # backward: closes of crossing runs
+    closes[-1] = shards[-1].tail_close
+    for r in range(len(shards) - 2, -1, -1):
+        closes[r] = shards[r].close_from_next(shards[r + 1].entry_close, closes[r + 1])
+    for sh, c in zip(shards, closes):      # independent: stitch + frames
+        sh.stitch(c)
+        sh.expand(out[sh.f0:sh.f1])
+    return shards
+
+
+def _staged(group):
+    """gloo moves host tensors: device tensors are staged through the host"""
+    return dist.get_backend(group) == "gloo"
+
+
+def _send(t: torch.Tensor, dst: int, group):
+    if _staged(group) and t.is_cuda:
+        t = t.cpu()
+    dist.send(t, dst=dst, group=group)
+
+
+def _recv(t: torch.Tensor, src: int, group):
+    if _staged(group) and t.is_cuda:
+        h = torch.empty(t.shape, dtype=t.dtype)
+        dist.recv(h, src=src, group=group)
+        t.copy_(h)
+    else:
+        dist.recv(t, src=src, group=group)
 
 
 def reconstruct_time_sharded_dist(shard: PackedVolume, method="fsr", group=None,
@@ -288,33 +348,63 @@ def reconstruct_time_sharded_dist(shard: PackedVolume, method="fsr", group=None,
 
     Data path: none; the only exchange is O(W*H) per boundary -- the true
     automaton state forward (rank r -> r+1, 68 B/px) and the close records of
-    boundary-crossing runs backward (rank r+1 -> r, 2 x 32 B/px)."""
+    boundary-crossing runs backward (rank r+1 -> r, 2 x 32 B/px).  NCCL moves
+    device tensors; gloo (several ranks sharing one GPU, tests) stages them
+    through the host.  The fast pass has no host synchronisation of its own;
+    one all-reduce of the ranks' overflow flags at the end decides whether
+    the robust pass must redo it."""
     rank, world = _group_info(group)
-    peer = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
     if out is None:
         out = torch.empty((shard.frames, shard.npix), dtype=dtype, device=shard.planes.device)
-    sh = shard_type(shard, 0, shard.frames, method, prefix_cap, stream)
+    sh = _time_shard_dist_pass(shard, method, group, prefix_cap, out, stream, shard_type, False)
+    flag = getattr(sh, "overflow", None)
+    if flag is not None and world > 1:
+        f = flag.to(torch.int32).reshape(1)
+        if _staged(group):
+            f = f.cpu()
+        dist.all_reduce(f, op=dist.ReduceOp.MAX, group=group)
+        flag = f
+    if flag is not None and bool(flag.any().item()):
+        _time_shard_dist_pass(shard, method, group, prefix_cap, out, stream, shard_type, True)
+    return out
+
+
+def _time_shard_dist_pass(shard, method, group, prefix_cap, out, stream, shard_type, robust):
+    rank, world = _group_info(group)
+    peer = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
+    if shard_type is TimeShard:
+        sh = TimeShard(shard, 0, shard.frames, method, prefix_cap, stream, robust)
+    else:
+        sh = shard_type(shard, 0, shard.frames, method, prefix_cap, stream)
+    ts = getattr(sh, "ts", None)
+    if ts is None:  # (test doubles without a device stream)
+        return _time_shard_dist_steps(sh, shard, group, rank, world, peer, out)
+    with torch.cuda.stream(ts):  # the collectives order against the shard's stream
+        return _time_shard_dist_steps(sh, shard, group, rank, world, peer, out)
+
+
+def _time_shard_dist_steps(sh, shard, group, rank, world, peer, out):
+    dev = shard.planes.device
     sh.speculate()                              # independent on every rank
     if rank == 0:
         entry = sh.fresh_entry()
     else:                                       # forward: true entry state
-        entry = torch.empty((STATE_FIELDS, shard.npix), dtype=torch.int32,
-                            device=shard.planes.device)
-        dist.recv(entry, src=peer(rank - 1), group=group)
+        entry = torch.empty((STATE_FIELDS, shard.npix), dtype=torch.int32, device=dev)
+        _recv(entry, peer(rank - 1), group)
     exit_state = sh.resolve(entry)
     if rank + 1 < world:
-        dist.send(exit_state, dst=peer(rank + 1), group=group)
+        _send(exit_state, peer(rank + 1), group)
     if rank + 1 == world:                       # backward: closes of crossing runs
         close = sh.tail_close
     else:
-        ec_next = torch.empty((shard.npix, CLOSE_DT), dtype=torch.int32, device=shard.planes.device)
+        ec_next = torch.empty((shard.npix, CLOSE_DT), dtype=torch.int32, device=dev)
         close_next = torch.empty_like(ec_next)
-        dist.recv(ec_next, src=peer(rank + 1), group=group)
-        dist.recv(close_next, src=peer(rank + 1), group=group)
+        _recv(ec_next, peer(rank + 1), group)
+        _recv(close_next, peer(rank + 1), group)
         close = sh.close_from_next(ec_next, close_next)
     if rank > 0:
-        dist.send(sh.entry_close, dst=peer(rank - 1), group=group)
-        dist.send(close, dst=peer(rank - 1), group=group)
+        _send(sh.entry_close, peer(rank - 1), group)
+        _send(close, peer(rank - 1), group)
     sh.stitch(close)                            # independent: stitch + frames
     sh.expand(out)
-    return out
+    return sh
