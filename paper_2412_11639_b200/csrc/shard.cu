@@ -178,8 +178,12 @@ __device__ void true_end(const ShardArgs& a, int64_t p, const spk_sync_t& sy, Sc
         }
     } else if (sy.npre == -2) {
         X.restore(a.tstate, a.npix, p);
-    } else {
+    } else if (a.fbstate != nullptr) {
         X.restore(a.fbstate, a.npix, p);
+    } else {
+        // prefix overflow in a fast pass without the re-scan: flagged on the
+        // host side (the pass is redone robustly); any in-bounds state will do
+        X.restore(a.sstate, a.npix, p);
     }
 }
 
@@ -223,9 +227,12 @@ struct TrueList {
             npre = T.nrun;
             has_extra = T.lo < kLim;
             extra = spk_run_t{(uint32_t)T.rs, (uint32_t)T.cnt};
-        } else {
+        } else if (a.fb != nullptr) {
             tail = a.fb + p * a.scap;
             ntail = (int)min(a.fbcount[p], (uint32_t)a.scap);
+        } else {  // fast pass without the re-scan (redone robustly): in-bounds stand-in
+            tail = a.spec + p * a.scap;
+            ntail = (int)min(a.scount[p], (uint32_t)a.scap);
         }
     }
     __device__ int count() const { return npre + (sy.npre == -2 ? (int)has_extra : ntail - j); }

@@ -194,11 +194,18 @@ def reconstruct(volume: PackedVolume, method="fsr", workers: int = 0,
     reference's quantize(), io.cpp:78-81), or float32 / float64 values
     (float64 is bit-identical to the reference doubles).  `out` may be a
     caller-owned [T, >=H*W] buffer (reused, like the reference's `out`).
-    `workers` is accepted for signature parity; a single call runs on one GPU
-    (multi-GPU sharding lives in paper_2412_11639_b200.shard).
+    `workers` -- the reference's CPU thread count -- selects up to that many
+    of the visible GPUs, one pixel band each (shard.reconstruct_devices); with
+    one GPU, or workers <= 1, it is one call.  The result is identical for
+    any worker count (reconstruct.hpp:70-72).  Multi-process sharding lives in
+    paper_2412_11639_b200.shard.
     """
-    del workers
     m = _method(method)
+    workers = int(workers)
+    nbands = min(max(workers, 1), torch.cuda.device_count()) if volume.frames else 1
+    if nbands > 1 and stream is None:
+        from .shard import reconstruct_devices
+        return reconstruct_devices(volume, m, list(range(nbands)), out=out, dtype=dtype)
     if out is not None:
         dtype = out.dtype
     if dtype not in _OUT:

@@ -110,6 +110,34 @@ def reconstruct_sharded(volume: PackedVolume, method="fsr", group=None,
     return full.view(volume.frames, volume.height, volume.width)
 
 
+def reconstruct_devices(volume: PackedVolume, method, devices: list[int],
+                        out: torch.Tensor | None = None, dtype: torch.dtype = torch.uint8):
+    """One process, several GPUs (the `workers` of reconstruct()): pixel band
+    i is copied to devices[i], reconstructed there on its own stream and its
+    columns copied back into `out` on the volume's device."""
+    home = volume.planes.device
+    npix, t = volume.npix, volume.frames
+    if out is None:
+        out = torch.empty((t, npix), dtype=dtype, device=home)
+    bands = pixel_bands(npix, len(devices))
+    pending = []
+    for (p0, p1), d in zip(bands, devices):
+        if p1 <= p0:
+            continue
+        dev = torch.device("cuda", d)
+        s = torch.cuda.Stream(dev)
+        with torch.cuda.device(dev), torch.cuda.stream(s):
+            view = band_view(volume, p0, p1)
+            bv = PackedVolume(view.width, 1, t, view.planes.to(dev, non_blocking=True))
+            frames = reconstruct(bv, method, out=torch.empty((t, p1 - p0), dtype=out.dtype, device=dev),
+                                 stream=s)
+        pending.append((p0, p1, frames.reshape(t, p1 - p0), s))
+    for p0, p1, frames, s in pending:
+        s.synchronize()
+        out[:, p0:p1].copy_(frames.to(home))
+    return out.view(t, volume.height, volume.width) if out.shape[1] == npix else out
+
+
 # ------------------------------------------------------------ time shards --
 # One long stream cut in frame ranges (BASELINE configs[4]): exact, see
 # csrc/shard.cu and DESIGN.md "Time sharding".  `TimeShard` holds one shard's
