@@ -297,6 +297,11 @@ const char* spk_last_error(void);
 /* number of visible CUDA devices (the C++ drop-in spreads `workers` bands
  * over them); -1 when the CUDA runtime reports an error */
 int spk_device_count(void);
+/* Workspaces come from the current device's default stream-ordered pool,
+ * which keeps freed blocks cached for the next call (no host sync per
+ * call).  This waits for the device and returns the cached blocks to the
+ * driver -- e.g. before other processes share the GPU. */
+int spk_release_memory(void);
 int spk_version(void);
 
 /* ---- quality metrics and the stability check ------- */

@@ -41,6 +41,7 @@ SIGNATURES = {
     "spk_upload_planes": (C.c_int, [_G, _P, C.c_size_t, C.c_int, _P, _P]),
     "spk_reconstruct_host": (C.c_int, [_G, _P, C.c_int, C.c_int, C.c_int, _P, C.c_size_t]),
     "spk_device_count": (C.c_int, []),
+    "spk_release_memory": (C.c_int, []),
     "spk_reconstruct_host_multi": (C.c_int, [_G, _P, C.c_int, C.c_int, C.c_int, _P, C.c_size_t, _P,
                                              C.c_int32]),
     "spk_segment_host": (C.c_int, [_G, _P, C.c_int, _P, C.c_int64, _P, _P]),

@@ -1371,6 +1371,16 @@ int spk_device_count(void) {
     return cudaGetDeviceCount(&n) == cudaSuccess ? n : -1;
 }
 
+int spk_release_memory(void) {
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    SPK_CK(cudaDeviceSynchronize());
+    cudaMemPool_t pool;
+    SPK_CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+    SPK_CK(cudaMemPoolTrimTo(pool, 0));
+    return SPK_OK;
+}
+
 int spk_version(void) { return 100; }
 
 // ---- quality metrics and the stability check (metrics.cu) ----

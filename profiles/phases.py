@@ -6,8 +6,13 @@ import sys
 import torch
 
 sys.path.insert(0, ".")
-import paper_2412_11639_b200 as spk  # noqa: E402
+import os  # noqa: E402
+from pathlib import Path  # noqa: E402
+
 from paper_2412_11639_b200 import _capi as capi  # noqa: E402
+if os.environ.get("SPK_PROBE_LIB"):  # A/B probes: another build of the library
+    capi.LIB_PATH = Path(os.environ["SPK_PROBE_LIB"]).resolve()
+import paper_2412_11639_b200 as spk  # noqa: E402
 
 scene, W, H, T = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
 methods = sys.argv[5].split(",") if len(sys.argv) > 5 else ["fsr", "ssr"]

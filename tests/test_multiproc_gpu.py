@@ -53,6 +53,11 @@ def _time_worker(rank, world, port, scene, w, h, t, method, q):
 
 
 def _spawn(target, world, args):
+    # the ranks share cuda:0 with this process: hand back what earlier tests
+    # left cached (torch's allocator and the library's stream-ordered pool)
+    from paper_2412_11639_b200 import _capi as capi
+    torch.cuda.empty_cache()
+    capi.check(capi.lib().spk_release_memory())
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
