@@ -151,6 +151,14 @@ int spk_segment_state(const spk_geom* g, const void* d_planes, int method, spk_r
  * close of boundary-crossing runs back; spk_shard_stitch writes each shard's
  * true run list, which spk_expand_runs_* turns into that shard's frames.
  * g->frames is the shard length throughout; state layout as spk_segment_state. */
+/* Every shard's speculative scan in ONE launch: shard r = frames
+ * [r*shard_frames, min(frames, (r+1)*shard_frames)) scanned from a fresh
+ * state, exactly as spk_segment_state(shard r's geometry, ..., NULL, ...)
+ * would; shard r writes d_runs + r*W*H*run_cap, d_counts / d_last + r*W*H and
+ * (if d_state_out) d_state_out + r*17*W*H.  shard_frames: a multiple of 32. */
+int spk_segment_shards(const spk_geom* g, const void* d_planes, int method, int64_t shard_frames,
+                       spk_run* d_runs, int64_t run_cap, uint32_t* d_counts, int32_t* d_last,
+                       int32_t* d_state_out, void* stream);
 /* the automaton state at the start of a stream (entry of the first shard) */
 int spk_state_fresh(int64_t npix, int32_t* d_state, void* stream);
 int spk_shard_resolve(const spk_geom* g, const void* d_planes, int method, const int32_t* d_entry,
@@ -293,6 +301,10 @@ int64_t spk_launch_count(int reset);
  * milliseconds (negative if a phase did not run). */
 int spk_set_timing(int enable);
 int spk_last_timing(float* segment_ms, float* finalize_ms, float* expand_ms, float* fixup_ms);
+/* The last timed FSR/SSR call's in-grid time split: the number of time shards
+ * its scan ran as (1: none) and the pixels whose shards could not be stitched
+ * from the one-launch resolve and were re-scanned whole. */
+int spk_last_split(int32_t* shards, int64_t* flagged);
 const char* spk_last_error(void);
 /* number of visible CUDA devices (the C++ drop-in spreads `workers` bands
  * over them); -1 when the CUDA runtime reports an error */

@@ -35,6 +35,7 @@ SIGNATURES = {
     "spk_reconstruct_u8": (C.c_int, [_G, _P, C.c_int, C.c_int, _P, C.c_size_t, _P]),
     "spk_reconstruct_f32": (C.c_int, [_G, _P, C.c_int, C.c_int, _P, C.c_size_t, _P]),
     "spk_reconstruct_f64": (C.c_int, [_G, _P, C.c_int, C.c_int, _P, C.c_size_t, _P]),
+    "spk_segment_shards": (C.c_int, [_G, _P, C.c_int, C.c_int64, _P, C.c_int64, _P, _P, _P, _P]),
     "spk_segment": (C.c_int, [_G, _P, C.c_int, _P, C.c_int64, _P, _P, _P]),
     "spk_pack_bytes": (C.c_int, [_G, _P, _P, _P]),
     "spk_unpack_planes": (C.c_int, [_G, _P, _P, _P]),
@@ -74,6 +75,7 @@ SIGNATURES = {
     "spk_plane_pitch": (C.c_size_t, [C.c_int32, C.c_int32]),
     "spk_launch_count": (C.c_int64, [C.c_int]),
     "spk_set_timing": (C.c_int, [C.c_int]),
+    "spk_last_split": (C.c_int, [_P, _P]),
     "spk_last_timing": (C.c_int, [_P, _P, _P, _P]),
     "spk_last_error": (C.c_char_p, []),
     "spk_version": (C.c_int, []),

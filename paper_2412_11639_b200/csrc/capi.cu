@@ -30,6 +30,10 @@ thread_local int64_t g_launches = 0;
 thread_local bool g_timing = false;
 thread_local cudaEvent_t g_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 thread_local int g_ev_used = 0;  // events recorded by the last call
+// in-grid time split of the last timed call: shards and flagged pixels
+// (copied into pinned memory behind the call; valid once its events are done)
+thread_local int g_split_shards = 1;
+thread_local uint32_t* g_split_flagged = nullptr;
 
 // phase marker k (0..4) on stream s when timing is enabled: 0 before K2,
 // 1 after K2, 2 after K2b/scan/K2c, 3 after K3, 4 after the fixup
@@ -144,7 +148,8 @@ int launch_segment(int method, const SegArgs& a, cudaStream_t s) {
     const size_t smem = (size_t)kSegWarps * kRing * 32 * sizeof(uint32_t);  // the warps' rings
     auto go = [&](auto kern) -> int {
         SPK_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<blocks, kSegThreads, smem, s>>>(a);
+        const unsigned shards = a.shard_frames > 0 ? (unsigned)((a.frames + a.shard_frames - 1) / a.shard_frames) : 1u;
+        kern<<<dim3(blocks, shards), kSegThreads, smem, s>>>(a);
         return SPK_OK;
     };
     int rc = method == SPK_FSR ? go(k_segment<kFSR>) : go(k_segment<kSSR>);
@@ -212,11 +217,16 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     f.tblv = w.tblv.p;
     f.offs = static_cast<const uint32_t*>(w.offs.p);
     f.stream = w.stream.p;
+    f.seg = sa.seg_in;
+    f.nseg = sa.nseg;
     // few groups (narrow sensors): split each group's pixels over 4 blocks
     const unsigned fsplit = w.ngroups < 1024 ? 4u : 1u;
     const dim3 fgrid((unsigned)w.ngroups, (unsigned)((sa.nchunks + kFinWindow - 1) / kFinWindow), fsplit);
     if (fsplit > 1) SPK_CK(cudaMemsetAsync(w.bins.p, 0, (size_t)w.nbins * sizeof(uint32_t), s));
-    k_fin_bins<GP><<<fgrid, kFinWarps * 32, 0, s>>>(f);
+    if (f.seg)
+        k_fin_bins<GP, true><<<fgrid, kFinWarps * 32, 0, s>>>(f);
+    else
+        k_fin_bins<GP, false><<<fgrid, kFinWarps * 32, 0, s>>>(f);
     SPK_LAUNCHED("k_fin_bins");
     // the scan also writes the copy K2c claims slots from
     int rc = launch_scan(f.bins, static_cast<uint32_t*>(w.offs.p), w.nbins, s,
@@ -228,7 +238,11 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     for (int g0 = 0; g0 < nseg; g0 += maxy) {  // grid.y limit: caps past 4.19M runs
         f.seg0 = g0;
         const unsigned ny = (unsigned)std::min(maxy, nseg - g0);
-        k_fin_scatter<OUT><<<dim3((unsigned)((sa.npix + 255) / 256), ny), 256, 0, s>>>(f);
+        const dim3 grid((unsigned)((sa.npix + 255) / 256), ny);
+        if (f.seg)
+            k_fin_scatter<OUT, true><<<grid, 256, 0, s>>>(f);
+        else
+            k_fin_scatter<OUT, false><<<grid, 256, 0, s>>>(f);
         SPK_LAUNCHED("k_fin_scatter");
     }
     mark(2, s);
@@ -278,6 +292,7 @@ int expand_parts(const SegArgs& sa, OUT* out, size_t out_pitch, cudaStream_t s) 
         sub.runs = sa.runs + p0 * sa.cap;
         sub.counts = sa.counts + p0;
         sub.last = sa.last + p0;
+        if (sa.seg_in) sub.seg_in = sa.seg_in + p0 * 2 * sa.nseg;
         ExpandWork<OUT> w(s);
         int rc = prepare_expand<OUT>(sub, w, s);
         if (rc) return rc;
@@ -327,6 +342,187 @@ int launch_causal(const spk_geom* g, const void* planes, int method, int window,
     return method == SPK_TFI ? go(k_causal<kTFI, OUT>) : go(k_causal<kTFP, OUT>);
 }
 
+// ------------------------------------------------------ in-grid time split --
+// K2 is one wave of 8-warp blocks (a block = 256 pixels = one 32-B sector of
+// every plane row) when the sensor has few pixels: 400x250 is 391 blocks on
+// 148 SMs x 3, so some SMs hold three blocks and others two, and each warp's
+// serial chain spans the whole stream.  Cutting the stream in S time shards
+// scanned in ONE launch (S x more blocks, each 1/S as long) balances the SMs;
+// the exact stitching (csrc/shard.cu) runs as one resolve launch and one
+// combine pass.  Measured (K2 alone, profiles/shard_k2_probe.py): C2 0.966 ->
+// 0.844 ms at S = 4, configs[4] 11.26 -> 9.26 ms at S = 16.
+int split_shards(int method, int64_t npix, int64_t frames, int dev) {
+    // test hook: SPK_SPLIT=S forces S shards (1 = off), read on every call
+    const char* fv = std::getenv("SPK_SPLIT");
+    if (fv && *fv) {
+        const int64_t S = std::min<int64_t>(std::min<int64_t>(std::atoll(fv), (frames + 31) / 32),
+                                            kSplitMaxShards);
+        return S >= 2 ? (int)S : 1;
+    }
+    // FSR only: SSR's resolves sync late and cost more than the balance
+    // gains (C2 SSR K2 5.54 vs 5.36 ms).  Long streams only: the resolve,
+    // the combine and the segmented finalize cost ~0.16 ms at 400x250, about
+    // what the balance saves on a 40,000-frame K2 (C2: 2.11 vs 2.07 ms) and
+    // far less than on a 1,000,000-frame one (configs[4]: 24.2 vs 26.0 ms).
+    if (method != SPK_FSR || frames < kSplitMinStream) return 1;
+    int sms = 148, per_sm = 3;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = (size_t)kSegWarps * kRing * 32 * sizeof(uint32_t);
+    if (method == SPK_FSR)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_segment<kFSR>, kSegThreads, smem);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_segment<kSSR>, kSegThreads, smem);
+    const int64_t blocks = (npix + kSegThreads - 1) / kSegThreads;
+    const int64_t slots = (int64_t)sms * std::max(per_sm, 1);
+    int64_t S = 6 * slots / std::max<int64_t>(blocks, 1);  // ~6 waves
+    S = std::min<int64_t>(S, frames / kSplitMinFrames);
+    S = std::min<int64_t>(S, kSplitMaxShards);
+    return S >= 2 ? (int)S : 1;
+}
+
+template <typename OUT>
+int reconstruct_split(const spk_geom* g, const void* planes, int method, int S, OUT* out,
+                      size_t out_pitch, cudaStream_t s) {
+    const int64_t npix = npix_of(g);
+    const int frames = (int)g->frames;
+    const int words = (frames + 31) / 32;
+    const int sf = (words + S - 1) / S * 32;
+    S = (frames + sf - 1) / sf;
+    const int scap = std::max(64, sf / 32);
+    const int64_t rstride = kSplitGap + scap;
+    const int64_t row = (int64_t)S * rstride;
+    if (row > INT_MAX) return fail(SPK_EINVAL, "spk: run list too long");
+    constexpr int F = Scan<kSSR>::kFields;
+    Scratch rows(s), scount(s), slast(s), sstate(s), prefix(s), sync(s), syncj(s), tstate(s), seg(s),
+        counts(s), last(s), flags(s), nflag(s);
+    SPK_CK(rows.alloc((size_t)npix * row * sizeof(spk_run_t)));
+    SPK_CK(scount.alloc((size_t)S * npix * sizeof(uint32_t)));
+    SPK_CK(slast.alloc((size_t)S * npix * sizeof(int32_t)));
+    SPK_CK(sstate.alloc((size_t)S * F * npix * sizeof(int32_t)));
+    SPK_CK(prefix.alloc((size_t)S * npix * kSplitGap * sizeof(spk_run_t)));
+    SPK_CK(sync.alloc((size_t)S * npix * sizeof(spk_sync_t)));
+    SPK_CK(syncj.alloc((size_t)S * npix * sizeof(int32_t)));
+    SPK_CK(tstate.alloc((size_t)S * F * npix * sizeof(int32_t)));
+    SPK_CK(seg.alloc((size_t)npix * S * 2 * sizeof(uint32_t)));
+    SPK_CK(counts.alloc((size_t)npix * sizeof(uint32_t)));
+    SPK_CK(last.alloc((size_t)npix * sizeof(int32_t)));
+    SPK_CK(flags.alloc((size_t)npix));
+    SPK_CK(nflag.alloc(sizeof(uint32_t)));
+    SPK_CK(cudaMemsetAsync(nflag.p, 0, sizeof(uint32_t), s));
+
+    mark(0, s);
+    // 1. every shard's speculative scan, one launch
+    SegArgs a;
+    a.planes = planes;
+    a.pitch = g->plane_pitch;
+    a.npix = npix;
+    a.frames = frames;
+    a.cap = scap;
+    a.nchunks = (frames + kChunk - 1) / kChunk;
+    a.runs = static_cast<spk_run_t*>(rows.p);
+    a.counts = static_cast<uint32_t*>(scount.p);
+    a.last = static_cast<int32_t*>(slast.p);
+    a.state_out = static_cast<int32_t*>(sstate.p);
+    a.shard_frames = sf;
+    a.run_pix_stride = row;
+    a.run_shard_stride = rstride;
+    a.run_base = kSplitGap;
+    a.abs_frames = 1;
+    int rc = launch_segment(method, a, s);
+    if (rc) return rc;
+    // 2. every boundary's resolve, one launch (shard r from shard r-1's
+    //    speculative end state)
+    ShardArgs h{};
+    h.planes = planes;
+    h.pitch = g->plane_pitch;
+    h.npix = npix;
+    h.frames = sf;
+    h.prefix = static_cast<spk_run_t*>(prefix.p);
+    h.pcap = kSplitGap;
+    h.sync = static_cast<spk_sync_t*>(sync.p);
+    h.tstate = static_cast<int32_t*>(tstate.p);
+    h.spec = static_cast<spk_run_t*>(rows.p);
+    h.scap = scap;
+    h.scount = static_cast<uint32_t*>(scount.p);
+    h.sstate = static_cast<int32_t*>(sstate.p);
+    h.grid_sf = sf;
+    h.nshards = S;
+    h.rstride = rstride;
+    h.total_frames = frames;
+    h.syncj = static_cast<int32_t*>(syncj.p);
+    {
+        const int64_t threads = (npix + 31) / 32 * 32;
+        const dim3 grid((unsigned)((threads + 63) / 64), (unsigned)(S - 1));
+        if (method == SPK_FSR)
+            k_resolve<kFSR><<<grid, 64, 0, s>>>(h);
+        else
+            k_resolve<kSSR><<<grid, 64, 0, s>>>(h);
+        SPK_LAUNCHED("k_resolve");
+    }
+    // 3. the true run list per pixel as segments of its row
+    SplitArgs c;
+    c.npix = npix;
+    c.nshards = S;
+    c.sf = sf;
+    c.frames = frames;
+    c.rstride = rstride;
+    c.scap = scap;
+    c.pcap = kSplitGap;
+    c.runs = static_cast<spk_run_t*>(rows.p);
+    c.scount = static_cast<uint32_t*>(scount.p);
+    c.sstate = static_cast<int32_t*>(sstate.p);
+    c.prefix = static_cast<spk_run_t*>(prefix.p);
+    c.sync = static_cast<spk_sync_t*>(sync.p);
+    c.syncj = static_cast<const int32_t*>(syncj.p);
+    c.tstate = static_cast<int32_t*>(tstate.p);
+    c.seg = static_cast<uint32_t*>(seg.p);
+    c.counts = static_cast<uint32_t*>(counts.p);
+    c.last = static_cast<int32_t*>(last.p);
+    c.flags = static_cast<uint8_t*>(flags.p);
+    c.nflag = static_cast<uint32_t*>(nflag.p);
+    c.method = method;
+    {
+        const unsigned blocks = (unsigned)((npix + 127) / 128);
+        if (method == SPK_FSR)
+            k_split_combine<kFSR><<<blocks, 128, 0, s>>>(c);
+        else
+            k_split_combine<kSSR><<<blocks, 128, 0, s>>>(c);
+        SPK_LAUNCHED("k_split_combine");
+    }
+    // 4. flagged pixels (an entry that decides differently, a capacity
+    //    overflow): whole-stream re-scan into their rows; warps without a
+    //    flagged pixel exit at once
+    SegArgs r;
+    r.planes = planes;
+    r.pitch = g->plane_pitch;
+    r.npix = npix;
+    r.frames = frames;
+    r.cap = (int)row;
+    r.nchunks = a.nchunks;
+    r.runs = static_cast<spk_run_t*>(rows.p);
+    r.counts = static_cast<uint32_t*>(counts.p);
+    r.last = static_cast<int32_t*>(last.p);
+    r.flags = static_cast<uint8_t*>(flags.p);
+    r.seg_out = static_cast<uint32_t*>(seg.p);
+    r.nseg = S;
+    if ((rc = launch_segment(method, r, s))) return rc;
+    if (g_timing) {
+        if (!g_split_flagged) SPK_CK(cudaMallocHost(&g_split_flagged, sizeof(uint32_t)));
+        SPK_CK(cudaMemcpyAsync(g_split_flagged, nflag.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        g_split_shards = S;
+    }
+    // 5. frames from the segmented lists; overflowed pixels by k_fixup
+    SegArgs e = r;
+    e.flags = nullptr;
+    e.seg_out = nullptr;
+    e.seg_in = static_cast<const uint32_t*>(seg.p);
+    if ((rc = expand_parts<OUT>(e, out, out_pitch, s))) return rc;
+    mark(3, s);
+    rc = launch_fixup<OUT>(method, e, out, out_pitch, s);
+    mark(4, s);
+    return rc;
+}
+
 template <typename OUT>
 int reconstruct_impl(const spk_geom* g, const void* planes, int method, int window, OUT* out,
                      size_t out_pitch, void* stream) {
@@ -339,6 +535,7 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
     if (out_pitch < (size_t)npix) return fail(SPK_EINVAL, "spk: out_pitch must be >= W*H");
     cudaStream_t s = as_stream(stream);
     g_ev_used = 0;
+    g_split_shards = 1;
     if (method == SPK_TFI || method == SPK_TFP) {
         mark(0, s);
         mark(1, s);
@@ -351,6 +548,10 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
     int dev = 0;
     SPK_CK(cudaGetDevice(&dev));
     ensure_pool(dev);
+    if (g_run_cap.load() <= 0) {  // (a fixed run capacity is a test setting: one pass)
+        const int S = split_shards(method, npix, g->frames, dev);
+        if (S > 1) return reconstruct_split<OUT>(g, planes, method, S, out, out_pitch, s);
+    }
     SegArgs a;
     a.planes = planes;
     a.pitch = g->plane_pitch;
@@ -497,6 +698,38 @@ int spk_segment_state(const spk_geom* g, const void* d_planes, int method, spk_r
     a.last = d_last;
     a.state_in = d_state_in;
     a.state_out = d_state_out;
+    return launch_segment(method, a, as_stream(stream));
+}
+
+int spk_segment_shards(const spk_geom* g, const void* d_planes, int method, int64_t shard_frames,
+                       spk_run* d_runs, int64_t run_cap, uint32_t* d_counts, int32_t* d_last,
+                       int32_t* d_state_out, void* stream) {
+    int rc = check_geom(g, true);
+    if (rc) return rc;
+    if (method != SPK_FSR && method != SPK_SSR)
+        return fail(SPK_EINVAL, "spk_segment_shards: method must be fsr or ssr");
+    if (run_cap < 1 || run_cap > INT_MAX) return fail(SPK_EINVAL, "spk_segment_shards: bad run_cap");
+    if (shard_frames < 32 || shard_frames % 32 != 0 || shard_frames > INT_MAX)
+        return fail(SPK_EINVAL, "spk_segment_shards: shard_frames must be a positive multiple of 32");
+    if (g->frames == 0) return SPK_OK;
+    if (!d_planes || !d_runs || !d_counts || !d_last) return fail(SPK_EINVAL, "spk: null device buffer");
+    const int64_t shards = (g->frames + shard_frames - 1) / shard_frames;
+    if (shards > 65535) return fail(SPK_EINVAL, "spk_segment_shards: more than 65535 shards");
+    int dev = 0;
+    SPK_CK(cudaGetDevice(&dev));
+    ensure_pool(dev);
+    SegArgs a;
+    a.planes = d_planes;
+    a.pitch = g->plane_pitch;
+    a.npix = npix_of(g);
+    a.frames = (int)g->frames;
+    a.cap = (int)run_cap;
+    a.nchunks = 0;
+    a.runs = d_runs;
+    a.counts = d_counts;
+    a.last = d_last;
+    a.state_out = d_state_out;
+    a.shard_frames = (int)shard_frames;
     return launch_segment(method, a, as_stream(stream));
 }
 
@@ -1347,6 +1580,14 @@ int64_t spk_launch_count(int reset) {
 
 int spk_set_timing(int enable) {
     g_timing = enable != 0;
+    return SPK_OK;
+}
+
+int spk_last_split(int32_t* shards, int64_t* flagged) {
+    if (g_ev_used < 2) return fail(SPK_EINVAL, "spk_last_split: no timed call");
+    SPK_CK(cudaEventSynchronize(g_ev[g_ev_used - 1]));
+    if (shards) *shards = g_split_shards;
+    if (flagged) *flagged = g_split_shards > 1 && g_split_flagged ? (int64_t)*g_split_flagged : 0;
     return SPK_OK;
 }
 

@@ -48,7 +48,7 @@ __device__ __forceinline__ void st_v4(char* p, uint4 v) {
 // shared memory, so no global atomics.
 
 // K2b: run starts per (chunk, group, sub-tile)
-template <int GP>
+template <int GP, bool SPLIT>
 __global__ void __launch_bounds__(kFinWarps * 32, 2) k_fin_bins(FinArgs a) {
     __shared__ uint32_t hist[kFinWindow * kBins];
     const int g = blockIdx.x;
@@ -62,26 +62,63 @@ __global__ void __launch_bounds__(kFinWarps * 32, 2) k_fin_bins(FinArgs a) {
     const int pl0 = (int)blockIdx.z * share, pl1 = pl0 + share;
     for (int i = threadIdx.x; i < kFinWindow * kBins; i += blockDim.x) hist[i] = 0;
     __syncthreads();
+    auto bin_start = [&](uint32_t sv) {
+        const int st = (int)sv;
+        const int c = st >> kChunkLog2;
+        if (sv != 0xffffffffu && c >= cw0 && c < cw1)
+            atomicAdd(&hist[(c - cw0) * kBins + ((st & (kChunk - 1)) / kSub)], 1u);
+    };
     for (int pl = pl0 + warp; pl < pl1; pl += kFinWarps) {
         const int64_t p = (int64_t)g * GP + pl;
         if (p >= a.npix) break;
-        const int n = (int)min(a.counts[p], (uint32_t)a.cap);
         const spk_run_t* rp = a.runs + p * a.cap;
-        for (int b = 0; b < n; b += 128) {
+        const int n = (int)min(a.counts[p], (uint32_t)a.cap);
+        if constexpr (!SPLIT) {  // one contiguous list: 128 runs per pass
+            for (int b = 0; b < n; b += 128) {
+                uint32_t sv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = b + 32 * u + lane;
+                    // a run started before frame 0 (time shards) changes the value at frame 0
+                    sv[u] = k < n ? (uint32_t)max((int)rp[k].start, 0) : 0xffffffffu;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) bin_start(sv[u]);
+            }
+            continue;
+        } else {
+        // in-grid time split: the row's segments, 32-slot blocks of them four
+        // per pass; lane r holds segment r (begin, end, first block index)
+        const uint32_t* sg = a.seg + p * a.nseg * 2;
+        int sb = 0, se = 0, nb = 0;
+        if (lane < a.nseg) {
+            sb = (int)__ldg(sg + 2 * lane);
+            se = (int)__ldg(sg + 2 * lane + 1);
+            nb = (se - sb + 31) >> 5;
+        }
+        int inc = nb;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(kFull, inc, d);
+            if (lane >= d) inc += y;
+        }
+        const int bs = inc - nb;  // first block of segment `lane`
+        const int blocks = __shfl_sync(kFull, inc, 31);
+        for (int q0 = 0; q0 < blocks; q0 += 4) {
             uint32_t sv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int k = b + 32 * u + lane;
-                // a run started before frame 0 (time shards) changes the value at frame 0
-                sv[u] = k < n ? (uint32_t)max((int)rp[k].start, 0) : 0xffffffffu;
+                const int q = q0 + u;  // warp-uniform block index
+                // the last non-empty segment starting at or before block q
+                const uint32_t m = __ballot_sync(kFull, (lane < a.nseg) & (bs <= q) & (nb > 0));
+                const int rr = m ? 31 - __clz(m) : 0;
+                const int k = __shfl_sync(kFull, sb, rr) + 32 * (q - __shfl_sync(kFull, bs, rr)) + lane;
+                const int e = __shfl_sync(kFull, se, rr);
+                sv[u] = (q < blocks) & (k < e) ? (uint32_t)max((int)rp[k].start, 0) : 0xffffffffu;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int st = (int)sv[u];
-                const int c = st >> kChunkLog2;
-                if (sv[u] != 0xffffffffu && c >= cw0 && c < cw1)
-                    atomicAdd(&hist[(c - cw0) * kBins + ((st & (kChunk - 1)) / kSub)], 1u);
-            }
+            for (int u = 0; u < 4; ++u) bin_start(sv[u]);
+        }
         }
     }
     __syncthreads();
@@ -95,8 +132,26 @@ __global__ void __launch_bounds__(kFinWarps * 32, 2) k_fin_bins(FinArgs a) {
     }
 }
 
-template __global__ void k_fin_bins<512>(FinArgs);
-template __global__ void k_fin_bins<256>(FinArgs);
+template __global__ void k_fin_bins<512, false>(FinArgs);
+template __global__ void k_fin_bins<256, false>(FinArgs);
+template __global__ void k_fin_bins<512, true>(FinArgs);
+template __global__ void k_fin_bins<256, true>(FinArgs);
+
+template <typename OUT>
+__device__ __forceinline__ Change<OUT> make_change(uint32_t fo, uint32_t pl, OUT val) {
+    Change<OUT> ch;
+    if constexpr (sizeof(OUT) == 1) {
+        ch.w = fo << 17 | pl << 8 | (uint32_t)val;
+    } else if constexpr (sizeof(OUT) == 4) {
+        ch.key = fo << 16 | pl;
+        ch.bits = __float_as_uint(val);
+    } else {
+        ch.key = fo << 16 | pl;
+        ch.pad = 0;
+        ch.v = val;
+    }
+    return ch;
+}
 
 // K2c: the change stream and the value at every chunk start.  Thread = one
 // pixel, free-running (no block synchronisation): runs are read 8 at a time
@@ -104,7 +159,7 @@ template __global__ void k_fin_bins<256>(FinArgs);
 // their stream slots are claimed with 8 independent atomics on a copy of the
 // scanned histogram, then the 8 changes are stored -- one memory round trip
 // per 8 runs.
-template <typename OUT>
+template <typename OUT, bool SPLIT>
 __global__ void __launch_bounds__(256) k_fin_scatter(FinArgs a) {
     constexpr int GP = 32 * Geo<OUT>::P;
     constexpr int B = 8;
@@ -114,12 +169,13 @@ __global__ void __launch_bounds__(256) k_fin_scatter(FinArgs a) {
     const uint32_t pl = (uint32_t)(p % GP);
     const uint32_t cnt = a.counts[p];
     const bool over = cnt > (uint32_t)a.cap;  // k_fixup rewrites it: values don't matter
-    const int n = (int)min(cnt, (uint32_t)a.cap);
-    // blockIdx.y: this thread's segment of kFinSeg runs (runs are independent
-    // here -- a value needs only the next run's start -- so a pixel's list is
-    // spread over several threads: enough loads and atomics in flight even
-    // for sensors with few pixels)
+    // blockIdx.y: this thread's block of kFinSeg list slots (runs are
+    // independent here -- a value needs only the next run's start -- so a
+    // pixel's list is spread over several threads: enough loads and atomics
+    // in flight even for sensors with few pixels)
+    // (split lists: the same numbering over the row's segments in order)
     const int kb = (a.seg0 + (int)blockIdx.y) * kFinSeg;
+    const int n = (int)min(cnt, (uint32_t)a.cap);
     if (kb >= n) return;
     const int ke = min(n, kb + kFinSeg);
     const spk_run_t* rp = a.runs + p * a.cap;
@@ -127,52 +183,109 @@ __global__ void __launch_bounds__(256) k_fin_scatter(FinArgs a) {
     Change<OUT>* stp = reinterpret_cast<Change<OUT>*>(a.stream);
     OUT* tb = reinterpret_cast<OUT*>(a.tblv);
     const int64_t total_frames = (int64_t)a.nchunks << kChunkLog2;
-    for (int k0 = kb; k0 < ke; k0 += B) {
-        spk_run_t r[B + 1];
+    // the runs of [b, e) (slots of one list segment), `nxt` = the start of the
+    // run after e (the next segment's first run, or the last spike when the
+    // segment ends the list: `fin`)
+    auto range = [&](int b, int e, uint32_t nxt, bool fin) {
+        for (int k0 = b; k0 < e; k0 += B) {
+            spk_run_t r[B + 1];
 #pragma unroll
-        for (int j = 0; j <= B; ++j)
-            r[j] = k0 + j < n ? rp[k0 + j] : spk_run_t{k0 + j == n ? lastp : 0x7fffffffu, 0u};
-        uint32_t pos[B];
+            for (int j = 0; j <= B; ++j)
+                r[j] = k0 + j < e ? rp[k0 + j] : spk_run_t{k0 + j == e ? nxt : 0x7fffffffu, 0u};
+            uint32_t pos[B];
 #pragma unroll
-        for (int j = 0; j < B; ++j) {
-            if (k0 + j < ke) {
-                const int st = max((int)r[j].start, 0);  // see K2b: starts before frame 0
-                const int c = st >> kChunkLog2;
-                const int bi = (st & (kChunk - 1)) / kSub;
-                pos[j] = atomicAdd(&a.cursor[((int64_t)c * a.ngroups + g) * kBins + bi], 1u);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < B; ++j) {
-            if (k0 + j < ke) {
-                const int st = max((int)r[j].start, 0);
-                const uint32_t fo = (uint32_t)(st & (kChunk - 1));
-                const OUT val = over ? OUT(0) : OutVal<OUT>::run(r[j].intervals, r[j + 1].start - r[j].start);
-                Change<OUT> ch;
-                if constexpr (sizeof(OUT) == 1) {
-                    ch.w = fo << 17 | pl << 8 | (uint32_t)val;
-                } else if constexpr (sizeof(OUT) == 4) {
-                    ch.key = fo << 16 | pl;
-                    ch.bits = __float_as_uint(val);
-                } else {
-                    ch.key = fo << 16 | pl;
-                    ch.pad = 0;
-                    ch.v = val;
+            for (int j = 0; j < B; ++j) {
+                if (k0 + j < e) {
+                    const int st = max((int)r[j].start, 0);  // see K2b: starts before frame 0
+                    const int c = st >> kChunkLog2;
+                    const int bi = (st & (kChunk - 1)) / kSub;
+                    pos[j] = atomicAdd(&a.cursor[((int64_t)c * a.ngroups + g) * kBins + bi], 1u);
                 }
-                stp[pos[j]] = ch;
-                if (!over) {  // chunk starts in [start, next start); the last run covers the tail
-                    const int64_t hi = k0 + j + 1 < n ? (int64_t)(int)r[j + 1].start : total_frames;
-                    for (int64_t cc = ((int64_t)st + kChunk - 1) >> kChunkLog2; cc <= (hi - 1) >> kChunkLog2; ++cc)
-                        tb[cc * a.npix + p] = val;
+            }
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                if (k0 + j < e) {
+                    const int st = max((int)r[j].start, 0);
+                    const uint32_t fo = (uint32_t)(st & (kChunk - 1));
+                    const OUT val = over ? OUT(0) : OutVal<OUT>::run(r[j].intervals, r[j + 1].start - r[j].start);
+                    stp[pos[j]] = make_change<OUT>(fo, pl, val);
+                    if (!over) {  // chunk starts in [start, next start); the last run covers the tail
+                        const int64_t hi = (fin & (k0 + j + 1 == e)) ? total_frames : (int64_t)(int)r[j + 1].start;
+                        for (int64_t cc = ((int64_t)st + kChunk - 1) >> kChunkLog2; cc <= (hi - 1) >> kChunkLog2; ++cc)
+                            tb[cc * a.npix + p] = val;
+                    }
                 }
             }
         }
+    };
+    if constexpr (!SPLIT) {  // one contiguous list
+        for (int k0 = kb; k0 < ke; k0 += B) {
+            spk_run_t r[B + 1];
+#pragma unroll
+            for (int j = 0; j <= B; ++j)
+                r[j] = k0 + j < n ? rp[k0 + j] : spk_run_t{k0 + j == n ? lastp : 0x7fffffffu, 0u};
+            uint32_t pos[B];
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                if (k0 + j < ke) {
+                    const int st = max((int)r[j].start, 0);  // see K2b: starts before frame 0
+                    const int c = st >> kChunkLog2;
+                    const int bi = (st & (kChunk - 1)) / kSub;
+                    pos[j] = atomicAdd(&a.cursor[((int64_t)c * a.ngroups + g) * kBins + bi], 1u);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                if (k0 + j < ke) {
+                    const int st = max((int)r[j].start, 0);
+                    const uint32_t fo = (uint32_t)(st & (kChunk - 1));
+                    const OUT val = over ? OUT(0) : OutVal<OUT>::run(r[j].intervals, r[j + 1].start - r[j].start);
+                    stp[pos[j]] = make_change<OUT>(fo, pl, val);
+                    if (!over) {  // chunk starts in [start, next start); the last run covers the tail
+                        const int64_t hi = k0 + j + 1 < n ? (int64_t)(int)r[j + 1].start : total_frames;
+                        for (int64_t cc = ((int64_t)st + kChunk - 1) >> kChunkLog2; cc <= (hi - 1) >> kChunkLog2; ++cc)
+                            tb[cc * a.npix + p] = val;
+                    }
+                }
+            }
+        }
+        return;
+    }
+    // in-grid time split: list entries [kb, ke) over the row's segments
+    const uint32_t* sg = a.seg + p * a.nseg * 2;
+    int vo = 0;  // list index of segment r's first run
+    for (int r = 0; r < a.nseg && vo < ke; ++r) {
+        const int b = (int)__ldg(sg + 2 * r), e = (int)__ldg(sg + 2 * r + 1);
+        const int len = e - b;
+        if (vo + len > kb) {
+            const int lo = b + max(kb - vo, 0), hi = b + min(ke - vo, len);
+            uint32_t nxt = lastp;
+            bool fin = true;
+            if (hi < e) {
+                nxt = rp[hi].start;
+                fin = false;
+            } else {
+                for (int q = r + 1; q < a.nseg; ++q) {
+                    const int qb = (int)__ldg(sg + 2 * q);
+                    if ((int)__ldg(sg + 2 * q + 1) > qb) {
+                        nxt = rp[qb].start;
+                        fin = false;
+                        break;
+                    }
+                }
+            }
+            range(lo, hi, nxt, fin);
+        }
+        vo += len;
     }
 }
 
-template __global__ void k_fin_scatter<uint8_t>(FinArgs);
-template __global__ void k_fin_scatter<float>(FinArgs);
-template __global__ void k_fin_scatter<double>(FinArgs);
+template __global__ void k_fin_scatter<uint8_t, false>(FinArgs);
+template __global__ void k_fin_scatter<float, false>(FinArgs);
+template __global__ void k_fin_scatter<double, false>(FinArgs);
+template __global__ void k_fin_scatter<uint8_t, true>(FinArgs);
+template __global__ void k_fin_scatter<float, true>(FinArgs);
+template __global__ void k_fin_scatter<double, true>(FinArgs);
 
 // -------------------------------------------------------------- K3 expand --
 // Per-warp shared memory: for each frame of the sub-tile and each lane, the

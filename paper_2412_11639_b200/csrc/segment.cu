@@ -45,12 +45,13 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int64_t word = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (threadIdx.x < kSegWarps) {
-        const int64_t w = (int64_t)blockIdx.x * kSegWarps + threadIdx.x;
-        prog[threadIdx.x] = w * 32 < a.npix ? 0 : 0x7fffffff;  // warps without pixels never hold others back
-    }
+    const int64_t p = word * 32 + lane;
+    // re-scan mode (a.flags): only flagged pixels are scanned and stored
+    const bool valid = p < a.npix && (a.flags == nullptr || a.flags[p] != 0);
+    const bool busy = __any_sync(kFull, valid);
+    if (lane == 0) prog[wid] = busy ? 0 : 0x7fffffff;  // idle warps never hold others back
     __syncthreads();
-    if (word * 32 >= a.npix) return;  // warp-uniform
+    if (!busy) return;  // warp-uniform
     uint32_t(*rg)[32] = reinterpret_cast<uint32_t(*)[32]>(seg_smem + (size_t)wid * kRing * 32);
     volatile int* vprog = prog;
     // stay within the drift bound of the block's slowest warp (L2 sector sharing)
@@ -63,16 +64,20 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
             __nanosleep(256);
         }
     };
-    const int64_t p = word * 32 + lane;
-    const bool valid = p < a.npix;
-    const int frames = a.frames;
+    const size_t pitch = a.pitch;
+    // time shard of this block (a.shard_frames > 0: blockIdx.y = shard)
+    const int sf0 = a.shard_frames > 0 ? (int)blockIdx.y * a.shard_frames : 0;
+    const int frames = a.shard_frames > 0 ? min(a.shard_frames, a.frames - sf0) : a.frames;
+    const int64_t sh = blockIdx.y;  // 0 unless sharded
     const int ngroups = (frames + 31) >> 5;
     // lane i loads frame 32g + (31 - i): after the transpose bit 31 is the
     // group's first frame, so spikes come out in time order with clz
-    const char* col = reinterpret_cast<const char*>(a.planes) + word * 4;
-    const size_t pitch = a.pitch;
+    const char* col = reinterpret_cast<const char*>(a.planes) + (size_t)sf0 * pitch + word * 4;
     const int rev = 31 - lane;
-    spk_run_t* rp = a.runs + (valid ? p * a.cap : 0);
+    const int64_t pstride = a.run_pix_stride > 0 ? a.run_pix_stride : a.cap;
+    const int64_t sstride = a.run_shard_stride >= 0 ? a.run_shard_stride : a.npix * a.cap;
+    spk_run_t* rp = a.runs + sh * sstride + (valid ? p * pstride : 0) + a.run_base;
+    const int fbase = a.abs_frames ? sf0 : 0;  // stored run starts: shard or stream frames
     const int capm1 = a.cap - 1;
 
     Scan<METHOD> sc;
@@ -90,7 +95,7 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     // address arithmetic per emit); past the capacity nothing is stored
     spk_run_t* wp = rp;
     auto emit = [&](bool e, int rs, int cnt) {
-        o_rs = e ? rs : o_rs;
+        o_rs = e ? rs + fbase : o_rs;
         o_cnt = e ? cnt : o_cnt;
         st_run_if(e & (nrun <= capm1), wp, o_rs, o_cnt);
         wp += (int)e;
@@ -268,12 +273,20 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     }
     if (lane == 0) vprog[wid] = 0x7fffffff;  // done: never hold the others back
     if (valid) {
-        if (a.state_out != nullptr) sc.save(a.state_out, a.npix, p);
+        if (a.state_out != nullptr) sc.save(a.state_out + sh * Scan<METHOD>::kFields * a.npix, a.npix, p);
         int rs, cnt;
         const bool e = sc.tail(rs, cnt);
         emit(e, rs, cnt);
-        a.counts[p] = (uint32_t)nrun;
-        a.last[p] = sc.last == kNoSpike ? -1 : sc.last;
+        a.counts[sh * a.npix + p] = (uint32_t)nrun;
+        a.last[sh * a.npix + p] = sc.last == kNoSpike ? -1 : sc.last + fbase;
+        if (a.seg_out != nullptr) {  // re-scan: the whole list is segment 0
+            uint32_t* sg = a.seg_out + p * 2 * a.nseg;
+            const uint32_t nk = (uint32_t)min(nrun, a.cap);
+            for (int r = 0; r < a.nseg; ++r) {  // [0, n), then empty segments at n
+                sg[2 * r] = r == 0 ? 0u : nk;
+                sg[2 * r + 1] = nk;
+            }
+        }
     }
 }
 

@@ -31,16 +31,38 @@ namespace spk {
 
 namespace {
 
+// first speculative run's start, shard frames (in-grid split: the rows hold
+// stream frames, shard r's region at r*rstride + kSplitGap)
+__device__ __forceinline__ int spec_first_start(const ShardArgs& a, int64_t p) {
+    if (a.grid_sf > 0) {
+        const int r = (int)blockIdx.y + 1;
+        return (int)a.spec[p * a.nshards * a.rstride + r * a.rstride + kSplitGap].start - r * a.grid_sf;
+    }
+    return (int)a.spec[p * a.scap].start;
+}
+
+// shift a state's frame fields by -len (to the next shard's frames)
+template <int METHOD>
+__device__ __forceinline__ void shift_state(Scan<METHOD>& X, int len) {
+    if (X.last != kNoSpike) X.last -= len;
+    if (X.lo < kLim) X.rs -= len;
+    if (X.fl0 != kNoSpike) X.fl0 -= len;
+    if (X.fl1 != kNoSpike) X.fl1 -= len;
+    if (X.sf != kNoSpike) X.sf -= len;
+}
+
 // FSR shortcut: when the speculative scan had no break in the whole shard, the
 // shard's intervals all lie in its final pair, so the true automaton never
 // breaks either iff E's pair, the boundary-crossing interval and that pair fit
 // one pair {x, x+1} -- then its end state follows without a scan.  (Pixels
 // whose speculative pair never completes in a long shard would otherwise keep
 // their warp scanning to the shard end.)
-__device__ bool fsr_no_break(const ShardArgs& a, int64_t p, const Scan<kFSR>& E, Scan<kFSR>& X) {
-    if (a.scount[p] > 1u) return false;  // the speculative scan broke in the shard
-    Scan<kFSR> S;
-    S.restore(a.sstate, a.npix, p);
+// E: the true entry; S, scount: the speculative end state and run count of
+// the shard; f1: the speculative first run's start (its second spike's frame
+// is not needed: S.cnt counts the intervals after it)
+__device__ bool fsr_no_break_core(const Scan<kFSR>& E, const Scan<kFSR>& S, uint32_t scount, int f1s,
+                                  Scan<kFSR>& X) {
+    if (scount > 1u) return false;  // the speculative scan broke in the shard
     if (S.last == kNoSpike) {  // no spike in the shard
         X = E;
         return true;
@@ -50,7 +72,7 @@ __device__ bool fsr_no_break(const ShardArgs& a, int64_t p, const Scan<kFSR>& E,
         return true;
     }
     const bool hasS = S.lo < kLim;  // >= 2 spikes in the shard
-    const int f1 = hasS ? (int)a.spec[p * a.scap].start : S.last;
+    const int f1 = hasS ? f1s : S.last;
     const int t0 = f1 - E.last;
     int lo = t0, hi = t0;
     if (E.lo < kLim) {
@@ -75,6 +97,13 @@ __device__ bool fsr_no_break(const ShardArgs& a, int64_t p, const Scan<kFSR>& E,
     return true;
 }
 
+__device__ bool fsr_no_break(const ShardArgs& a, int64_t p, const Scan<kFSR>& E, Scan<kFSR>& X) {
+    if (a.scount[p] > 1u) return false;
+    Scan<kFSR> S;
+    S.restore(a.sstate, a.npix, p);
+    return fsr_no_break_core(E, S, a.scount[p], S.lo < kLim ? spec_first_start(a, p) : 0, X);
+}
+
 }  // namespace
 
 // Thread per pixel in warp lockstep over 32-frame words: lanes load the
@@ -82,6 +111,21 @@ __device__ bool fsr_no_break(const ShardArgs& a, int64_t p, const Scan<kFSR>& E,
 // every lane of the warp has synced (or the shard ends).
 template <int METHOD>
 __global__ void __launch_bounds__(64) k_resolve(ShardArgs a) {
+    int entry_shift = 0;
+    if (a.grid_sf > 0) {  // in-grid split: shard r = blockIdx.y + 1, entry = spec end of r-1
+        const int r = (int)blockIdx.y + 1;
+        const int64_t n = a.npix;
+        a.planes = reinterpret_cast<const char*>(a.planes) + (size_t)r * a.grid_sf * a.pitch;
+        a.frames = min(a.grid_sf, a.total_frames - r * a.grid_sf);
+        a.entry = a.sstate + (int64_t)(r - 1) * Scan<METHOD>::kFields * n;
+        entry_shift = a.grid_sf;
+        a.scount += (int64_t)r * n;
+        a.sstate += (int64_t)r * Scan<METHOD>::kFields * n;
+        a.prefix += (int64_t)r * n * a.pcap;
+        a.sync += (int64_t)r * n;
+        a.tstate += (int64_t)r * Scan<METHOD>::kFields * n;
+        a.syncj += (int64_t)r * n;
+    }
     const int lane = threadIdx.x & 31;
     const int64_t word = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (word * 32 >= a.npix) return;  // warp-uniform
@@ -97,9 +141,11 @@ __global__ void __launch_bounds__(64) k_resolve(ShardArgs a) {
     if (valid) {
         T.restore(a.entry, a.npix, p);
         T.nrun = 0;
+        if (entry_shift) shift_state(T, entry_shift);
     }
     spk_run_t* pre = a.prefix + (valid ? p * a.pcap : 0);
     int m = 0;
+    int sj = 0, jsync = -1;  // speculative runs closed (before the sync)
     bool done = !valid;
     spk_sync_t out{0, 0, 0, -1};
     if constexpr (METHOD == kFSR) {
@@ -144,9 +190,10 @@ __global__ void __launch_bounds__(64) k_resolve(ShardArgs a) {
                 if (m < a.pcap) pre[m] = spk_run_t{(uint32_t)rs, (uint32_t)cnt};
                 ++m;
             }
-            S.step(n, rs, cnt);
+            sj += (int)S.step(n, rs, cnt);
             if (T.same_future(S)) {
                 out = spk_sync_t{T.rs, S.rs, T.cnt - S.cnt, m};
+                jsync = sj;
                 done = true;
                 break;
             }
@@ -163,6 +210,7 @@ __global__ void __launch_bounds__(64) k_resolve(ShardArgs a) {
         out.npre = -1;
     }
     a.sync[p] = out;
+    if (a.syncj != nullptr) a.syncj[p] = jsync;  // index of the synced speculative run
 }
 
 namespace {
@@ -384,6 +432,179 @@ __global__ void __launch_bounds__(128) k_stitch(ShardArgs a) {
     a.rcount[p] = (uint32_t)k;
     a.rlast[p] = last;
 }
+
+// ------------------------------------------------------ in-grid time split --
+// One stream cut in S shards on ONE GPU (capi.cu reconstruct_impl): all
+// speculative scans in one K2 launch, all resolves in one k_resolve launch
+// (shard r resolved from the speculative end state of shard r-1 instead of
+// the true one), then this pass walks each pixel's shards in order.  The
+// resolve of shard r is the true one iff its entry decides like the true
+// entry (Scan::same_future, or both without an interval and the same last
+// spike): the states can then differ only in the open run's bookkeeping, so
+// the true runs are the resolved ones with the entry run's start / count
+// corrected.  A pixel failing that (or overflowing a capacity) is flagged
+// for a whole-stream re-scan (k_segment with flags).
+namespace {
+
+template <int METHOD>
+__device__ bool decision_equal(const Scan<METHOD>& A, const Scan<METHOD>& B) {
+    const bool ia = A.lo < kLim, ib = B.lo < kLim;
+    if (ia != ib) return false;
+    if (!ia) return A.last == B.last;
+    return A.same_future(B);
+}
+
+}  // namespace
+
+// a state's fields through the read-only path (FSR: the 6 it uses)
+template <int METHOD>
+__device__ __forceinline__ void load_state(Scan<METHOD>& X, const int32_t* __restrict__ st, int64_t n,
+                                           int64_t p) {
+    if constexpr (METHOD == kFSR) {
+        X.init();
+        X.last = __ldg(st + p);
+        X.lo = __ldg(st + n + p);
+        X.rs = __ldg(st + 2 * n + p);
+        X.cnt = __ldg(st + 3 * n + p);
+        X.nrun = __ldg(st + 4 * n + p);
+        X.hw = (uint32_t)__ldg(st + 5 * n + p);
+    } else {
+        X.restore(st, n, p);
+    }
+}
+
+template <int METHOD>
+__global__ void __launch_bounds__(128) k_split_combine(SplitArgs a) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= a.npix) return;
+    constexpr int F = Scan<METHOD>::kFields;
+    const int S = a.nshards;
+    const int64_t n = a.npix;
+    spk_run_t* row = a.runs + p * S * a.rstride;
+    uint32_t* sg = a.seg + p * S * 2;
+    bool bad = false;
+    uint32_t total = 0;
+    int32_t last_abs = -1;
+    Scan<METHOD> E;   // true entry of shard r (shard r frames)
+    Scan<METHOD> Xp;  // speculative end state of shard r-1 (its own frames)
+    E.init();
+    Xp.init();
+    for (int r = 0; r < S; ++r) {
+        const int f0 = r * a.sf;
+        const int len = min(a.sf, a.frames - f0);
+        const int64_t base = (int64_t)r * a.rstride + kSplitGap;
+        const uint32_t cr = __ldg(a.scount + r * n + p);
+        Scan<METHOD> Xs;  // speculative end state of shard r
+        load_state(Xs, a.sstate + (int64_t)r * F * n, n, p);
+        const spk_sync_t sy = r > 0 ? a.sync[r * n + p] : spk_sync_t{0, 0, 0, 0};
+        const int jr = r > 0 ? __ldg(a.syncj + r * n + p) : 0;
+        if (cr > (uint32_t)a.scap) {  // speculative list overflowed
+            bad = true;
+            break;
+        }
+        Scan<METHOD> X = Xs;  // true end state of shard r (shard r frames)
+        int64_t b = base, e = base + cr;
+        if (r > 0) {
+            Scan<METHOD> Ep = Xp;  // the entry the resolve used
+            shift_state(Ep, a.sf);
+            if (!decision_equal(E, Ep)) {
+                // FSR: a shard whose speculative scan never broke is decided
+                // by the pairs alone (fsr_no_break): no run closes in it
+                bool ok = false;
+                if constexpr (METHOD == kFSR) {
+                    const int f1s = cr >= 1u ? (int)row[base].start - f0 : 0;
+                    ok = fsr_no_break_core(E, Xs, cr, f1s, X);
+                }
+                if (!ok) {
+                    bad = true;
+                    break;
+                }
+                b = e = base;
+                if ((r == S - 1) & (X.lo < kLim)) {
+                    row[e] = spk_run_t{(uint32_t)(X.rs + f0), (uint32_t)X.cnt};
+                    ++e;
+                }
+            } else {
+                // the entry run (open at the shard start, with an interval) is
+                // the only run whose bookkeeping differs: start E.rs, count + dcnt
+                const bool adj = Ep.lo < kLim;
+                const int eprs = Ep.rs, ers = E.rs, dcnt = E.cnt - Ep.cnt;
+                auto fixed = [&](spk_run_t q) {
+                    if (adj & ((int)q.start == eprs)) {
+                        q.start = (uint32_t)ers;
+                        q.intervals += (uint32_t)dcnt;
+                    }
+                    q.start += (uint32_t)f0;  // stream frames
+                    return q;
+                };
+                const spk_run_t* pre = a.prefix + (r * n + p) * a.pcap;
+                if (sy.npre == -1) {  // prefix list overflowed
+                    bad = true;
+                    break;
+                }
+                if (sy.npre >= 0) {
+                    // the synced speculative run (its index: the speculative
+                    // automaton's closures before the sync, counted by k_resolve)
+                    const int64_t j = base + jr;
+                    if (jr < 0 || (uint32_t)jr >= cr || sy.npre > kSplitGap) {
+                        bad = true;
+                        break;
+                    }
+                    const spk_run_t rj = row[j];
+                    if (rj.start != (uint32_t)(sy.rs_spec + f0)) {
+                        bad = true;
+                        break;
+                    }
+                    for (int k = 0; k < sy.npre; ++k) row[j - sy.npre + k] = fixed(pre[k]);
+                    const spk_run_t tj = fixed(spk_run_t{(uint32_t)sy.rs_true, rj.intervals + (uint32_t)sy.delta});
+                    row[j] = tj;
+                    b = j - sy.npre;
+                    if ((X.lo < kLim) & (X.rs == sy.rs_spec)) {  // the synced run is still open
+                        X.rs = (int)tj.start - f0;
+                        X.cnt += (int)tj.intervals - (int)rj.intervals;
+                    }
+                } else {  // never synced: the prefix list + the open run of the true end state
+                    load_state(X, a.tstate + (int64_t)r * F * n, n, p);
+                    const int m = X.nrun;
+                    if (m > a.pcap || m + 1 > a.scap) {
+                        bad = true;
+                        break;
+                    }
+                    for (int k = 0; k < m; ++k) row[base + k] = fixed(pre[k]);
+                    e = base + m;
+                    if (X.lo < kLim) {
+                        if (adj & (X.rs == eprs)) {
+                            X.rs = ers;
+                            X.cnt += dcnt;
+                        }
+                        row[e] = spk_run_t{(uint32_t)(X.rs + f0), (uint32_t)X.cnt};
+                        ++e;
+                    }
+                }
+            }
+        }
+        // the run open at the shard end continues in the next shard (it comes
+        // back there as the entry run); the last shard keeps it
+        if ((r < S - 1) & (X.lo < kLim) & (e > b)) --e;
+        sg[2 * r] = (uint32_t)b;
+        sg[2 * r + 1] = (uint32_t)e;
+        total += (uint32_t)(e - b);
+        if (X.last != kNoSpike) last_abs = X.last + f0;
+        E = X;
+        shift_state(E, len);
+        Xp = Xs;
+    }
+    a.flags[p] = bad ? 1 : 0;
+    if (bad) {
+        atomicAdd(a.nflag, 1u);
+        return;  // the re-scan writes seg / counts / last
+    }
+    a.counts[p] = total;
+    a.last[p] = last_abs;
+}
+
+template __global__ void k_split_combine<kFSR>(SplitArgs);
+template __global__ void k_split_combine<kSSR>(SplitArgs);
 
 // the state at the start of a stream (Scan::init), for the first shard's entry
 __global__ void __launch_bounds__(256) k_state_fresh(int32_t* st, int64_t npix) {

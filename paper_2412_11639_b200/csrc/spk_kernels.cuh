@@ -52,7 +52,36 @@ struct SegArgs {
     int32_t* last;
     const int32_t* state_in = nullptr;  // time shards: automaton state at frame 0
     int32_t* state_out = nullptr;       //              state after the last frame
+    // Several time shards in one launch (blockIdx.y = shard r, fresh state):
+    // shard r covers frames [r*shard_frames, min(frames, (r+1)*shard_frames))
+    // and writes its own runs / counts / last / state_out block (counts,
+    // last: + r*npix; state_out: + r*17*npix).  shard_frames = 0: one shard.
+    int shard_frames = 0;
+    // run list placement: pixel p, shard r -> runs + r*run_shard_stride +
+    // p*run_pix_stride + run_base (run_pix_stride 0: `cap`; run_shard_stride
+    // -1: npix*cap); abs_frames: run starts in stream frames, not shard frames
+    int64_t run_pix_stride = 0;
+    int64_t run_shard_stride = -1;
+    int run_base = 0;
+    int abs_frames = 0;
+    // re-scan of selected pixels (in-grid time split fallback): only lanes
+    // with flags[p] != 0 store; warps without one exit.  seg_out: their
+    // segment table becomes one segment [0, count) (nseg entries of 2 x u32)
+    const uint8_t* flags = nullptr;
+    uint32_t* seg_out = nullptr;
+    int nseg = 0;
+    // expand stage input in split form: the pixel's runs are the segments
+    // seg_in[p*nseg + r] = {begin, end} of its row (runs + p*cap)
+    const uint32_t* seg_in = nullptr;
 };
+
+// In-grid time split of one stream (capi.cu reconstruct_impl): shard r's
+// speculative runs start kSplitGap slots into its region of the pixel's row
+// (room for the resolved prefix runs placed in front of the synced run).
+constexpr int kSplitGap = 64;
+constexpr int kSplitMinFrames = 4096;    // shortest shard worth its resolve
+constexpr int kSplitMinStream = 65536;  // shortest stream split by default
+constexpr int kSplitMaxShards = 32;  // a pixel's segment table fits one warp
 
 // ---- time shards (shard.cu): exact stitching of independently scanned
 // frame ranges, see DESIGN.md "Time sharding".
@@ -82,6 +111,45 @@ struct ShardArgs {
     int rcap;
     uint32_t* rcount;
     int32_t* rlast;             // end of the last region run (may lie past the shard)
+    // In-grid time split (grid_sf > 0): one launch resolves shards 1..S-1
+    // (blockIdx.y + 1) of a stream cut in grid_sf-frame shards; `planes`,
+    // `frames` describe the whole stream; per shard r: entry = the
+    // speculative end state of shard r-1 (sstate + (r-1)*17*npix, shifted to
+    // shard r's frames), spec runs in the pixel rows (row = S*rstride
+    // elements, shard r at r*rstride + kSplitGap, stream frames), scount /
+    // sync / (prefix: npix*pcap) / tstate blocks + r*npix (*17 for states).
+    int grid_sf = 0;
+    int nshards = 0;
+    int64_t rstride = 0;
+    int total_frames = 0;
+    int32_t* syncj = nullptr;  // index of the synced speculative run (-1: none)
+};
+
+// In-grid time split: the true run list per pixel is a sequence of segments
+// of its row, one per shard (seg[p*S + r] = {begin, end}); the combine pass
+// (k_split_combine) writes them, flags pixels whose shards need a full
+// re-scan, and sets counts / last for the whole stream.
+struct SplitArgs {
+    int64_t npix;
+    int nshards;
+    int sf;                 // shard length (the last shard may be shorter)
+    int frames;             // stream length
+    int64_t rstride;        // row elements per shard region
+    int scap;               // speculative capacity per shard (region - kSplitGap)
+    int pcap;
+    spk_run_t* runs;        // rows (npix x S*rstride)
+    const uint32_t* scount; // [S][npix]
+    const int32_t* sstate;  // [S][17][npix]
+    const spk_run_t* prefix;  // [S][npix][pcap]
+    const spk_sync_t* sync;   // [S][npix]
+    const int32_t* syncj;     // [S][npix]
+    const int32_t* tstate;    // [S][17][npix]
+    uint32_t* seg;          // [npix][S] x {begin, end}
+    uint32_t* counts;       // total true runs (or cap + 1: overflow -> k_fixup)
+    int32_t* last;          // last spike (stream frames, -1: none)
+    uint8_t* flags;         // 1: re-scan the whole stream (k_segment with flags)
+    uint32_t* nflag;        // number of flagged pixels (one counter)
+    int method;
 };
 
 // Geometry of the expand stage per output type: a warp owns a group of
@@ -150,6 +218,11 @@ struct FinArgs {
     uint32_t* cursor;      // K2c: running copy of offs (claimed with atomics)
     void* stream;          // Change<OUT>[total] (K2c)
     int seg0 = 0;          // K2c: first run segment of this launch (blockIdx.y offset)
+    // in-grid time split: runs of pixel p are the segments seg[p*nseg + r] =
+    // {begin, end} of its row (runs + p*row); cap = row length.  null: one
+    // contiguous list of min(counts[p], cap) runs.
+    const uint32_t* seg = nullptr;
+    int nseg = 0;
 };
 constexpr int kFinSeg = 64;       // K2c: runs per thread (a pixel's list spans cap / kFinSeg threads)
 constexpr int kFinWarps = 16;     // K2b/K2c: warps per block (block = one pixel group)
@@ -218,6 +291,8 @@ template <int METHOD>
 __global__ void k_resolve(ShardArgs a);
 template <int METHOD>
 __global__ void k_junction(ShardArgs a);
+template <int METHOD>
+__global__ void k_split_combine(SplitArgs a);
 __global__ void k_state_fresh(int32_t* st, int64_t npix);
 __global__ void k_close_chain(const spk_close_t* entry_next, const spk_close_t* close_next,
                               int shard_len, int64_t npix, spk_close_t* close);
@@ -229,9 +304,9 @@ template <int METHOD>
 __global__ void k_rec_write(RecArgs a);
 template <int METHOD, typename OUT>
 __global__ void k_fixup(SegArgs a, OUT* out, size_t out_pitch);
-template <int GP>
+template <int GP, bool SPLIT>
 __global__ void k_fin_bins(FinArgs a);
-template <typename OUT>
+template <typename OUT, bool SPLIT>
 __global__ void k_fin_scatter(FinArgs a);
 template <typename OUT>
 __global__ void k_expand(ExpArgs a);
