@@ -420,6 +420,35 @@ SPK_HD int bit_popc(uint32_t x) {
 SPK_HD uint32_t bit_sel(bool cond, uint32_t a, uint32_t b) {
     return b ^ ((a ^ b) & (0u - (uint32_t)cond));
 }
+// cond ? a : b as one SEL (the compiler would branch around a costly a)
+SPK_HD int bit_selp(bool cond, int a, int b) {
+#ifdef __CUDA_ARCH__
+    int r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tselp.b32 %0, %2, %3, q;\n\t}"
+        : "=r"(r) : "r"((uint32_t)cond), "r"(a), "r"(b));
+    return r;
+#else
+    return cond ? a : b;
+#endif
+}
+// index of the highest set bit, -1 for 0 (FLO)
+SPK_HD int bit_flo(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    int r;
+    asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+#else
+    return x ? 31 - __builtin_clz(x) : -1;
+#endif
+}
+// x << min(s, 32) (s = 0xffffffff, i.e. -1, also gives 0)
+SPK_HD uint32_t bit_shl_clamp(uint32_t x, uint32_t s) {
+#ifdef __CUDA_ARCH__
+    return __funnelshift_lc(0u, x, s);
+#else
+    return s >= 32u ? 0u : x << s;
+#endif
+}
 // x >> min(s, 32)
 SPK_HD uint32_t bit_shr_clamp(uint32_t x, uint32_t, uint32_t s) {
 #ifdef __CUDA_ARCH__
@@ -505,7 +534,7 @@ SPK_HD int fsr_batch4(SC& sc, uint32_t W0, uint32_t W1, uint32_t W2, uint32_t W3
     // per-window constants: a second shift by lo when the pair is single
     // (OR-idempotent, no select per word), the adjacency mask when lo >= 2
     const uint32_t sh1 = (uint32_t)lo, sh2 = (uint32_t)lo + hw;
-    const uint32_t twom = lo >= 2 ? 0xffffffffu : 0u;
+    const uint32_t sa = lo >= 2 ? 1u : 32u;  // adjacency test shift (32: off)
     const uint32_t r0 = W0 & bit_shr_clamp(0xffffffffu, 0u, (uint32_t)cpos);
     int pv = sc.last + lo;  // last spike before the word under test, plus lo
     int p0v, p1v, p2v, p3v;
@@ -513,13 +542,12 @@ SPK_HD int fsr_batch4(SC& sc, uint32_t W0, uint32_t W1, uint32_t W2, uint32_t W3
     auto test = [&](uint32_t w, uint32_t r, int base, int& prev_out, uint32_t& V) {
         prev_out = pv;
         const uint32_t Q = bit_shr_clamp(w, 0u, sh1) | bit_shr_clamp(w, 0u, sh2);
-        const int f = bit_clz(r | 1u);
-        const uint32_t fb = (0x80000000u >> f) & r;  // r's first spike (0 if none)
-        const uint32_t bad0 = (uint32_t)(base + f - pv) > hw ? fb : 0u;
-        V = (r & ~(Q | fb)) | (r & (w >> 1) & w & twom) | bad0;
-        // r's last spike is its lowest set bit: frame base + clz(r & -r)
-        const int lastr = base + bit_clz(r & (0u - r)) + lo;
-        pv = r ? lastr : pv;
+        const int hi = bit_flo(r);  // r's first spike: frame base + 31 - hi
+        const uint32_t fb = bit_shl_clamp(1u, (uint32_t)hi);  // its bit (0 if none)
+        const uint32_t bad0 = (uint32_t)(base + 31 - hi - pv) > hw ? fb : 0u;
+        V = (r & ~(Q | fb)) | (r & w & bit_shr_clamp(w, 0u, sa)) | bad0;
+        // r's last spike is its lowest set bit: frame base + 32 - ffs(r)
+        pv = bit_selp(r != 0u, base + lo + 32 - bit_ffs(r), pv);
     };
     test(W0, r0, base0, p0v, V0);
     test(W1, W1, base0 + 32, p1v, V1);
@@ -562,12 +590,16 @@ SPK_HD int fsr_batch4(SC& sc, uint32_t W0, uint32_t W1, uint32_t W2, uint32_t W3
 // a quiet window costs about half a 4-word batch per word (static scenes,
 // long streams).  word(k) returns word k of the window; words past the end
 // of the stream must read as 0.
+//
+// Per word ~20 instructions and no branch: the first spike as FLO (fb = its
+// bit, 0 for an empty word), the adjacency test as one clamped shift (by 32
+// when lo < 2: off), the last spike as FFS with a select.
 template <int N, class SC, class WORD>
 SPK_HD bool fsr_quiet(SC& sc, WORD&& word, int base0, int& cpos) {
     const int lo = sc.lo;
     const uint32_t hw = sc.hw;
     const uint32_t sh1 = (uint32_t)lo, sh2 = (uint32_t)lo + hw;
-    const uint32_t twom = lo >= 2 ? 0xffffffffu : 0u;
+    const uint32_t sa = lo >= 2 ? 1u : 32u;
     int pv = sc.last + lo;  // last spike before the word under test, plus lo
     uint32_t bad = 0u, n = 0u;
 #pragma unroll
@@ -576,12 +608,13 @@ SPK_HD bool fsr_quiet(SC& sc, WORD&& word, int base0, int& cpos) {
         const uint32_t r = k == 0 ? w & bit_shr_clamp(0xffffffffu, 0u, (uint32_t)cpos) : w;
         const int base = base0 + 32 * k;
         const uint32_t Q = bit_shr_clamp(w, 0u, sh1) | bit_shr_clamp(w, 0u, sh2);
-        const int f = bit_clz(r | 1u);
-        const uint32_t fb = (0x80000000u >> f) & r;
-        const uint32_t bad0 = (uint32_t)(base + f - pv) > hw ? fb : 0u;
-        bad |= (r & ~(Q | fb)) | (r & (w >> 1) & w & twom) | bad0;
+        const int hi = bit_flo(r);                // r's first spike is frame base + 31 - hi
+        const uint32_t fb = bit_shl_clamp(1u, (uint32_t)hi);  // its bit (0: no spike)
+        const uint32_t bad0 = (uint32_t)(base + 31 - hi - pv) > hw ? fb : 0u;
+        bad |= (r & ~(Q | fb)) | (r & w & bit_shr_clamp(w, 0u, sa)) | bad0;
         n += (uint32_t)bit_popc(r);
-        pv = r ? base + bit_clz(r & (0u - r)) + lo : pv;
+        // r's last spike (lowest set bit) is frame base + 32 - ffs(r)
+        pv = bit_selp(r != 0u, base + lo + 32 - bit_ffs(r), pv);
     }
     if (bad) return false;
     sc.cnt += (int)n;

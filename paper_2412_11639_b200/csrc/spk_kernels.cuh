@@ -159,7 +159,13 @@ constexpr int kSub = 16;
 constexpr int kBins = kChunk / kSub;
 constexpr int kPieceSubs = 4;                // K3 tile height: 64 frames
 constexpr int kPieces = kBins / kPieceSubs;  // K3 tiles per (group, chunk)
-constexpr int kPieceSparse = 2;              // changes per pixel per chunk up to which
+#ifndef SPK_PIECE_SPARSE  // (build-time overrides: A/B probes)
+#define SPK_PIECE_SPARSE 2
+#endif
+#ifndef SPK_EXP_WARPS
+#define SPK_EXP_WARPS 4
+#endif
+constexpr int kPieceSparse = SPK_PIECE_SPARSE;  // changes per pixel per chunk up to which
                                              // K3 tiles are 64 frames high (else 128)
 constexpr int kPieceDensity = 12;            // ... up to which 128 frames high (else 256)
 constexpr int kPieceDense = 48;              // ... above which K3 writes the chunk whole
@@ -170,7 +176,7 @@ template <typename OUT>
 struct Geo;
 template <>
 struct Geo<uint8_t> {
-    static constexpr int P = 16, WARPS = 4;
+    static constexpr int P = 16, WARPS = SPK_EXP_WARPS;
 };
 template <>
 struct Geo<float> {
