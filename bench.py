@@ -676,10 +676,24 @@ def long_stream(args, rank, world, dev):
         res.update(value=T5 / (ms * 1e-3), ms_per_step=ms,
                    parallelism=f"time shards x{world} (exact boundary resolution)")
     else:
+        import ctypes as C
+
+        from paper_2412_11639_b200 import _capi as capi
         ms = timed(lambda: spk.reconstruct(vol, args.method, out=out))
         ref = sums()
+        # the in-grid time split reconstruct() chose (capi.cu reconstruct_split)
+        lib = capi.lib()
+        lib.spk_set_timing(1)
+        spk.reconstruct(vol, args.method, out=out)
+        sh, fl = C.c_int32(), C.c_int64()
+        capi.check(lib.spk_last_split(C.byref(sh), C.byref(fl)))
+        lib.spk_set_timing(0)
         ms8 = timed(lambda: reconstruct_time_sharded(vol, args.method, nshards=8, out=out), 3, 3)
-        res.update(value=T5 / (ms * 1e-3), ms_per_step=ms, parallelism="single pass",
+        res.update(value=T5 / (ms * 1e-3), ms_per_step=ms,
+                   parallelism=(f"one GPU, one call: in-grid time split x{sh.value} "
+                                f"(one K2 launch for all shards, exact stitching)" if sh.value > 1
+                                else "one GPU, single pass"),
+                   in_grid_split={"shards": sh.value, "pixels_rescanned": fl.value},
                    time_sharded_8_on_1gpu_ms=ms8,
                    time_sharded_equal=bool(torch.equal(sums(), ref)))
     pxf = W * H * T5
