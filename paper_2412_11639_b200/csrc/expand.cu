@@ -159,10 +159,16 @@ __device__ __forceinline__ Change<OUT> make_change(uint32_t fo, uint32_t pl, OUT
 // their stream slots are claimed with 8 independent atomics on a copy of the
 // scanned histogram, then the 8 changes are stored -- one memory round trip
 // per 8 runs.
+#ifndef SPK_K2C_MINB
+#define SPK_K2C_MINB 4  // uint8 lists: 64 registers, more warps in flight (C2 finalize 0.411 -> 0.398 ms)
+#endif
+#ifndef SPK_K2C_B
+#define SPK_K2C_B 8
+#endif
 template <typename OUT, bool SPLIT>
-__global__ void __launch_bounds__(256) k_fin_scatter(FinArgs a) {
+__global__ void __launch_bounds__(256, sizeof(OUT) == 1 && !SPLIT ? SPK_K2C_MINB : 1) k_fin_scatter(FinArgs a) {
     constexpr int GP = 32 * Geo<OUT>::P;
-    constexpr int B = 8;
+    constexpr int B = SPK_K2C_B;
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= a.npix) return;
     const int g = (int)(p / GP);
