@@ -78,19 +78,25 @@ def kernel_rows(rep: str):
     return out
 
 
-def summarize(reps):
+def summarize(reps, out=None):
     d = {"build_sha16": hashlib.sha256(LIB.read_bytes()).hexdigest()[:16],
          "source": "ncu --set full --clock-control none, one warm configs[1] step per method "
                    "(profiles/ncu_step_profile.py)"}
     for rep in reps:
         method = "ssr" if "ssr" in Path(rep).name else "fsr"
         d[method] = kernel_rows(rep)
-    (ROOT / "profiles" / "ncu_step.json").write_text(json.dumps(d, indent=1) + "\n")
+    Path(out or ROOT / "profiles" / "ncu_step.json").write_text(json.dumps(d, indent=1) + "\n")
     print(json.dumps(d, indent=1))
 
 
 if __name__ == "__main__":
     if sys.argv[1] == "run":
         run(sys.argv[2])
-    else:
-        summarize(sys.argv[2:])
+    else:  # summarize REP... [--out FILE]
+        args = sys.argv[2:]
+        out = None
+        if "--out" in args:
+            i = args.index("--out")
+            out = args[i + 1]
+            del args[i:i + 2]
+        summarize(args, out)
