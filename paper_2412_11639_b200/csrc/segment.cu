@@ -19,6 +19,8 @@
 // counts[p] (may exceed cap: overflow) and last[p] (last spike, -1 if none).
 // K2b/K2c (expand.cu) turn them into values and a frame-sorted change stream
 // for K3; overflowed pixels are rewritten exactly by k_fixup after K3.
+#include <type_traits>
+
 #include "spk_fsm.cuh"
 #include "spk_kernels.cuh"
 
@@ -205,25 +207,33 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         if (ev <= kSsrDense * 32 * probe) {
             bulk(ngroups);
         } else {  // lanes all stand at word `probe`
-            auto spikes = [&](int g) {
-                uint32_t w = rg[g & (kRing - 1)][lane];
-                const int base = g * 32;
-                while (w) {
-                    const int c = __clz(w);
-                    w ^= 0x80000000u >> c;
-                    int rs, cnt;
-                    const bool e = sc.step(base + c, rs, cnt);
-                    emit(e, rs, cnt);
+            // the frame fields of the state matter only for a saved state
+            auto run_spikes = [&](auto frames) {
+                constexpr bool FR = decltype(frames)::value;
+                auto spikes = [&](int g) {
+                    uint32_t w = rg[g & (kRing - 1)][lane];
+                    const int base = g * 32;
+                    while (w) {
+                        const int c = __clz(w);
+                        w ^= 0x80000000u >> c;
+                        int rs, cnt;
+                        const bool e = sc.template step<FR>(base + c, rs, cnt);
+                        emit(e, rs, cnt);
+                    }
+                };
+                int g = probe;
+                for (; g < produced && g < ngroups; ++g) spikes(g);  // words already in the ring
+                for (int g0 = g; g0 < ngroups; g0 += kBatch) {
+                    produce(g0);
+#pragma unroll
+                    for (int j = 0; j < kBatch; ++j)
+                        if (g0 + j < ngroups) spikes(g0 + j);
                 }
             };
-            int g = probe;
-            for (; g < produced && g < ngroups; ++g) spikes(g);  // words already in the ring
-            for (int g0 = g; g0 < ngroups; g0 += kBatch) {
-                produce(g0);
-#pragma unroll
-                for (int j = 0; j < kBatch; ++j)
-                    if (g0 + j < ngroups) spikes(g0 + j);
-            }
+            if (a.state_out != nullptr)
+                run_spikes(std::true_type{});
+            else
+                run_spikes(std::false_type{});
         }
     } else {
     // FSR consumers: every lane walks its own pixel through the words at its

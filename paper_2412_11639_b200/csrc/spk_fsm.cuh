@@ -283,7 +283,10 @@ struct Scan {
 
     // returns true when the run (rs, cnt) closed before this spike.  Written
     // with bitwise logic only (no && / ||), so the compiler emits selects,
-    // not divergent branches.
+    // not divergent branches.  FRAMES = false skips the frame fields fl0,
+    // fl1, sf (read only by the bulk test ssr_flags and saved states): the
+    // SSR spike loop uses it when neither follows.
+    template <bool FRAMES = true>
     SPK_HD bool step(int n, int& out_rs, int& out_cnt) {
         const int t = fsub(n, last);
         const int d = fsub(t, lo);
@@ -314,14 +317,16 @@ struct Scan {
             const uint32_t nghw = (fresh | gnone) ? 0u : (ghw | (uint32_t)gext);
             l0 = fsel(kn, ii, l0);
             l1 = fsel(ki, ii, l1);
-            fl0 = fsel(kn, n, fl0);
-            fl1 = fsel(ki, n, fl1);
+            if (FRAMES) {
+                fl0 = fsel(kn, n, fl0);
+                fl1 = fsel(ki, n, fl1);
+            }
             g0 = fsel(kn, nglo, g0);
             g1 = fsel(ki, nglo, g1);
             h0 = (uint32_t)fsel(kn, (int)nghw, (int)h0);
             h1 = (uint32_t)fsel(ki, (int)nghw, (int)h1);
             sub0 = brk ? ii : sub0;
-            sf = brk ? n : sf;
+            if (FRAMES) sf = brk ? n : sf;
             ii = fadd(ii, 1);
         }
         out_rs = rs;

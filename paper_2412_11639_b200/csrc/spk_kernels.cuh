@@ -28,7 +28,10 @@ constexpr int kDriftFsr = 48;
 constexpr int kDriftSsr = 160;
 constexpr int kBatch = 8;        // 32-frame groups per prefetch batch
 constexpr int kSsrProbe = 64;    // SSR: words scanned in bulk mode before choosing the mode
-constexpr int kSsrDense = 2;     // SSR: events per lane-word above which spike mode wins
+#ifndef SPK_SSR_DENSE
+#define SPK_SSR_DENSE 2
+#endif
+constexpr int kSsrDense = SPK_SSR_DENSE;  // SSR: events per lane-word above which spike mode wins
 // transposed words buffered per lane (bounds lane drift); 32 keeps the rings
 // at 32 KB per block, which leaves L1 room for the plane sectors the block's
 // warps share (64: C3 K2 4.01 vs 3.82 ms)
