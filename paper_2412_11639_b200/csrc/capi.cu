@@ -233,18 +233,16 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
                          static_cast<uint32_t*>(w.cursor.p));
     if (rc) return rc;
     f.cursor = static_cast<uint32_t*>(w.cursor.p);
+    // threads stride over a pixel's kFinSeg-run blocks (grid.y <= 64: a
+    // 1M-frame list of one run per pixel is not 500 block rows of exits)
     const int nseg = (sa.cap + kFinSeg - 1) / kFinSeg;
-    static const int maxy = (int)test_limit("SPK_TEST_GRID_Y", 65535);
-    for (int g0 = 0; g0 < nseg; g0 += maxy) {  // grid.y limit: caps past 4.19M runs
-        f.seg0 = g0;
-        const unsigned ny = (unsigned)std::min(maxy, nseg - g0);
-        const dim3 grid((unsigned)((sa.npix + 255) / 256), ny);
-        if (f.seg)
-            k_fin_scatter<OUT, true><<<grid, 256, 0, s>>>(f);
-        else
-            k_fin_scatter<OUT, false><<<grid, 256, 0, s>>>(f);
-        SPK_LAUNCHED("k_fin_scatter");
-    }
+    static const int maxy = (int)test_limit("SPK_TEST_GRID_Y", 64);
+    const dim3 grid((unsigned)((sa.npix + 255) / 256), (unsigned)std::min(maxy, nseg));
+    if (f.seg)
+        k_fin_scatter<OUT, true><<<grid, 256, 0, s>>>(f);
+    else
+        k_fin_scatter<OUT, false><<<grid, 256, 0, s>>>(f);
+    SPK_LAUNCHED("k_fin_scatter");
     mark(2, s);
 
     ExpArgs e;

@@ -180,10 +180,10 @@ __global__ void __launch_bounds__(256, sizeof(OUT) == 1 && !SPLIT ? SPK_K2C_MINB
     // pixel's list is spread over several threads: enough loads and atomics
     // in flight even for sensors with few pixels)
     // (split lists: the same numbering over the row's segments in order)
-    const int kb = (a.seg0 + (int)blockIdx.y) * kFinSeg;
+    // blocks of kFinSeg list entries, strided over gridDim.y (a long list
+    // with few runs per pixel does not launch a block row per capacity block)
     const int n = (int)min(cnt, (uint32_t)a.cap);
-    if (kb >= n) return;
-    const int ke = min(n, kb + kFinSeg);
+    if ((int)blockIdx.y * kFinSeg >= n) return;
     const spk_run_t* rp = a.runs + p * a.cap;
     const uint32_t lastp = (uint32_t)a.last[p];
     Change<OUT>* stp = reinterpret_cast<Change<OUT>*>(a.stream);
@@ -224,6 +224,8 @@ __global__ void __launch_bounds__(256, sizeof(OUT) == 1 && !SPLIT ? SPK_K2C_MINB
             }
         }
     };
+    for (int kb = (int)blockIdx.y * kFinSeg; kb < n; kb += (int)gridDim.y * kFinSeg) {
+    const int ke = min(n, kb + kFinSeg);
     if constexpr (!SPLIT) {  // one contiguous list
         for (int k0 = kb; k0 < ke; k0 += B) {
             spk_run_t r[B + 1];
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(256, sizeof(OUT) == 1 && !SPLIT ? SPK_K2C_MINB
                 }
             }
         }
-        return;
+        continue;
     }
     // in-grid time split: list entries [kb, ke) over the row's segments
     const uint32_t* sg = a.seg + p * a.nseg * 2;
@@ -283,6 +285,7 @@ __global__ void __launch_bounds__(256, sizeof(OUT) == 1 && !SPLIT ? SPK_K2C_MINB
             range(lo, hi, nxt, fin);
         }
         vo += len;
+    }
     }
 }
 

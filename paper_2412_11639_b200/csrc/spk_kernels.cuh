@@ -226,7 +226,6 @@ struct FinArgs {
     const uint32_t* offs;  // exclusive prefix of bins
     uint32_t* cursor;      // K2c: running copy of offs (claimed with atomics)
     void* stream;          // Change<OUT>[total] (K2c)
-    int seg0 = 0;          // K2c: first run segment of this launch (blockIdx.y offset)
     // in-grid time split: runs of pixel p are the segments seg[p*nseg + r] =
     // {begin, end} of its row (runs + p*row); cap = row length.  null: one
     // contiguous list of min(counts[p], cap) runs.

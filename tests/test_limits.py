@@ -1,6 +1,6 @@
 """Workspace limits of the expand stage: the change stream's
 32-bit offsets (pixel parts when npix * cap would pass 2^32) and the K2c
-grid.y limit (launches split in segment slabs).  The limits are lowered
+grid.y bound (threads stride over a pixel's run blocks).  The limits are lowered
 through test hooks (SPK_TEST_PART_ENTRIES / SPK_TEST_GRID_Y, read once per
 process) so the split paths run on small volumes; each subprocess compares
 its frames with the oracle."""
@@ -51,5 +51,5 @@ def test_expand_in_pixel_parts():
 
 @pytest.mark.gpu
 def test_fin_scatter_segment_slabs():
-    # cap 3000 -> 47 run segments of 64; grid.y limited to 5 -> 10 launches
+    # cap 3000 -> 47 run blocks of 64; grid.y limited to 5 -> each thread strides over ~10
     _run({"SPK_TEST_GRID_Y": "5"}, 3000)
