@@ -232,6 +232,19 @@ int spk_reconstruct_host_batch(const spk_geom* g, int32_t count, const void* con
                                int method, int tfp_window, int out_type, void* const* h_outs,
                                size_t out_pitch);
 
+/* Device batch (BASELINE configs[3]: many independent streams of one
+ * geometry): volume i = d_planes[i] -> d_outs[i] (out_type SPK_OUT_*, pitch
+ * out_pitch elements), exactly as `count` spk_reconstruct_* calls.  The calls
+ * are captured once into a CUDA graph over four forked branches (kernels of
+ * different volumes overlap; no per-call launch gaps), cached per thread and
+ * device by geometry, method and buffer addresses, and replayed on `stream`
+ * by later calls with the same buffers.  Asynchronous. */
+int spk_reconstruct_batch(const spk_geom* g, int32_t count, const void* const* d_planes, int method,
+                          int tfp_window, int out_type, void* const* d_outs, size_t out_pitch,
+                          void* stream);
+/* drop this thread's cached batch graphs (waits for the device) */
+int spk_batch_release(void);
+
 /* Host boundary of segment_fsr / segment_ssr (proj/src/reconstruct.cpp:198-211):
  * dense SPK1 payload in, per-pixel run lists out (layout as spk_segment;
  * h_runs holds W*H*run_cap entries).  Synchronous. */

@@ -17,6 +17,7 @@ from .recon import (  # noqa: F401
     read_raw,
     read_spk,
     reconstruct,
+    reconstruct_batch,
     reconstruct_host,
     reconstruct_host_batch,
     reconstruct_host_multi,

@@ -46,6 +46,8 @@ SIGNATURES = {
     "spk_reconstruct_host_multi": (C.c_int, [_G, _P, C.c_int, C.c_int, C.c_int, _P, C.c_size_t, _P,
                                              C.c_int32]),
     "spk_segment_host": (C.c_int, [_G, _P, C.c_int, _P, C.c_int64, _P, _P]),
+    "spk_reconstruct_batch": (C.c_int, [_G, C.c_int32, _P, C.c_int, C.c_int, C.c_int, _P, C.c_size_t, _P]),
+    "spk_batch_release": (C.c_int, []),
     "spk_reconstruct_host_batch": (C.c_int, [_G, C.c_int32, _P, C.c_int, C.c_int, C.c_int, _P,
                                              C.c_size_t]),
     "spk_records": (C.c_int, [_G, _P, C.c_int, C.c_uint32, _P, _P, _P]),

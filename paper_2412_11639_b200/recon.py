@@ -227,6 +227,51 @@ def reconstruct(volume: PackedVolume, method="fsr", workers: int = 0,
     return out
 
 
+def reconstruct_batch(volumes, method="fsr", outs=None, dtype: torch.dtype = torch.uint8,
+                      stream=None) -> list[torch.Tensor]:
+    """reconstruct() of many volumes of one geometry on one device (BASELINE
+    configs[3]) as one CUDA graph (spk_reconstruct_batch): the calls are
+    captured once over four branches and the graph is replayed while the
+    same buffers come back (`outs`: caller-owned [T, >= H*W] tensors, reused
+    like the reference's `out`; allocated when None).  Returns the outputs as
+    [T, H, W] views; identical to per-volume reconstruct() calls."""
+    from . import _capi as C_
+    volumes = list(volumes)
+    if not volumes:
+        return []
+    m = _method(method)
+    v0 = volumes[0]
+    for v in volumes:
+        if (v.width, v.height, v.frames, v.pitch) != (v0.width, v0.height, v0.frames, v0.pitch):
+            raise ValueError("reconstruct_batch: volumes must share width, height, frames and pitch")
+        if v.planes.device != v0.planes.device:
+            raise ValueError("reconstruct_batch: volumes must be on one device")
+    npix = v0.npix
+    dev = v0.planes.device
+    if outs is None:
+        outs = [torch.empty((v0.frames, npix), dtype=dtype, device=dev) for _ in volumes]
+    outs = list(outs)
+    if len(outs) != len(volumes):
+        raise ValueError("reconstruct_batch: one output per volume")
+    dtype = outs[0].dtype
+    if dtype not in _OUT:
+        raise ValueError(f"unsupported output dtype {dtype}")
+    for o in outs:
+        if (o.dtype != dtype or o.dim() != 2 or o.shape[0] != v0.frames or o.shape[1] < npix or
+                o.stride(1) != 1 or o.stride(0) != outs[0].stride(0) or o.device != dev):
+            raise ValueError("outs must be [frames, >= W*H] row-major tensors of one dtype and pitch")
+    out_type = {torch.uint8: C_.SPK_OUT_U8, torch.float32: C_.SPK_OUT_F32,
+                torch.float64: C_.SPK_OUT_F64}[dtype]
+    if v0.frames > 0:
+        planes = (C.c_void_p * len(volumes))(*[v.planes.data_ptr() for v in volumes])
+        ptrs = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        with torch.cuda.device(dev):
+            capi.check(capi.lib().spk_reconstruct_batch(
+                v0.geom(), len(volumes), planes, int(m.kind), int(m.tfp_window), out_type, ptrs,
+                outs[0].stride(0), _stream(stream)))
+    return [o.view(v0.frames, v0.height, v0.width) if o.shape[1] == npix else o for o in outs]
+
+
 def segments(volume: PackedVolume, method="fsr", run_cap: int | None = None, stream=None):
     """Stable runs of every pixel (segment_fsr / segment_ssr without the
     degenerate lead/tail segments): returns (runs [npix, cap, 2] int64 as
