@@ -636,19 +636,20 @@ template <class SC>
 SPK_HD uint32_t fsr_flags(const SC& sc, uint32_t So, uint32_t S, int base) {
     const int lo = sc.lo;
     const uint32_t hw = sc.hw;
-    const uint32_t Q = bit_shr_clamp(So, 0u, (uint32_t)lo) |
-                       bit_sel(hw != 0u, bit_shr_clamp(So, 0u, (uint32_t)lo + 1u), 0u);
-    const uint32_t G1 = So & (So >> 1);
-    const int f = bit_clz(So | 1u);
-    const uint32_t fb = So ? (0x80000000u >> f) : 0u;
-    const bool bad0 = ((S & fb) != 0u) & ((uint32_t)(base + f - sc.last - lo) > hw);
-    return (S & ~(Q | fb)) | bit_sel(lo >= 2, S & G1, 0u) | bit_sel(bad0, fb, 0u);
+    // (a single pair shifts by lo twice: OR-idempotent; the adjacency shift
+    // is clamped to 32 -- off -- when lo < 2)
+    const uint32_t Q = bit_shr_clamp(So, 0u, (uint32_t)lo) | bit_shr_clamp(So, 0u, (uint32_t)lo + hw);
+    const int hi = bit_flo(So);  // So's first spike: frame base + 31 - hi
+    const uint32_t fb = bit_shl_clamp(1u, (uint32_t)hi);
+    const uint32_t sa = lo >= 2 ? 1u : 32u;
+    const uint32_t bad0 = (uint32_t)(base + 31 - hi - sc.last - lo) > hw ? (S & fb) : 0u;
+    return (S & ~(Q | fb)) | (S & So & bit_shr_clamp(So, 0u, sa)) | bad0;
 }
 
 template <class SC>
 SPK_HD void fsr_accept(SC& sc, uint32_t A, int base) {
     sc.cnt += bit_popc(A);
-    sc.last = A ? base + 32 - bit_ffs(A) : sc.last;
+    sc.last = bit_selp(A != 0u, base + 32 - bit_ffs(A), sc.last);
 }
 
 // ---- SSR in bulk ----------------------------------------------------------
@@ -674,21 +675,19 @@ SPK_HD uint32_t ssr_flags(const SC& sc, uint32_t So, uint32_t S, int base, int p
                           uint32_t& Cs, uint32_t& Cl) {
     const uint32_t Vf = fsr_flags(sc, So, S, base);
     const int lo = sc.lo;
-    if (lo >= kLim) {
-        Cs = Cl = 0u;
-        return Vf;
-    }
     const uint32_t hw = sc.hw;
-    const int f = bit_clz(So | 1u);
-    const uint32_t fb = So ? (0x80000000u >> f) : 0u;
-    const int d0 = base + f - prevlast;
+    // no class spikes before the first interval (lo >= kLim); branch-free:
+    // the shifts below clamp to 0 and the masks clear C
+    const uint32_t live = lo < kLim ? 0xffffffffu : 0u;
+    const int hi = bit_flo(So);
+    const uint32_t fb = bit_shl_clamp(1u, (uint32_t)hi);
+    const int d0 = base + 31 - hi - prevlast;
     // spikes closing an interval of the current sub-run: frames >= sf
-    const uint32_t sub = sc.sf <= base ? 0xffffffffu
-                                       : bit_shr_clamp(0xffffffffu, 0u, (uint32_t)(sc.sf - base));
+    const uint32_t sub = bit_shr_clamp(0xffffffffu, 0u, (uint32_t)max(sc.sf - base, 0)) & live;
     const uint32_t at_lo = bit_shr_clamp(So, 0u, (uint32_t)lo);
     const uint32_t at_lo1 = bit_shr_clamp(So, 0u, (uint32_t)lo + 1u);
-    Cs = ((So & at_lo) | bit_sel(d0 == lo, fb, 0u)) & sub;
-    Cl = ((So & at_lo1 & ~at_lo) | bit_sel(d0 == lo + 1, fb, 0u)) & bit_sel(hw != 0u, sub, 0u);
+    Cs = ((So & at_lo) | (d0 == lo ? fb : 0u)) & sub;
+    Cl = ((So & at_lo1 & ~at_lo) | (d0 == lo + 1 ? fb : 0u)) & (hw != 0u ? sub : 0u);
     uint32_t V = Vf;
 #pragma unroll
     for (int cls = 0; cls < 2; ++cls) {  // 0 = short (value lo), 1 = long (lo + 1)
@@ -700,46 +699,43 @@ SPK_HD uint32_t ssr_flags(const SC& sc, uint32_t So, uint32_t S, int base, int p
         const int fl = x ? sc.fl1 : sc.fl0;
         const uint32_t CS = C & S;
         const bool est = (l >= sc.sub0) & (g < kLim);
-        const uint32_t fcs = CS ? (0x80000000u >> bit_clz(CS)) : 0u;
-        const int D1 = cls ? g * lo + 1 : g * (lo + 1) - 1;
-        const int D2 = D1 + h * (cls ? lo : lo + 1);
-        const uint32_t Q = bit_shr_clamp(C, 0u, (uint32_t)D1) |
-                           bit_sel(h != 0, bit_shr_clamp(C, 0u, (uint32_t)D2), 0u);
-        const int fc = bit_clz(C | 1u);
-        const uint32_t fcw = C ? (0x80000000u >> fc) : 0u;
-        const int dfirst = base + fc - fl;
+        const uint32_t fcs = bit_shl_clamp(1u, (uint32_t)bit_flo(CS));  // CS's first spike
+        const int stp = cls ? lo : lo + 1;
+        const int D1 = g * stp + (cls ? 1 : -1);
+        const int D2 = D1 + h * stp;  // (h = 0: D1 again, OR-idempotent)
+        const uint32_t Q = bit_shr_clamp(C, 0u, (uint32_t)D1) | bit_shr_clamp(C, 0u, (uint32_t)D2);
+        const int hic = bit_flo(C);
+        const uint32_t fcw = bit_shl_clamp(1u, (uint32_t)hic);  // C's first spike (0 if none)
+        const int dfirst = base + 31 - hic - fl;
         const bool badf = ((fcw & S) != 0u) & (dfirst != D1) & (dfirst != D2);
-        const uint32_t gap1 = bit_sel((cls == 0) & (g >= 2), CS & bit_shr_clamp(C, 0u, (uint32_t)lo), 0u);
-        const uint32_t Vc = (CS & ~(Q | fcw)) | bit_sel(badf, fcw, 0u) | gap1;
-        V |= bit_sel(est, Vc, fcs);
+        const uint32_t gap1 = (cls == 0) & (g >= 2) ? CS & bit_shr_clamp(C, 0u, (uint32_t)lo) : 0u;
+        const uint32_t Vc = (CS & ~(Q | fcw)) | (badf ? fcw : 0u) | gap1;
+        V |= est ? Vc : fcs;
     }
     return V;
 }
 
-// bookkeeping of an accepted prefix A (no event inside) for SSR
+// bookkeeping of an accepted prefix A (no event inside) for SSR (branch-free:
+// the lanes of a warp accept different prefixes)
 template <class SC>
 SPK_HD void ssr_accept(SC& sc, uint32_t A, uint32_t Cs, uint32_t Cl, int base) {
-    if (!A) return;
     const int n = bit_popc(A);
 #pragma unroll
     for (int cls = 0; cls < 2; ++cls) {
         const uint32_t Ac = A & (cls ? Cl : Cs);
-        if (Ac) {
-            const int b = bit_ffs(Ac);  // latest class spike: bit b-1
-            const int idx = sc.ii + bit_popc(A >> (b - 1)) - 1;
-            const int fr = base + 32 - b;
-            if (((sc.lo + cls) & 1) != 0) {
-                sc.l1 = idx;
-                sc.fl1 = fr;
-            } else {
-                sc.l0 = idx;
-                sc.fl0 = fr;
-            }
-        }
+        const int b = bit_ffs(Ac);  // latest class spike: bit b-1 (b = 0: none)
+        const int idx = sc.ii + bit_popc(bit_shr_clamp(A, 0u, (uint32_t)(b - 1))) - 1;
+        const int fr = base + 32 - b;
+        const bool have = Ac != 0u;
+        const bool odd = ((sc.lo + cls) & 1) != 0;
+        sc.l1 = bit_selp(have & odd, idx, sc.l1);
+        sc.fl1 = bit_selp(have & odd, fr, sc.fl1);
+        sc.l0 = bit_selp(have & !odd, idx, sc.l0);
+        sc.fl0 = bit_selp(have & !odd, fr, sc.fl0);
     }
     sc.cnt += n;
     sc.ii += n;
-    sc.last = base + 32 - bit_ffs(A);
+    sc.last = bit_selp(A != 0u, base + 32 - bit_ffs(A), sc.last);
 }
 
 // SSR over one word: bulk acceptance up to each event, the event exact
