@@ -60,7 +60,7 @@ SPK_HD int fsub(int a, int b) {  // a - b
 // k ? a : b for an integer k in {0, 1}, as b + k * (a - b): two IMADs on the
 // FMA pipe instead of a SEL on the (saturated) integer ALU pipe.
 SPK_HD int fsel(int k, int a, int b) {
-#ifdef __CUDA_ARCH__
+#if defined(__CUDA_ARCH__) && !defined(SPK_FSEL_SEL)
     int r;
     asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(k), "r"(fsub(a, b)), "r"(b));
     return r;
