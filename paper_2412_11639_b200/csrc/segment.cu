@@ -9,8 +9,8 @@
 // frames lane i loads the warp's word from plane 32g + (31 - i); a 5-stage
 // shuffle transpose (Transpose32) turns the 32x32 bit block into one 32-frame
 // word per pixel with the earliest frame in bit 31, kept in a per-warp ring
-// in shared memory.  FSR: every lane walks its own pixel four words per
-// iteration (fsr_batch4: bit-parallel acceptance up to the next event, one
+// in shared memory.  FSR: every lane walks its own pixel kWin (3) words per
+// iteration (fsr_batch: bit-parallel acceptance up to the next event, one
 // exact automaton step for the event); SSR: bulk (ssr_flags) or word-lockstep
 // spike mode per warp.  Plane loads run one batch (kBatch groups = 256
 // frames) ahead of the scan.
@@ -237,15 +237,19 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         }
     } else {
     // FSR consumers: every lane walks its own pixel through the words at its
-    // own pace -- a window of four words per iteration, stopping at the first
-    // event (fsr_batch4) -- so a lane with many breaks does not hold the others
+    // own pace -- a window of kWin words per iteration, stopping at the first
+    // event (fsr_batch) -- so a lane with many breaks does not hold the others
     // back word by word; the ring bounds how far lanes may drift apart.
     // After an iteration in which no lane met an event, the warp tries kQuiet
     // words at once (fsr_quiet: the test alone, no selection across words);
-    // lanes whose window holds an event take the 4-word batch in the same
+    // lanes whose window holds an event take the event window in the same
     // iteration.  Moving scenes rarely have such an iteration, static scenes
     // and long quiet stretches almost always.
     static_assert(kQuiet + kBatch <= kRing, "a quiet window must fit the ring beside a batch");
+    // window of kWin words per iteration (fsr_batch): 3 measured best on
+    // moving scenes (C2 K2 0.843 ms vs 0.876 at 4, 0.869 at 2), within 2% of
+    // 4 on static and long streams
+    constexpr int kWin = SPK_WIN;
     int wi = 0;    // first word of this lane's window
     int cpos = 0;  // frames of word wi already consumed
     bool quiet = false;  // warp-uniform: the last iteration had no event
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     // needs a bounds check.
     for (;;) {
         const bool more = wi < ngroups;
-        const bool ready = wi + 4 <= produced;
+        const bool ready = wi + kWin <= produced;
         // refill only when a lane is starved (or, when quiet, short of a quiet
         // window), and only into slots no lane can still read (lowest = the
         // earliest window start)
@@ -271,11 +275,10 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
             }
         }
         bool ev = false;
-        if (more & !tookq & (wi + 4 <= produced)) {
-            const int k = fsr_batch4(sc, rg[wi & (kRing - 1)][lane], rg[(wi + 1) & (kRing - 1)][lane],
-                                     rg[(wi + 2) & (kRing - 1)][lane], rg[(wi + 3) & (kRing - 1)][lane],
-                                     wi * 32, cpos, emit);
-            ev = k < 4;
+        if (more & !tookq & (wi + kWin <= produced)) {
+            const int k = fsr_batch<kWin>(sc, [&](int j) { return rg[(wi + j) & (kRing - 1)][lane]; },
+                                         wi * 32, cpos, emit);
+            ev = k < kWin;
             wi += k;
         }
         quiet = !__any_sync(kFull, ev);

@@ -258,6 +258,10 @@ constexpr int kLim = 1 << 29;
 #define SPK_QUIET 8
 #endif
 constexpr int kQuiet = SPK_QUIET;
+// FSR event windows: words tested per iteration (fsr_batch, segment kernel)
+#ifndef SPK_WIN
+#define SPK_WIN 3
+#endif
 
 template <int METHOD>
 struct Scan {
@@ -521,78 +525,78 @@ struct FsrWord {
     }
 };
 
-// FSR over a window of four consecutive words (frames base0 .. base0+127; the
+// FSR over a window of N consecutive words (frames base0 .. base0+32N-1; the
 // first `cpos` frames of word 0 already consumed).  The FsrWord test is run on
-// all four words at once -- independent given the open run's pair, so they
+// all N words at once -- independent given the open run's pair, so they
 // overlap in the pipeline -- with each word's first remaining spike checked
 // against the last spike before it (in an earlier word of the window, or
 // sc.last).  The first word holding a violation decides: everything before
 // the violating spike is accepted in bulk and the spike itself goes through
-// the exact automaton.  Returns the number of words fully consumed (4 when no
+// the exact automaton.  Returns the number of words fully consumed (N when no
 // word of the window violates) and leaves `cpos` = frames consumed in the new
 // first word.  Words past the end of the stream must be passed as 0.
-template <class SC, class EMIT>
-SPK_HD int fsr_batch4(SC& sc, uint32_t W0, uint32_t W1, uint32_t W2, uint32_t W3, int base0,
-                      int& cpos, EMIT&& emit) {
+// word(j) returns word j of the window.
+template <int N, class SC, class WORD, class EMIT>
+SPK_HD int fsr_batch(SC& sc, WORD&& word, int base0, int& cpos, EMIT&& emit) {
     const int lo = sc.lo;
     const uint32_t hw = sc.hw;
-    // per-window constants: a second shift by lo when the pair is single
-    // (OR-idempotent, no select per word), the adjacency mask when lo >= 2
     const uint32_t sh1 = (uint32_t)lo, sh2 = (uint32_t)lo + hw;
-    const uint32_t sa = lo >= 2 ? 1u : 32u;  // adjacency test shift (32: off)
-    const uint32_t r0 = W0 & bit_shr_clamp(0xffffffffu, 0u, (uint32_t)cpos);
-    int pv = sc.last + lo;  // last spike before the word under test, plus lo
-    int p0v, p1v, p2v, p3v;
-    uint32_t V0, V1, V2, V3;
-    auto test = [&](uint32_t w, uint32_t r, int base, int& prev_out, uint32_t& V) {
-        prev_out = pv;
+    const uint32_t sa = lo >= 2 ? 1u : 32u;
+    int pv = sc.last + lo;
+    uint32_t R[N], V[N], c[N];
+    int PV[N];
+    uint32_t nz = 1u << N;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const uint32_t w = word(j);
+        const uint32_t r = j == 0 ? w & bit_shr_clamp(0xffffffffu, 0u, (uint32_t)cpos) : w;
+        const int base = base0 + 32 * j;
+        PV[j] = pv;
         const uint32_t Q = bit_shr_clamp(w, 0u, sh1) | bit_shr_clamp(w, 0u, sh2);
-        const int hi = bit_flo(r);  // r's first spike: frame base + 31 - hi
-        const uint32_t fb = bit_shl_clamp(1u, (uint32_t)hi);  // its bit (0 if none)
+        const int hi = bit_flo(r);
+        const uint32_t fb = bit_shl_clamp(1u, (uint32_t)hi);
         const uint32_t bad0 = (uint32_t)(base + 31 - hi - pv) > hw ? fb : 0u;
-        V = (r & ~(Q | fb)) | (r & w & bit_shr_clamp(w, 0u, sa)) | bad0;
-        // r's last spike is its lowest set bit: frame base + 32 - ffs(r)
+        V[j] = (r & ~(Q | fb)) | (r & w & bit_shr_clamp(w, 0u, sa)) | bad0;
         pv = bit_selp(r != 0u, base + lo + 32 - bit_ffs(r), pv);
-    };
-    test(W0, r0, base0, p0v, V0);
-    test(W1, W1, base0 + 32, p1v, V1);
-    test(W2, W2, base0 + 64, p2v, V2);
-    test(W3, W3, base0 + 96, p3v, V3);
-    const uint32_t c0 = (uint32_t)bit_popc(r0), c1 = (uint32_t)bit_popc(W1);
-    const uint32_t c2 = (uint32_t)bit_popc(W2), c3 = (uint32_t)bit_popc(W3);
-    const uint32_t nz = (uint32_t)(V0 != 0u) | (uint32_t)(V1 != 0u) << 1 |
-                        (uint32_t)(V2 != 0u) << 2 | (uint32_t)(V3 != 0u) << 3 | 16u;
-    // first violating word; with none, word 3 is taken whole (Vk = 0 -> p = 32)
+        R[j] = r;
+        c[j] = (uint32_t)bit_popc(r);
+        nz |= (uint32_t)(V[j] != 0u) << j;
+    }
     const int k = bit_ffs(nz) - 1;
-    const bool ev = k < 4;
-    const int kk = ev ? k : 3;
-    const bool s0 = kk == 0, s1 = kk == 1, s2 = kk == 2;
-    const uint32_t Vk = bit_sel(s0, V0, bit_sel(s1, V1, bit_sel(s2, V2, V3)));
-    const uint32_t rk = bit_sel(s0, r0, bit_sel(s1, W1, bit_sel(s2, W2, W3)));
-    const int prevk = -lo + (int)bit_sel(s0, (uint32_t)p0v,
-                                        bit_sel(s1, (uint32_t)p1v, bit_sel(s2, (uint32_t)p2v, (uint32_t)p3v)));
-    const uint32_t before = bit_sel(kk > 0, c0, 0u) + bit_sel(kk > 1, c1, 0u) + bit_sel(kk > 2, c2, 0u);
+    const bool ev = k < N;
+    const int kk = ev ? k : N - 1;
+    uint32_t Vk = V[0], rk = R[0], before = 0u;
+    int prevk = PV[0];
+#pragma unroll
+    for (int j = 1; j < N; ++j) {
+        const bool sj = kk >= j;
+        Vk = sj ? V[j] : Vk;
+        rk = sj ? R[j] : rk;
+        prevk = sj ? PV[j] : prevk;
+        before += sj ? c[j - 1] : 0u;
+    }
+    prevk -= lo;
     const int basek = base0 + 32 * kk;
     const int p = bit_clz(Vk);
     const uint32_t A = rk & ~bit_shr_clamp(0xffffffffu, 0u, (uint32_t)p);
     sc.cnt += (int)(before + (uint32_t)bit_popc(A));
     sc.last = A ? basek + 32 - bit_ffs(A) : prevk;
     cpos = ev ? p + 1 : 0;
-    if (ev) {  // the violating spike through the exact automaton
+    if (ev) {
         int rs, cnt;
         const bool e = sc.step(basek + p, rs, cnt);
         emit(e, rs, cnt);
     }
-    return ev ? kk : 4;
+    return ev ? kk : N;
 }
 
 // FSR over N consecutive words when the window holds no event at all: the
-// fsr_batch4 test on every word (each word's first remaining spike against
+// fsr_batch test on every word (each word's first remaining spike against
 // the last spike before it), OR-ed.  With no violation anywhere the whole
 // window is accepted at once (cnt += spikes, last = the latest spike,
 // cpos = 0) and true is returned; otherwise nothing changes and the caller
-// takes the exact fsr_batch4 path.  No selection across words is needed, so
-// a quiet window costs about half a 4-word batch per word (static scenes,
+// takes the exact fsr_batch path.  No selection across words is needed, so
+// a quiet window costs about half a window test per word (static scenes,
 // long streams).  word(k) returns word k of the window; words past the end
 // of the stream must read as 0.
 //

@@ -149,7 +149,7 @@ extern "C" long ssrword_runs(const uint8_t* bits, long frames, int method, long*
     return word_runs_impl(bits, frames, method, start, end, cnt, cap, true);
 }
 
-// The FSR 4-word window driver of the segment kernel (fsr_batch4).
+// The FSR window driver of the segment kernel (fsr_batch<SPK_WIN>).
 extern "C" long batch_runs(const uint8_t* bits, long frames, int method, long* start, long* end,
                            long* cnt, long cap) {
     if (method != 0) return word_runs(bits, frames, method, start, end, cnt, cap);
@@ -175,8 +175,7 @@ extern "C" long batch_runs(const uint8_t* bits, long frames, int method, long* s
     long wi = 0;
     int cpos = 0;
     while (wi < ngroups)
-        wi += spk::fsr_batch4(sc, words[wi], words[wi + 1], words[wi + 2], words[wi + 3],
-                              (int)(wi * 32), cpos, put);
+        wi += spk::fsr_batch<SPK_WIN>(sc, [&](int j) { return words[wi + j]; }, (int)(wi * 32), cpos, put);
     int rs, c;
     const bool e = sc.tail(rs, c);
     put(e, rs, c);
@@ -186,7 +185,7 @@ extern "C" long batch_runs(const uint8_t* bits, long frames, int method, long* s
 
 // The FSR driver of the segment kernel with quiet windows: after an
 // iteration without an event, kQuiet words are tried at once (fsr_quiet),
-// and the 4-word batch runs when they hold an event.
+// and the event window (fsr_batch) runs when they hold an event.
 extern "C" long quiet_runs(const uint8_t* bits, long frames, int method, long* start, long* end,
                            long* cnt, long cap) {
     if (method != 0) return word_runs(bits, frames, method, start, end, cnt, cap);
@@ -218,9 +217,8 @@ extern "C" long quiet_runs(const uint8_t* bits, long frames, int method, long* s
             wi += spk::kQuiet;
             continue;
         }
-        const int k = spk::fsr_batch4(sc, words[wi], words[wi + 1], words[wi + 2], words[wi + 3],
-                                      (int)(wi * 32), cpos, put);
-        quiet = k == 4;
+        const int k = spk::fsr_batch<SPK_WIN>(sc, [&](int j) { return words[wi + j]; }, (int)(wi * 32), cpos, put);
+        quiet = k == SPK_WIN;
         wi += k;
     }
     int rs, c;
@@ -235,7 +233,7 @@ extern "C" void host_run_u8(const uint32_t* n, const uint32_t* span, uint32_t* o
     for (long i = 0; i < m; ++i) out[i] = spk::run_u8(n[i], span[i]);
 }
 
-// profiling aid: fsr_batch4 iterations and events (exact steps) for one pixel
+// profiling aid: fsr_batch iterations and events (exact steps) for one pixel
 extern "C" void batch_iters(const uint8_t* bits, long frames, long* iters, long* events) {
     const long ngroups = (frames + 31) / 32;
     std::vector<uint32_t> words(ngroups + 4, 0u);
@@ -247,8 +245,7 @@ extern "C" void batch_iters(const uint8_t* bits, long frames, long* iters, long*
     int cpos = 0;
     auto put = [&](bool, int, int) {};
     while (wi < ngroups) {
-        const int k = spk::fsr_batch4(sc, words[wi], words[wi + 1], words[wi + 2], words[wi + 3],
-                                      (int)(wi * 32), cpos, put);
+        const int k = spk::fsr_batch<SPK_WIN>(sc, [&](int j) { return words[wi + j]; }, (int)(wi * 32), cpos, put);
         ev += cpos != 0;
         wi += k;
         ++it;
