@@ -580,7 +580,7 @@ SPK_HD int fsr_batch(SC& sc, WORD&& word, int base0, int& cpos, EMIT&& emit) {
     const int p = bit_clz(Vk);
     const uint32_t A = rk & ~bit_shr_clamp(0xffffffffu, 0u, (uint32_t)p);
     sc.cnt += (int)(before + (uint32_t)bit_popc(A));
-    sc.last = A ? basek + 32 - bit_ffs(A) : prevk;
+    sc.last = bit_selp(A != 0u, basek + 32 - bit_ffs(A), prevk);
     cpos = ev ? p + 1 : 0;
     if (ev) {
         int rs, cnt;
