@@ -309,10 +309,10 @@ struct ExpSmem {
     static constexpr int per_warp = kSub * 32 * (DE + BE);
 };
 
-size_t expand_smem_bytes(int out_size) {
-    return out_size == 1 ? (size_t)ExpSmem<uint8_t>::per_warp * Geo<uint8_t>::WARPS
-         : out_size == 4 ? (size_t)ExpSmem<float>::per_warp * Geo<float>::WARPS
-                         : (size_t)ExpSmem<double>::per_warp * Geo<double>::WARPS;
+size_t expand_smem_bytes(int out_size, int warps) {
+    return (size_t)warps * (out_size == 1 ? ExpSmem<uint8_t>::per_warp
+                          : out_size == 4 ? ExpSmem<float>::per_warp
+                                          : ExpSmem<double>::per_warp);
 }
 
 // Mask bit of pixel i of a lane: for uint8 output (4 pixels per 32-bit word)
@@ -326,8 +326,8 @@ __device__ __forceinline__ uint32_t pend_bit(int i) {
         return 1u << i;
 }
 
-template <typename OUT>
-__global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
+template <typename OUT, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_expand(ExpArgs a) {
     using G = ExpSmem<OUT>;
     constexpr int P = G::P;
     constexpr int GP = 32 * P;
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
     unsigned char* D = sm + (size_t)warp * G::per_warp;
     uint32_t* B = reinterpret_cast<uint32_t*>(D + kSub * 32 * G::DE);
 
-    const int g = blockIdx.x * Geo<OUT>::WARPS + warp;
+    const int g = blockIdx.x * WARPS + warp;
     // tile = (group, chunk, piece of kPieceSubs sub-tiles): blocks of one
     // piece row run together, so the rows being written at any time stay
     // within a narrow band of frames (DRAM page locality: 64-row tiles write
@@ -555,9 +555,10 @@ __global__ void __launch_bounds__(Geo<OUT>::WARPS * 32) k_expand(ExpArgs a) {
     }
 }
 
-template __global__ void k_expand<uint8_t>(ExpArgs);
-template __global__ void k_expand<float>(ExpArgs);
-template __global__ void k_expand<double>(ExpArgs);
+template __global__ void k_expand<uint8_t, Geo<uint8_t>::WARPS>(ExpArgs);
+template __global__ void k_expand<uint8_t, 2 * Geo<uint8_t>::WARPS>(ExpArgs);
+template __global__ void k_expand<float, Geo<float>::WARPS>(ExpArgs);
+template __global__ void k_expand<double, Geo<double>::WARPS>(ExpArgs);
 
 // ----------------------------------------------------------------- scan --
 // Exclusive prefix sum of uint32 counts (three launches: block scans, scan

@@ -165,21 +165,22 @@ constexpr int kPieces = kBins / kPieceSubs;  // K3 tiles per (group, chunk)
 #ifndef SPK_PIECE_SPARSE  // (build-time overrides: A/B probes)
 #define SPK_PIECE_SPARSE 2
 #endif
-#ifndef SPK_EXP_WARPS
-#define SPK_EXP_WARPS 4
-#endif
 constexpr int kPieceSparse = SPK_PIECE_SPARSE;  // changes per pixel per chunk up to which
                                              // K3 tiles are 64 frames high (else 128)
 constexpr int kPieceDensity = 12;            // ... up to which 128 frames high (else 256)
 constexpr int kPieceDense = 48;              // ... above which K3 writes the chunk whole
-constexpr int kPieceMaxGroups = 512;         // pieces only for narrow frames (few groups
+#ifndef SPK_PIECE_MAXG
+#define SPK_PIECE_MAXG 512
+#endif
+constexpr int kPieceMaxGroups = SPK_PIECE_MAXG;
+constexpr int kWideGroups = 1024;  // K3: 8-warp blocks from this many groups per frame  // pieces only for narrow frames (few groups
                                              // per row: wide rows already keep the
                                              // concurrently written rows close)
 template <typename OUT>
 struct Geo;
 template <>
 struct Geo<uint8_t> {
-    static constexpr int P = 16, WARPS = SPK_EXP_WARPS;
+    static constexpr int P = 16, WARPS = 4;  // (8 for wide sensors: k_expand<uint8_t, 8>)
 };
 template <>
 struct Geo<float> {
@@ -316,9 +317,9 @@ template <int GP, bool SPLIT>
 __global__ void k_fin_bins(FinArgs a);
 template <typename OUT, bool SPLIT>
 __global__ void k_fin_scatter(FinArgs a);
-template <typename OUT>
+template <typename OUT, int WARPS>
 __global__ void k_expand(ExpArgs a);
-size_t expand_smem_bytes(int out_size);  // dynamic shared memory of k_expand<OUT>
+size_t expand_smem_bytes(int out_size, int warps);  // dynamic shared memory of k_expand<OUT, warps>
 // exclusive scan of uint32 counts into T (uint32_t, or unsigned long long
 // where totals may pass 2^32)
 template <typename T>
