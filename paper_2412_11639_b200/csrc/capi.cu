@@ -6,6 +6,7 @@
 // streams), and every kernel launch is counted for the benchmark's
 // `gpu_launches` claim.  There is no CPU fallback: every path launches the
 // sm_100a kernels or returns an error.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -13,6 +14,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 #include <thread>
 #include <vector>
@@ -174,6 +176,41 @@ int launch_scan(const uint32_t* in, T* out, int64_t n, cudaStream_t s, T* out2 =
     return SPK_OK;
 }
 
+// TMA tile stores of K3: the frames as a 2-D uint32 tensor (W*H/4 columns,
+// `frames` rows, `pitch_bytes` apart), box 128 columns (512 B) x `rows`.
+// cuTensorMapEncodeTiled through the runtime's driver entry point.
+// Opt-in (SPK_TMA=1): measured on B200 the same as the per-lane stores --
+// K3 is bound by its change handling, not by the store path (C2 K3 0.726 vs
+// 0.718 ms, C3 3.615 vs 3.625 ms; profiles/r02/walk_experiments.md).
+bool tma_enabled() {
+    const char* v = std::getenv("SPK_TMA");
+    return v && *v && *v != '0';
+}
+
+bool encode_out_map(CUtensorMap* m, const void* out, int64_t npix, int64_t frames, size_t pitch_bytes,
+                    int rows) {
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                CUtensorMapFloatOOBfill);
+    static Encode enc = []() -> Encode {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return reinterpret_cast<Encode>(f);
+    }();
+    if (!enc || frames < 1 || npix < 4 || pitch_bytes % 16 != 0 || (reinterpret_cast<uintptr_t>(out) & 15))
+        return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)(npix / 4), (cuuint64_t)frames};
+    const cuuint64_t strides[1] = {(cuuint64_t)pitch_bytes};
+    const cuuint32_t box[2] = {128u, (cuuint32_t)rows}, es[2] = {1u, 1u};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(out), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // workspaces of the expand stage (allocated before K2, which fills `bins`)
 template <typename OUT>
 struct ExpandWork {
@@ -263,10 +300,24 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     const bool wide = sizeof(OUT) == 1 && w.ngroups >= kWideGroups;
     const int warps = wide ? 2 * Geo<OUT>::WARPS : Geo<OUT>::WARPS;
     const unsigned bx = (unsigned)((w.ngroups + warps - 1) / warps);
-    const size_t smem = expand_smem_bytes(sizeof(OUT), warps);
-    void (*kexp)(ExpArgs) = k_expand<OUT, Geo<OUT>::WARPS>;
-    if constexpr (sizeof(OUT) == 1)
-        if (wide) kexp = k_expand<OUT, 2 * Geo<OUT>::WARPS>;
+    // uint8 frames can leave K3 as TMA tensor stores of whole sub-tiles (one
+    // cp.async.bulk.tensor per kSub rows x 512 B; SPK_TMA=1): the write probe
+    // (profiles/tma_write.cu) gives 7.3 TB/s for K3's 128-row tiles against
+    // 6.5 with per-lane 16-B stores, but inside K3 the two measure the same.
+    // Needs 16-B aligned rows and W*H a multiple of 4 (the map's uint32
+    // columns end at the last pixel).
+    CUtensorMap tmap;
+    std::memset(&tmap, 0, sizeof(tmap));
+    const bool tma = sizeof(OUT) == 1 && e.vec_ok && sa.npix % 4 == 0 && tma_enabled() &&
+                     encode_out_map(&tmap, out, sa.npix, sa.frames, out_pitch * sizeof(OUT), kSub);
+    const size_t smem = expand_smem_bytes(sizeof(OUT), warps, tma);
+    void (*kexp)(ExpArgs, const CUtensorMap) = k_expand<OUT, Geo<OUT>::WARPS, false>;
+    if constexpr (sizeof(OUT) == 1) {
+        if (tma)
+            kexp = wide ? k_expand<OUT, 2 * Geo<OUT>::WARPS, true> : k_expand<OUT, Geo<OUT>::WARPS, true>;
+        else if (wide)
+            kexp = k_expand<OUT, 2 * Geo<OUT>::WARPS, false>;
+    }
     if (smem > 48 * 1024)
         SPK_CK(cudaFuncSetAttribute(kexp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     e.pieces = w.ngroups <= kPieceMaxGroups ? kPieces : 1;
@@ -274,7 +325,7 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     for (int c0 = 0; c0 < sa.nchunks; c0 += per_launch) {
         e.chunk0 = c0;
         const unsigned by = (unsigned)(std::min(per_launch, sa.nchunks - c0) * e.pieces);
-        kexp<<<dim3(bx, by), warps * 32, smem, s>>>(e);
+        kexp<<<dim3(bx, by), warps * 32, smem, s>>>(e, tmap);
         SPK_LAUNCHED("k_expand");
     }
     return SPK_OK;

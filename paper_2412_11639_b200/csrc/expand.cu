@@ -26,7 +26,13 @@
 //       (16 B for u8: a warp writes 512 contiguous bytes of a frame row).
 #include <climits>
 
+#include <cuda.h>
+
 #include "spk_common.cuh"
+
+#ifndef SPK_TMA_BUFS
+#define SPK_TMA_BUFS 1  // staging buffers per warp (1: 10 KB per warp, 5 blocks per SM)
+#endif
 #include "spk_kernels.cuh"
 
 namespace spk {
@@ -307,9 +313,13 @@ struct ExpSmem {
     static constexpr int DE = P * (int)sizeof(OUT);  // D cell bytes
     static constexpr int BE = 4;                       // B cell bytes
     static constexpr int per_warp = kSub * 32 * (DE + BE);
+    // TMA stores (uint8): two D buffers -- the merged frames are written back
+    // into the cells, and the sub-tile leaves as one tensor store -- + B
+    static constexpr int per_warp_tma = SPK_TMA_BUFS * kSub * 32 * DE + kSub * 32 * BE;
 };
 
-size_t expand_smem_bytes(int out_size, int warps) {
+size_t expand_smem_bytes(int out_size, int warps, bool tma) {
+    if (tma) return (size_t)warps * ExpSmem<uint8_t>::per_warp_tma;
     return (size_t)warps * (out_size == 1 ? ExpSmem<uint8_t>::per_warp
                           : out_size == 4 ? ExpSmem<float>::per_warp
                                           : ExpSmem<double>::per_warp);
@@ -326,18 +336,21 @@ __device__ __forceinline__ uint32_t pend_bit(int i) {
         return 1u << i;
 }
 
-template <typename OUT, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_expand(ExpArgs a) {
+template <typename OUT, int WARPS, bool TMA>
+__global__ void __launch_bounds__(WARPS * 32) k_expand(ExpArgs a, const __grid_constant__ CUtensorMap tmap) {
     using G = ExpSmem<OUT>;
+    static_assert(!TMA || sizeof(OUT) == 1, "TMA tile stores: uint8 frames");
     constexpr int P = G::P;
     constexpr int GP = 32 * P;
     constexpr int NW = P * (int)sizeof(OUT) / 4;  // 32-bit words per lane-frame
     constexpr int NV = NW / 4;                     // 16-B vectors per lane-frame
-    extern __shared__ __align__(16) unsigned char sm[];
+    constexpr int DBYTES = kSub * 32 * G::DE;      // one D buffer: kSub rows x 32 lanes
+    extern __shared__ __align__(128) unsigned char sm[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    unsigned char* D = sm + (size_t)warp * G::per_warp;
-    uint32_t* B = reinterpret_cast<uint32_t*>(D + kSub * 32 * G::DE);
+    unsigned char* const D0 = sm + (size_t)warp * (TMA ? G::per_warp_tma : G::per_warp);
+    unsigned char* D = D0;  // (TMA: the buffer of the current sub-tile, D0 or D0 + DBYTES)
+    uint32_t* B = reinterpret_cast<uint32_t*>(D0 + (TMA ? SPK_TMA_BUFS : 1) * DBYTES);
 
     const int g = blockIdx.x * WARPS + warp;
     // tile = (group, chunk, piece of kPieceSubs sub-tiles): blocks of one
@@ -486,9 +499,20 @@ __global__ void __launch_bounds__(WARPS * 32) k_expand(ExpArgs a) {
         atomicOr(&B[fs * 32 + own], pend_bit<OUT>(i));
     };
 
+    int tma_pending = 0;  // TMA: tile stores issued (the buffer alternates)
     for (int sub = sub0; sub < sub1; ++sub) {
         const int t0 = fc + sub * kSub;
         if (t0 >= f1) break;
+        if constexpr (TMA) {
+            D = D0 + (tma_pending % SPK_TMA_BUFS) * DBYTES;
+            if (tma_pending >= SPK_TMA_BUFS && lane == 0) {  // the store that last read this buffer is done reading
+                if (SPK_TMA_BUFS == 1)
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                else
+                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            }
+            __syncwarp();
+        }
         // ---- phase A: this sub-tile's changes -> owners' buckets
         uint32_t noff = 0, nn = 0;
         if (sub + 1 < sub1) bin_of(sub + 1, noff, nn);
@@ -530,7 +554,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_expand(ExpArgs a) {
                     }
                 }
             }
-            if (vec_ok) {
+            if constexpr (TMA) {  // the merged frame back into its cell (row fs of the tile)
+                *reinterpret_cast<uint4*>(D + (fs * 32 + lane) * G::DE) =
+                    make_uint4(words[0], words[1], words[2], words[3]);
+            } else if (vec_ok) {
 #pragma unroll
                 for (int k = 0; k < NV; ++k)
                     st_v4(ptr + 16 * k, make_uint4(words[4 * k], words[4 * k + 1], words[4 * k + 2],
@@ -551,14 +578,33 @@ __global__ void __launch_bounds__(WARPS * 32) k_expand(ExpArgs a) {
             }
             ptr += step;
         }
+        if constexpr (TMA) {
+            // the sub-tile (kSub rows x 512 B) as one tensor store; rows past
+            // the stream end and columns past the last pixel are clipped
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t sa = (uint32_t)__cvta_generic_to_shared(D);
+                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                             ::"l"(&tmap), "r"(g * (GP / 4)), "r"(t0), "r"(sa) : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            ++tma_pending;
+        }
         __syncwarp();  // bucket clears done before the next phase A refills them
+    }
+    if constexpr (TMA) {
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
     }
 }
 
-template __global__ void k_expand<uint8_t, Geo<uint8_t>::WARPS>(ExpArgs);
-template __global__ void k_expand<uint8_t, 2 * Geo<uint8_t>::WARPS>(ExpArgs);
-template __global__ void k_expand<float, Geo<float>::WARPS>(ExpArgs);
-template __global__ void k_expand<double, Geo<double>::WARPS>(ExpArgs);
+template __global__ void k_expand<uint8_t, Geo<uint8_t>::WARPS, false>(ExpArgs, const __grid_constant__ CUtensorMap);
+template __global__ void k_expand<uint8_t, 2 * Geo<uint8_t>::WARPS, false>(ExpArgs, const __grid_constant__ CUtensorMap);
+template __global__ void k_expand<uint8_t, Geo<uint8_t>::WARPS, true>(ExpArgs, const __grid_constant__ CUtensorMap);
+template __global__ void k_expand<uint8_t, 2 * Geo<uint8_t>::WARPS, true>(ExpArgs, const __grid_constant__ CUtensorMap);
+template __global__ void k_expand<float, Geo<float>::WARPS, false>(ExpArgs, const __grid_constant__ CUtensorMap);
+template __global__ void k_expand<double, Geo<double>::WARPS, false>(ExpArgs, const __grid_constant__ CUtensorMap);
 
 // ----------------------------------------------------------------- scan --
 // Exclusive prefix sum of uint32 counts (three launches: block scans, scan

@@ -5,6 +5,8 @@
 #include <cstddef>
 #include <cstdint>
 
+#include <cuda.h>
+
 #include "spikecam_b200.h"
 
 namespace spk {
@@ -158,9 +160,12 @@ struct SplitArgs {
 // Geometry of the expand stage per output type: a warp owns a group of
 // GP = 32*P consecutive pixels (P per lane) and walks one kChunk-frame chunk
 // in sub-tiles of kSub frames (kBins sub-tiles per chunk).
-constexpr int kSub = 16;
+#ifndef SPK_SUB
+#define SPK_SUB 16
+#endif
+constexpr int kSub = SPK_SUB;
 constexpr int kBins = kChunk / kSub;
-constexpr int kPieceSubs = 4;                // K3 tile height: 64 frames
+constexpr int kPieceSubs = 64 / kSub;        // K3 tile height: 64 frames
 constexpr int kPieces = kBins / kPieceSubs;  // K3 tiles per (group, chunk)
 #ifndef SPK_PIECE_SPARSE  // (build-time overrides: A/B probes)
 #define SPK_PIECE_SPARSE 2
@@ -317,9 +322,9 @@ template <int GP, bool SPLIT>
 __global__ void k_fin_bins(FinArgs a);
 template <typename OUT, bool SPLIT>
 __global__ void k_fin_scatter(FinArgs a);
-template <typename OUT, int WARPS>
-__global__ void k_expand(ExpArgs a);
-size_t expand_smem_bytes(int out_size, int warps);  // dynamic shared memory of k_expand<OUT, warps>
+template <typename OUT, int WARPS, bool TMA>
+__global__ void k_expand(ExpArgs a, const __grid_constant__ CUtensorMap tmap);
+size_t expand_smem_bytes(int out_size, int warps, bool tma);  // dynamic shared memory of k_expand
 // exclusive scan of uint32 counts into T (uint32_t, or unsigned long long
 // where totals may pass 2^32)
 template <typename T>

@@ -373,3 +373,20 @@ def test_repeatability_under_concurrency():
             torch.cuda.synchronize()
             for k in range(3):
                 assert torch.equal(outs[k], ref[k].reshape(t, -1)), (m, rep, k)
+
+
+def test_k3_tma_store_path():
+    """K3's opt-in TMA tile-store path (SPK_TMA=1: one cp.async.bulk.tensor per
+    16-row sub-tile) writes exactly the frames of the per-lane store path --
+    partial last groups, a last sub-tile past the stream end, pieces."""
+    import os
+    for (w, h, t) in ((400, 25, 3000), (64, 48, 1037), (1000, 60, 2100)):
+        v = spk.synth("moving", 9, w, h, t)
+        for m in ("fsr", "ssr"):
+            ref = run(v, m).clone()
+            os.environ["SPK_TMA"] = "1"
+            try:
+                got = run(v, m)
+            finally:
+                del os.environ["SPK_TMA"]
+            assert torch.equal(got, ref), (w, h, t, m)
