@@ -325,6 +325,14 @@ size_t expand_smem_bytes(int out_size, int warps, bool tma) {
                                           : ExpSmem<double>::per_warp);
 }
 
+// each byte of x -> 0xff if its top bit is set, else 0 (PRMT with sign
+// replication; __byte_perm ignores the selector's replicate bit)
+__device__ __forceinline__ uint32_t sign_bytes(uint32_t x) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(r) : "r"(x));
+    return r;
+}
+
 // Mask bit of pixel i of a lane: for uint8 output (4 pixels per 32-bit word)
 // bit 8*(i&3) + (i>>2), so word w's byte mask is ((m >> w) & 0x01010101)*255;
 // otherwise bit i.
@@ -425,30 +433,41 @@ __global__ void __launch_bounds__(WARPS * 32) k_expand(ExpArgs a, const __grid_c
         __syncwarp();
         const uint32_t pb = __shfl_sync(kFull, off_lo, 0);
         const uint32_t pe = __shfl_sync(kFull, sub0 < 32 ? off_lo : off_hi, sub0 & 31);
-        for (uint32_t k = lane; k < pe - pb; k += 32) {
-            const Change<OUT> ch = st[pb + k];
-            uint32_t fo, pix;
+        // uint8: the key carries the value itself ((frame + 1) << 8 | value),
+        // so the winner needs no second load; wider values keep the index.
+        // Four changes per lane per pass (independent loads in flight).
+        auto take = [&](const Change<OUT>& ch, uint32_t k) {
             if constexpr (sizeof(OUT) == 1) {
-                fo = ch.w >> 17;
-                pix = (ch.w >> 8) & 0x1ffu;
+                const uint32_t fo = ch.w >> 17, pix = (ch.w >> 8) & 0x1ffu;
+                atomicMax(&K[pix], (fo + 1u) << 8 | (ch.w & 0xffu));
             } else {
-                fo = ch.key >> 16;
-                pix = ch.key & 0xffffu;
+                const uint32_t fo = ch.key >> 16, pix = ch.key & 0xffffu;
+                atomicMax(&K[pix], (fo + 1u) << 20 | k);  // k < 2^20: at most 512 x 1024 changes
             }
-            atomicMax(&K[pix], (fo + 1u) << 20 | k);  // k < 2^20: at most 512 x 1024 changes
+        };
+        const uint32_t np_ = pe - pb;
+        uint32_t k = lane;
+        for (; k + 96 < np_; k += 128) {
+            Change<OUT> c4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) c4[u] = st[pb + k + 32 * u];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) take(c4[u], k + 32 * u);
         }
+        for (; k < np_; k += 32) take(st[pb + k], k);
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < P; ++i) {
             const uint32_t key = K[lane * P + i];
             if (key) {
-                const Change<OUT> ch = st[pb + (key & 0xfffffu)];
                 if constexpr (sizeof(OUT) == 1) {
                     const int sh = (i & 3) * 8;
-                    words[i >> 2] = (words[i >> 2] & ~(0xffu << sh)) | ((ch.w & 0xffu) << sh);
+                    words[i >> 2] = (words[i >> 2] & ~(0xffu << sh)) | ((key & 0xffu) << sh);
                 } else if constexpr (sizeof(OUT) == 4) {
+                    const Change<OUT> ch = st[pb + (key & 0xfffffu)];
                     words[i] = ch.bits;
                 } else {
+                    const Change<OUT> ch = st[pb + (key & 0xfffffu)];
                     const unsigned long long bits = __double_as_longlong(ch.v);
                     words[2 * i] = (uint32_t)bits;
                     words[2 * i + 1] = (uint32_t)(bits >> 32);
@@ -534,8 +553,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_expand(ExpArgs a, const __grid_c
             if constexpr (sizeof(OUT) == 1) {  // branch-free: a clear mask keeps every byte
                 B[fs * 32 + lane] = 0u;
                 const uint4 dv = *reinterpret_cast<const uint4*>(D + (fs * 32 + lane) * G::DE);
-                const uint32_t m0 = (bm & 0x01010101u) * 0xffu, m1 = ((bm >> 1) & 0x01010101u) * 0xffu;
-                const uint32_t m2 = ((bm >> 2) & 0x01010101u) * 0xffu, m3 = ((bm >> 3) & 0x01010101u) * 0xffu;
+                // word w's pending bits sit at 8b + w: shifted to the byte
+                // sign bits, one PRMT replicates each into its byte
+                const uint32_t m0 = sign_bytes(bm << 7), m1 = sign_bytes(bm << 6);
+                const uint32_t m2 = sign_bytes(bm << 5), m3 = sign_bytes(bm << 4);
                 words[0] = (words[0] & ~m0) | (dv.x & m0);
                 words[1] = (words[1] & ~m1) | (dv.y & m1);
                 words[2] = (words[2] & ~m2) | (dv.z & m2);
