@@ -8,7 +8,12 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libspikecam_b200.so"
+import os
+
+# SPIKECAM_B200_LIB: another build of the library (the bounds-checked one,
+# build.build_checked(), for tests/test_checked_build.py)
+LIB_PATH = Path(os.environ.get("SPIKECAM_B200_LIB") or
+                Path(__file__).resolve().parent / "libspikecam_b200.so").resolve()
 
 SPK_OK, SPK_EINVAL, SPK_ECUDA, SPK_ENOMEM = 0, 1, 2, 3
 SPK_FSR, SPK_SSR, SPK_TFI, SPK_TFP = 0, 1, 2, 3

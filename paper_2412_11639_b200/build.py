@@ -15,6 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libspikecam_b200.so"
+CHECKED_LIB = PKG / "libspikecam_b200_checked.so"  # bounds-checked build (SPK_CHECK traps)
 CPP_LIB = PKG / "libspikecam_cpp.so"
 CXX = "/usr/bin/g++"  # the system compiler (the image's CC/CXX env may point elsewhere)
 
@@ -58,6 +59,23 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_checked(force: bool = False, verbose: bool = False) -> Path:
+    """The same library with the kernels' index invariants asserted
+    (-DSPK_CHECKED: SPK_CHECK traps).  compute-sanitizer is closed on the GPU
+    pool; tests/test_checked_build.py runs GPU tests against this build
+    (SPIKECAM_B200_LIB points the package at it)."""
+    deps = sources() + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "spikecam_b200.h"]
+    if not force and not _stale(CHECKED_LIB, deps):
+        return CHECKED_LIB
+    tmp = CHECKED_LIB.with_suffix(".so.tmp")
+    cmd = [nvcc(), *NVCC_FLAGS, "-DSPK_CHECKED", f"-I{ROOT / 'include'}", "-o", str(tmp), *map(str, sources())]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    tmp.replace(CHECKED_LIB)
+    return CHECKED_LIB
+
+
 def build_cpp(force: bool = False, verbose: bool = False) -> Path:
     """C++ drop-in (include/spikecam/b200.hpp) over the C-ABI: g++ only, linked
     against libspikecam_b200.so with an $ORIGIN rpath (no CUDA runtime of its own)."""
@@ -92,3 +110,4 @@ def build_cpp_program(src: Path, out: Path, verbose: bool = False) -> Path:
 if __name__ == "__main__":
     print(build_library(force=True, verbose=True))
     print(build_cpp(force=True, verbose=True))
+    print(build_checked(force=True, verbose=True))

@@ -254,6 +254,7 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     f.tblv = w.tblv.p;
     f.offs = static_cast<const uint32_t*>(w.offs.p);
     f.stream = w.stream.p;
+    f.stream_len = sa.npix * sa.cap;
     f.seg = sa.seg_in;
     f.nseg = sa.nseg;
     // few groups (narrow sensors): split each group's pixels over 4 blocks
@@ -287,6 +288,7 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     e.bins = static_cast<const uint32_t*>(w.bins.p);
     e.offs = f.offs;
     e.stream = w.stream.p;
+    e.stream_len = f.stream_len;
     e.npix = sa.npix;
     e.frames = sa.frames;
     e.nchunks = sa.nchunks;

@@ -211,7 +211,9 @@ __global__ void __launch_bounds__(256, sizeof(OUT) == 1 && !SPLIT ? SPK_K2C_MINB
                     const int st = max((int)r[j].start, 0);  // see K2b: starts before frame 0
                     const int c = st >> kChunkLog2;
                     const int bi = (st & (kChunk - 1)) / kSub;
+                    SPK_CHECK(c < a.nchunks);
                     pos[j] = atomicAdd(&a.cursor[((int64_t)c * a.ngroups + g) * kBins + bi], 1u);
+                    SPK_CHECK((int64_t)pos[j] < a.stream_len);
                 }
             }
 #pragma unroll
@@ -245,7 +247,9 @@ __global__ void __launch_bounds__(256, sizeof(OUT) == 1 && !SPLIT ? SPK_K2C_MINB
                     const int st = max((int)r[j].start, 0);  // see K2b: starts before frame 0
                     const int c = st >> kChunkLog2;
                     const int bi = (st & (kChunk - 1)) / kSub;
+                    SPK_CHECK(c < a.nchunks);
                     pos[j] = atomicAdd(&a.cursor[((int64_t)c * a.ngroups + g) * kBins + bi], 1u);
+                    SPK_CHECK((int64_t)pos[j] < a.stream_len);
                 }
             }
 #pragma unroll
@@ -410,6 +414,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_expand(ExpArgs a, const __grid_c
     const uint32_t off_lo = a.offs[b0 + lane], off_hi = a.offs[b0 + 32 + lane];
     const uint32_t cnt_lo = a.bins[b0 + lane], cnt_hi = a.bins[b0 + 32 + lane];
     const Change<OUT>* st = reinterpret_cast<const Change<OUT>*>(a.stream);
+    SPK_CHECK((int64_t)(off_hi + cnt_hi) <= a.stream_len);
     // Dense tiles (many changes per pixel in the chunk) are written whole by
     // the piece-0 warp: the piece prefix would re-read too many changes.
     // Tile height by the tile's change density: the denser, the longer the
@@ -439,6 +444,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_expand(ExpArgs a, const __grid_c
         auto take = [&](const Change<OUT>& ch, uint32_t k) {
             if constexpr (sizeof(OUT) == 1) {
                 const uint32_t fo = ch.w >> 17, pix = (ch.w >> 8) & 0x1ffu;
+                SPK_CHECK(fo < (uint32_t)(sub0 * kSub));  // a change of an earlier sub-tile
                 atomicMax(&K[pix], (fo + 1u) << 8 | (ch.w & 0xffu));
             } else {
                 const uint32_t fo = ch.key >> 16, pix = ch.key & 0xffffu;
@@ -507,6 +513,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_expand(ExpArgs a, const __grid_c
             pix = ch.key & 0xffffu;
         }
         const int fs = (int)fo - sub * kSub;  // frame within the sub-tile
+        SPK_CHECK((fs >= 0) & (fs < kSub) & (pix < (uint32_t)GP));
         const int own = (int)(pix / P), i = (int)(pix % P);
         unsigned char* dcell = D + (fs * 32 + own) * G::DE;
         if constexpr (sizeof(OUT) == 1)

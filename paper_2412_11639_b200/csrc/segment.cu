@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     // address arithmetic per emit); past the capacity nothing is stored
     spk_run_t* wp = rp;
     auto emit = [&](bool e, int rs, int cnt) {
+        SPK_CHECK(!e | (rs >= -(1 << 29)));  // a run start is a frame (time shards: may precede 0)
         o_rs = e ? rs + fbase : o_rs;
         o_cnt = e ? cnt : o_cnt;
         st_run_if(e & (nrun <= capm1), wp, o_rs, o_cnt);

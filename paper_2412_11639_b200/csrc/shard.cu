@@ -586,6 +586,7 @@ __global__ void __launch_bounds__(128) k_split_combine(SplitArgs a) {
         // the run open at the shard end continues in the next shard (it comes
         // back there as the entry run); the last shard keeps it
         if ((r < S - 1) & (X.lo < kLim) & (e > b)) --e;
+        SPK_CHECK((b >= (int64_t)r * a.rstride) & (b <= e) & (e <= (int64_t)(r + 1) * a.rstride));
         sg[2 * r] = (uint32_t)b;
         sg[2 * r + 1] = (uint32_t)e;
         total += (uint32_t)(e - b);

@@ -8,6 +8,21 @@ namespace spk {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Bounds checks of the checked build (-DSPK_CHECKED, build.build_checked():
+// compute-sanitizer is closed on the GPU pool, so the index invariants the
+// kernels rely on are asserted in a separate build the GPU tests run).  A
+// violated check traps the kernel (cudaErrorLaunchFailure).  Free otherwise.
+#ifdef SPK_CHECKED
+#define SPK_CHECK(cond)          \
+    do {                         \
+        if (!(cond)) __trap();   \
+    } while (0)
+#else
+#define SPK_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 // Frames per chunk: the expand kernel (K3) tiles time in chunks of kChunk
 // frames, and K2c records every pixel's value at each chunk start.
 constexpr int kChunkLog2 = 10;

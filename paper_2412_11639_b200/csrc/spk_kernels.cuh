@@ -232,6 +232,7 @@ struct FinArgs {
     const uint32_t* offs;  // exclusive prefix of bins
     uint32_t* cursor;      // K2c: running copy of offs (claimed with atomics)
     void* stream;          // Change<OUT>[total] (K2c)
+    int64_t stream_len = 0;  // its entries (checked build)
     // in-grid time split: runs of pixel p are the segments seg[p*nseg + r] =
     // {begin, end} of its row (runs + p*row); cap = row length.  null: one
     // contiguous list of min(counts[p], cap) runs.
@@ -247,6 +248,7 @@ struct ExpArgs {
     const uint32_t* bins;
     const uint32_t* offs;
     const void* stream;
+    int64_t stream_len = 0;  // entries of `stream` (checked build)
     int64_t npix;
     int frames;
     int nchunks;
