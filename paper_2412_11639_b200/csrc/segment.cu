@@ -21,6 +21,10 @@
 // for K3; overflowed pixels are rewritten exactly by k_fixup after K3.
 #include <type_traits>
 
+#ifndef SPK_SSR_REPS
+#define SPK_SSR_REPS 3  // SSR bulk mode: words (or events) per pass of its loop head (3: C3 SSR -1% vs 2)
+#endif
+
 #include "spk_fsm.cuh"
 #include "spk_kernels.cuh"
 
@@ -175,9 +179,9 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
                     if (produced < ngroups && produced + kBatch <= lowest + kRing) produce(lowest);
                 }
                 if (!__any_sync(kFull, (S != 0u) | more)) break;
-                // two words (or events) per pass of the loop head (four: C3 slower)
+                // SPK_SSR_REPS words (or events) per pass of the loop head
 #pragma unroll
-                for (int rep = 0; rep < 2; ++rep) {
+                for (int rep = 0; rep < SPK_SSR_REPS; ++rep) {
                     if ((S == 0u) & (wi + 1 < produced) & (wi + 1 < limit)) {
                         ++wi;
                         So = S = rg[wi & (kRing - 1)][lane];
