@@ -260,9 +260,10 @@ __global__ void __launch_bounds__(256, sizeof(OUT) == 1 && !SPLIT ? SPK_K2C_MINB
                     const OUT val = over ? OUT(0) : OutVal<OUT>::run(r[j].intervals, r[j + 1].start - r[j].start);
                     stp[pos[j]] = make_change<OUT>(fo, pl, val);
                     if (!over) {  // chunk starts in [start, next start); the last run covers the tail
-                        const int64_t hi = k0 + j + 1 < n ? (int64_t)(int)r[j + 1].start : total_frames;
-                        for (int64_t cc = ((int64_t)st + kChunk - 1) >> kChunkLog2; cc <= (hi - 1) >> kChunkLog2; ++cc)
-                            tb[cc * a.npix + p] = val;
+                        // (frames < 2^29: 32-bit arithmetic; most runs cover no chunk start)
+                        const int hi = k0 + j + 1 < n ? (int)r[j + 1].start : (int)total_frames;
+                        for (int cc = (st + kChunk - 1) >> kChunkLog2; cc <= (hi - 1) >> kChunkLog2; ++cc)
+                            tb[(int64_t)cc * a.npix + p] = val;
                     }
                 }
             }

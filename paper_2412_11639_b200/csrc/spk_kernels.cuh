@@ -21,7 +21,10 @@ using spk_stab_t = ::spk_stab;
 // the warps share each sector through L2, so they are kept within a drift
 // bound (kDriftFsr / kDriftSsr groups) of each other (otherwise every 4-byte load pulls its own sector from
 // DRAM on long streams)
-constexpr int kSegThreads = 256;
+#ifndef SPK_SEG_THREADS
+#define SPK_SEG_THREADS 256
+#endif
+constexpr int kSegThreads = SPK_SEG_THREADS;
 constexpr int kSegWarps = kSegThreads / 32;
 // max groups a warp may produce ahead of its block's slowest warp, per
 // method (measured: FSR 48 vs 96 -- C5 K2 -3%, C3 -2%; SSR 160 vs 96 --

@@ -123,6 +123,19 @@ def test_run_u8_exact_vs_integer_rule(fsm):
     # and equals quantize() of the reference double
     v = 255.0 * n.astype(np.float64) / span.astype(np.float64)
     assert np.array_equal(out, np.floor(np.clip(v, 0, 255) + 0.5).astype(np.uint32))
+    # every (N, span) with span <= 1536, and spans around the fast path's 2^22 limit
+    sp = np.repeat(np.arange(1, 1537, dtype=np.uint32), 1537)
+    nn = np.tile(np.arange(0, 1537, dtype=np.uint32), 1536)
+    keep = nn <= sp
+    sp, nn = sp[keep], nn[keep]
+    edge = rng.integers((1 << 22) - 4000, (1 << 22) + 4000, 100000).astype(np.uint32)
+    sp = np.concatenate([sp, edge])
+    nn = np.concatenate([nn, (rng.random(edge.size) * (edge + 1.0)).astype(np.uint32)])
+    nn = np.minimum(nn, sp)
+    out = np.zeros(sp.size, np.uint32)
+    h.host_run_u8(nn.ctypes.data, sp.ctypes.data, out.ctypes.data, sp.size)
+    want = (510 * nn.astype(np.uint64) + sp) // (2 * sp.astype(np.uint64))
+    assert np.array_equal(out, want.astype(np.uint32))
 
 
 @pytest.mark.parametrize("kind", ["batch", "quiet", "ssrword"])
