@@ -273,7 +273,8 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     f.cursor = static_cast<uint32_t*>(w.cursor.p);
     // threads stride over a pixel's kFinSeg-run blocks (grid.y <= 64: a
     // 1M-frame list of one run per pixel is not 500 block rows of exits)
-    const int nseg = (sa.cap + kFinSeg - 1) / kFinSeg;
+    f.fin_seg = fin_seg_for(sa.npix);
+    const int nseg = (sa.cap + f.fin_seg - 1) / f.fin_seg;
     static const int maxy = (int)test_limit("SPK_TEST_GRID_Y", 64);
     const dim3 grid((unsigned)((sa.npix + 255) / 256), (unsigned)std::min(maxy, nseg));
     if (f.seg)

@@ -169,7 +169,7 @@ __device__ __forceinline__ Change<OUT> make_change(uint32_t fo, uint32_t pl, OUT
 #define SPK_K2C_MINB 4  // uint8 lists: 64 registers, more warps in flight (C2 finalize 0.411 -> 0.398 ms)
 #endif
 #ifndef SPK_K2C_B
-#define SPK_K2C_B 8
+#define SPK_K2C_B 4
 #endif
 template <typename OUT, bool SPLIT>
 __global__ void __launch_bounds__(256, sizeof(OUT) == 1 && !SPLIT ? SPK_K2C_MINB : 1) k_fin_scatter(FinArgs a) {
@@ -181,15 +181,15 @@ __global__ void __launch_bounds__(256, sizeof(OUT) == 1 && !SPLIT ? SPK_K2C_MINB
     const uint32_t pl = (uint32_t)(p % GP);
     const uint32_t cnt = a.counts[p];
     const bool over = cnt > (uint32_t)a.cap;  // k_fixup rewrites it: values don't matter
-    // blockIdx.y: this thread's block of kFinSeg list slots (runs are
+    // blockIdx.y: this thread's block of a.fin_seg list slots (runs are
     // independent here -- a value needs only the next run's start -- so a
     // pixel's list is spread over several threads: enough loads and atomics
     // in flight even for sensors with few pixels)
     // (split lists: the same numbering over the row's segments in order)
-    // blocks of kFinSeg list entries, strided over gridDim.y (a long list
+    // blocks of a.fin_seg list entries, strided over gridDim.y (a long list
     // with few runs per pixel does not launch a block row per capacity block)
     const int n = (int)min(cnt, (uint32_t)a.cap);
-    if ((int)blockIdx.y * kFinSeg >= n) return;
+    if ((int)blockIdx.y * a.fin_seg >= n) return;
     const spk_run_t* rp = a.runs + p * a.cap;
     const uint32_t lastp = (uint32_t)a.last[p];
     Change<OUT>* stp = reinterpret_cast<Change<OUT>*>(a.stream);
@@ -232,14 +232,46 @@ __global__ void __launch_bounds__(256, sizeof(OUT) == 1 && !SPLIT ? SPK_K2C_MINB
             }
         }
     };
-    for (int kb = (int)blockIdx.y * kFinSeg; kb < n; kb += (int)gridDim.y * kFinSeg) {
-    const int ke = min(n, kb + kFinSeg);
+    // 16-byte run loads: the list base and every batch start (a multiple of B) are 16-byte aligned
+#ifndef SPK_K2C_VEC
+#define SPK_K2C_VEC 1
+#endif
+    const bool vec = (SPK_K2C_VEC != 0) & (B % 2 == 0) & ((a.cap & 1) == 0) &
+                     ((reinterpret_cast<uintptr_t>(a.runs) & 15) == 0);
+    for (int kb = (int)blockIdx.y * a.fin_seg; kb < n; kb += (int)gridDim.y * a.fin_seg) {
+    const int ke = min(n, kb + a.fin_seg);
     if constexpr (!SPLIT) {  // one contiguous list
-        for (int k0 = kb; k0 < ke; k0 += B) {
-            spk_run_t r[B + 1];
+        // Software pipeline: the loads of batch k0 + B are issued before the
+        // atomics and stores of batch k0 (the thread is bound by the latency
+        // of its run loads: ncu long-scoreboard at their first use).  Batch
+        // slots past the list hold the sentinel run {next start, 0}.
+        auto load_batch = [&](int k0, spk_run_t (&r)[B]) {
+            if (vec) {
+                // (every per-lane load is its own 128-byte line: two runs per 16-byte load)
 #pragma unroll
-            for (int j = 0; j <= B; ++j)
-                r[j] = k0 + j < n ? rp[k0 + j] : spk_run_t{k0 + j == n ? lastp : 0x7fffffffu, 0u};
+                for (int j = 0; j < B; j += 2) {
+                    if (k0 + j + 1 < n) {
+                        const uint4 v = *reinterpret_cast<const uint4*>(rp + k0 + j);
+                        r[j] = spk_run_t{v.x, v.y};
+                        r[j + 1] = spk_run_t{v.z, v.w};
+                    } else {
+                        r[j] = k0 + j < n ? rp[k0 + j] : spk_run_t{k0 + j == n ? lastp : 0x7fffffffu, 0u};
+                        r[j + 1] = spk_run_t{k0 + j + 1 == n ? lastp : 0x7fffffffu, 0u};
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < B; ++j)
+                    r[j] = k0 + j < n ? rp[k0 + j] : spk_run_t{k0 + j == n ? lastp : 0x7fffffffu, 0u};
+            }
+        };
+        spk_run_t r[B + 1], nx[B];
+        load_batch(kb, nx);
+        for (int k0 = kb; k0 < ke; k0 += B) {
+#pragma unroll
+            for (int j = 0; j < B; ++j) r[j] = nx[j];
+            load_batch(k0 + B, nx);  // (past ke: sentinels or the next thread's runs, only nx[0].start is used)
+            r[B] = nx[0];
             uint32_t pos[B];
 #pragma unroll
             for (int j = 0; j < B; ++j) {
