@@ -47,6 +47,18 @@ SPK_HD int fadd(int a, int b) {  // a + b
     return a + b;
 #endif
 }
+// the same with the multiplier in a register of the caller (Scan keeps 1 and
+// -1 loaded once: inside the scan loop the constant-bank load sat on the
+// step's critical path)
+SPK_HD int fmad(int a, int m, int b) {  // a * m + b, m = 1 or -1
+#ifdef __CUDA_ARCH__
+    int r;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(m), "r"(b));
+    return r;
+#else
+    return a * m + b;
+#endif
+}
 SPK_HD int fsub(int a, int b) {  // a - b
 #ifdef __CUDA_ARCH__
     int r;
@@ -292,10 +304,15 @@ struct Scan {
     // SSR spike loop uses it when neither follows.
     template <bool FRAMES = true>
     SPK_HD bool step(int n, int& out_rs, int& out_cnt) {
-        const int t = fsub(n, last);
-        const int d = fsub(t, lo);
+#ifdef SPK_FSR_PLAIN_STEP
+        constexpr bool plain = METHOD == kFSR;
+#else
+        constexpr bool plain = false;
+#endif
+        const int t = plain ? n - last : fsub(n, last);
+        const int d = plain ? t - lo : fsub(t, lo);
         const bool in = (uint32_t)d <= hw;
-        const bool ext = (!in) & (hw == 0u) & ((uint32_t)fadd(d, 1) <= 2u);
+        const bool ext = (!in) & (hw == 0u) & ((uint32_t)(plain ? d + 1 : fadd(d, 1)) <= 2u);
         const bool fbrk = !(in | ext);
         bool brk = fbrk;
         bool emit = fbrk & (lo < kLim);
@@ -339,7 +356,7 @@ struct Scan {
         lo = fbrk ? t : lext;
         hw = fbrk ? 0u : (hw | (uint32_t)ext);
         rs = brk ? last : rs;
-        cnt = brk ? 1 : fadd(cnt, 1);
+        cnt = brk ? 1 : (plain ? cnt + 1 : fadd(cnt, 1));
         last = n;
         return emit;
     }
@@ -545,7 +562,6 @@ SPK_HD int fsr_batch(SC& sc, WORD&& word, int base0, int& cpos, EMIT&& emit) {
     int pv = sc.last + lo;
     uint32_t R[N], V[N], c[N];
     int PV[N];
-    uint32_t nz = 1u << N;
 #pragma unroll
     for (int j = 0; j < N; ++j) {
         const uint32_t w = word(j);
@@ -560,9 +576,12 @@ SPK_HD int fsr_batch(SC& sc, WORD&& word, int base0, int& cpos, EMIT&& emit) {
         pv = bit_selp(r != 0u, base + lo + 32 - bit_ffs(r), pv);
         R[j] = r;
         c[j] = (uint32_t)bit_popc(r);
-        nz |= (uint32_t)(V[j] != 0u) << j;
     }
-    const int k = bit_ffs(nz) - 1;
+    // first word with a violation (N: none), as a chain of selects from the
+    // last word down (no bit scan over a flag word)
+    int k = N;
+#pragma unroll
+    for (int j = N - 1; j >= 0; --j) k = V[j] != 0u ? j : k;
     const bool ev = k < N;
     const int kk = ev ? k : N - 1;
     uint32_t Vk = V[0], rk = R[0], before = 0u;
