@@ -143,18 +143,42 @@ struct Scratch {
 };
 
 
+// warps per K2 block: kSegWarpsWide when FSR fits one wave and those blocks
+// leave fewer warps on the busiest SM (W * ceil(blocks / SMs)), else kSegWarps
+int seg_warps_for(int method, int64_t nwords, unsigned shards) {
+#ifdef SPK_SEG_WARPS_FIXED
+    (void)method; (void)nwords; (void)shards;
+    return kSegWarps;
+#else
+    if (method != SPK_FSR || shards != 1) return kSegWarps;
+    static int sms = [] {
+        int dev = 0, n = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return std::max(n, 1);
+    }();
+    auto busiest = [&](int w, int per_sm) -> int64_t {  // -1: more than one wave
+        const int64_t blocks = (nwords + w - 1) / w;
+        return blocks <= (int64_t)sms * per_sm ? w * ((blocks + sms - 1) / sms) : -1;
+    };
+    const int64_t b8 = busiest(kSegWarps, 3), b11 = busiest(kSegWarpsWide, 2);
+    return b8 > 0 && b11 > 0 && b11 < b8 ? kSegWarpsWide : kSegWarps;
+#endif
+}
+
 int launch_segment(int method, const SegArgs& a, cudaStream_t s) {
     const int64_t nwords = (a.npix + 31) / 32;
-    const int64_t threads = nwords * 32;
-    const unsigned blocks = (unsigned)((threads + kSegThreads - 1) / kSegThreads);
-    const size_t smem = (size_t)kSegWarps * kRing * 32 * sizeof(uint32_t);  // the warps' rings
-    auto go = [&](auto kern) -> int {
+    const unsigned shards = a.shard_frames > 0 ? (unsigned)((a.frames + a.shard_frames - 1) / a.shard_frames) : 1u;
+    auto go = [&](auto kern, int warps) -> int {
+        const size_t smem = (size_t)warps * kRing * 32 * sizeof(uint32_t);  // the warps' rings
+        const unsigned blocks = (unsigned)((nwords + warps - 1) / warps);
         SPK_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        const unsigned shards = a.shard_frames > 0 ? (unsigned)((a.frames + a.shard_frames - 1) / a.shard_frames) : 1u;
-        kern<<<dim3(blocks, shards), kSegThreads, smem, s>>>(a);
+        kern<<<dim3(blocks, shards), warps * 32, smem, s>>>(a);
         return SPK_OK;
     };
-    int rc = method == SPK_FSR ? go(k_segment<kFSR>) : go(k_segment<kSSR>);
+    const int warps = a.flags != nullptr ? kSegWarps : seg_warps_for(method, nwords, shards);
+    int rc = method == SPK_FSR ? (warps == kSegWarpsWide ? go(k_segment<kFSR, kSegWarpsWide>, warps)
+                                                         : go(k_segment<kFSR, kSegWarps>, warps))
+                               : go(k_segment<kSSR, kSegWarps>, kSegWarps);
     if (rc) return rc;
     SPK_LAUNCHED("k_segment");
     return SPK_OK;

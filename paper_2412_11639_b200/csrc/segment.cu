@@ -43,11 +43,11 @@ __device__ __forceinline__ void st_run_if(bool pred, spk_run_t* addr, int rs, in
 
 }  // namespace
 
-template <int METHOD>
-__global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
+template <int METHOD, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_segment(SegArgs a) {
     // transposed words of each warp: ring of kRing 32-frame words per lane
     extern __shared__ uint32_t seg_smem[];
-    __shared__ int prog[kSegWarps];  // per warp: earliest group still to be read
+    __shared__ int prog[WARPS];  // per warp: earliest group still to be read
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int64_t word = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
         for (;;) {
             int mn = 0x7fffffff;
 #pragma unroll
-            for (int i = 0; i < kSegWarps; ++i) mn = min(mn, vprog[i]);
+            for (int i = 0; i < WARPS; ++i) mn = min(mn, vprog[i]);
             if (front - mn <= (METHOD == kFSR ? kDriftFsr : kDriftSsr)) break;
             __nanosleep(256);
         }
@@ -308,8 +308,9 @@ __global__ void __launch_bounds__(kSegThreads) k_segment(SegArgs a) {
     }
 }
 
-template __global__ void k_segment<kFSR>(SegArgs);
-template __global__ void k_segment<kSSR>(SegArgs);
+template __global__ void k_segment<kFSR, kSegWarps>(SegArgs);
+template __global__ void k_segment<kSSR, kSegWarps>(SegArgs);
+template __global__ void k_segment<kFSR, kSegWarpsWide>(SegArgs);
 
 // ---------------------------------------------------------------- fixup ----
 // Pixels whose run list overflowed `cap`: rescan the pixel and write its

@@ -1,0 +1,5 @@
+for shp in "moving 400 250 40000 fsr,ssr" "static 400 250 20000 fsr" "moving 400 250 4000 fsr" "range 400 250 200000 fsr"; do
+  echo "== new"; timeout 300 python profiles/phases.py $shp
+done
+timeout 600 python profiles/c4_probe.py 2>&1 | tail -6
+python -m pytest tests/test_gpu_parity.py tests/test_split.py tests/test_time_shards.py -x -q 2>&1 | tail -3
