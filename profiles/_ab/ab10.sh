@@ -1,0 +1,4 @@
+for shp in "moving 400 250 40000 fsr" "sensor 1000 1000 20000 fsr" "static 400 250 20000 fsr" "moving 400 250 4000 fsr" "range 400 250 60000 fsr"; do
+  for v in tw0 tw1; do echo "== $v"; SPK_PROBE_LIB=profiles/_ab/lib_$v.so timeout 300 python profiles/phases.py $shp; done
+done
+python -m pytest tests/test_gpu_parity.py tests/test_split.py -x -q 2>&1 | tail -3
