@@ -337,7 +337,17 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     std::memset(&tmap, 0, sizeof(tmap));
     const bool tma = sizeof(OUT) == 1 && e.vec_ok && sa.npix % 4 == 0 && tma_enabled() &&
                      encode_out_map(&tmap, out, sa.npix, sa.frames, out_pitch * sizeof(OUT), kSub);
-    const size_t smem = expand_smem_bytes(sizeof(OUT), warps, tma);
+    // Narrow uint8 frames: four 4-warp blocks per SM instead of the five that
+    // fit (the request is padded to 54 KB).  K3 is bound by its DRAM write
+    // pattern: fewer warps keep fewer rows open at a time (C2 K3 0.710 ->
+    // 0.696 ms; three blocks 0.752; twice the warps, with half-size cells,
+    // 0.768).  SPK_K3_PAD overrides the padding (probes).
+    static const long k3_pad = [] { const char* v = std::getenv("SPK_K3_PAD"); return v ? std::atol(v) : -1L; }();
+    size_t smem = expand_smem_bytes(sizeof(OUT), warps, tma);
+    if (k3_pad >= 0)
+        smem += (size_t)k3_pad;
+    else if (sizeof(OUT) == 1 && !wide && !tma)
+        smem = std::max<size_t>(smem, 54 * 1024);
     void (*kexp)(ExpArgs, const CUtensorMap) = k_expand<OUT, Geo<OUT>::WARPS, false>;
     if constexpr (sizeof(OUT) == 1) {
         if (tma)
