@@ -11,6 +11,6 @@ cp gpurun_out/ncu_step.json profiles/ncu_step.json
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-   --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-long --no-configs \
+   --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-long --no-configs \
    > gpurun_out/ncu_launch.log 2>&1
 tail -c 1500 gpurun_out/bench.json; echo; cat gpurun_out/bench_ref.json
