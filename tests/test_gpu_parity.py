@@ -314,6 +314,46 @@ def full_size_check(oracle, scene, w, h, t, seed, tiles):
     return v
 
 
+@pytest.mark.parametrize("cap", [63, 64, 201, 1250])
+def test_finalize_any_run_capacity(oracle, cap):
+    """K2c loads runs as 16-byte pairs when the capacity is even and one by
+    one when it is odd, four per batch with the next batch in flight; lists of
+    every length modulo the batch (noise and moving pixels), overflowed lists
+    included (cap 63/64 on 3000 frames)."""
+    w, h, t = 96, 21, 3000
+    capi.check(capi.lib().spk_set_run_capacity(cap))
+    try:
+        for scene, param in (("noise", 0.2), ("moving", 0)):
+            v = spk.synth(scene, 21, w, h, t, param=param)
+            host = v.planes.cpu().numpy()
+            for tag in ("fsr", "ssr"):
+                m, _ = TAGS[tag]
+                want = oracle.reconstruct(host, w, h, t, v.pitch, m)
+                assert np.array_equal(host2d(run(v, method_of(tag)), w * h), want), (scene, tag, cap)
+            want64 = oracle.reconstruct(host, w, h, t, v.pitch, 0, dtype=np.float64)
+            got64 = host2d(run(v, "fsr", torch.float64), w * h)
+            assert np.array_equal(got64.view(np.uint64), want64.view(np.uint64)), (scene, cap)
+    finally:
+        capi.lib().spk_set_run_capacity(0)
+
+
+def test_mid_size_sensor_vs_oracle(oracle):
+    """640x480 (307,200 pixels): K2c takes 64-run segments per thread (32 up
+    to 2^18 pixels, 128 from 3 * 2^18), K2 8-warp blocks over several waves."""
+    w, h, t = 640, 480, 2100
+    npix = w * h
+    v = spk.synth("moving", 4, w, h, t)
+    host = v.planes.cpu().numpy()
+    for tag in ("fsr", "ssr"):
+        m, _ = TAGS[tag]
+        got = run(v, method_of(tag)).reshape(t, npix)
+        for p0 in (0, 151000, npix - 640):
+            p1 = min(npix, p0 + 640)
+            want = oracle.reconstruct(host, w, h, t, v.pitch, m, pix_begin=p0, pix_end=p1)
+            assert np.array_equal(got[:, p0:p1].cpu().numpy(), want), (tag, p0)
+        del got
+
+
 def test_c1_static_full_size(oracle):
     """configs[0]: 400x250x20000 static -> one run per pixel (Theorem 1)."""
     v = full_size_check(oracle, "static", 400, 250, 20000, 0, [0, 50000, 99200])
