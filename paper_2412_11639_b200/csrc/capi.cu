@@ -169,7 +169,8 @@ int launch_segment(int method, const SegArgs& a, cudaStream_t s) {
     const int64_t nwords = (a.npix + 31) / 32;
     const unsigned shards = a.shard_frames > 0 ? (unsigned)((a.frames + a.shard_frames - 1) / a.shard_frames) : 1u;
     auto go = [&](auto kern, int warps) -> int {
-        const size_t smem = (size_t)warps * kRing * 32 * sizeof(uint32_t);  // the warps' rings
+        // the warps' rings (+ SSR: their parity-slot records)
+        const size_t smem = (size_t)warps * (kRing * 32 * sizeof(uint32_t) + (method == SPK_SSR ? kSsrSlotBytes : 0));
         const unsigned blocks = (unsigned)((nwords + warps - 1) / warps);
         SPK_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<dim3(blocks, shards), warps * 32, smem, s>>>(a);
@@ -337,8 +338,9 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     std::memset(&tmap, 0, sizeof(tmap));
     const bool tma = sizeof(OUT) == 1 && e.vec_ok && sa.npix % 4 == 0 && tma_enabled() &&
                      encode_out_map(&tmap, out, sa.npix, sa.frames, out_pitch * sizeof(OUT), kSub);
-    // Narrow uint8 frames: four 4-warp blocks per SM instead of the five that
-    // fit (the request is padded to 54 KB).  K3 is bound by its DRAM write
+    // Narrow uint8 frames, FSR run lists: four 4-warp blocks per SM instead of
+    // the five that fit (the request is padded to 54 KB; SSR's denser change
+    // stream wants the five: C2 SSR K3 0.808 vs 0.842 ms).  K3 is bound by its DRAM write
     // pattern: fewer warps keep fewer rows open at a time (C2 K3 0.710 ->
     // 0.696 ms; three blocks 0.752; twice the warps, with half-size cells,
     // 0.768).  SPK_K3_PAD overrides the padding (probes).
@@ -346,7 +348,7 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
     size_t smem = expand_smem_bytes(sizeof(OUT), warps, tma);
     if (k3_pad >= 0)
         smem += (size_t)k3_pad;
-    else if (sizeof(OUT) == 1 && !wide && !tma)
+    else if (sizeof(OUT) == 1 && !wide && !tma && !sa.dense_runs)
         smem = std::max<size_t>(smem, 54 * 1024);
     void (*kexp)(ExpArgs, const CUtensorMap) = k_expand<OUT, Geo<OUT>::WARPS, false>;
     if constexpr (sizeof(OUT) == 1) {
@@ -663,6 +665,7 @@ int reconstruct_impl(const spk_geom* g, const void* planes, int method, int wind
     // every size (K2 fills the SMs, so K3 of part k only runs in the gaps of
     // part k+1: C3 FSR 9.72 vs 9.34 ms, SSR 25.5 vs 24.5 ms).
     mark(0, s);
+    a.dense_runs = method == SPK_SSR;
     if ((rc = launch_segment(method, a, s))) return rc;
     if ((rc = expand_parts<OUT>(a, out, out_pitch, s))) return rc;
     mark(3, s);

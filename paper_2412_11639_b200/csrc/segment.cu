@@ -25,6 +25,10 @@
 #define SPK_SSR_REPS 3  // SSR bulk mode: words (or events) per pass of its loop head (3: C3 SSR -1% vs 2)
 #endif
 
+#ifndef SPK_SSR_SLOTS_SMEM
+#define SPK_SSR_SLOTS_SMEM 1  // SSR spike loop: parity slots in shared memory (Scan::step_mem)
+#endif
+
 #include "spk_fsm.cuh"
 #include "spk_kernels.cuh"
 
@@ -105,6 +109,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_segment(SegArgs a) {
         o_rs = e ? rs + fbase : o_rs;
         o_cnt = e ? cnt : o_cnt;
         st_run_if(e & (nrun <= capm1), wp, o_rs, o_cnt);
+        wp += (int)e;
+        nrun += (int)e;
+    };
+
+    // The same for the SSR spike loop (integer-pipe bound): the store reads
+    // the step's own copies of (rs, cnt) -- no selects into o_rs / o_cnt --
+    // and the frame offset is added on the FMA pipe.
+    auto emit_now = [&](bool e, int rs, int cnt) {
+        st_run_if(e & (nrun <= capm1), wp, fadd(rs, fbase), cnt);
         wp += (int)e;
         nrun += (int)e;
     };
@@ -212,9 +225,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_segment(SegArgs a) {
         if (ev <= kSsrDense * 32 * probe) {
             bulk(ngroups);
         } else {  // lanes all stand at word `probe`
-            // the frame fields of the state matter only for a saved state
+            // the frame fields of the state matter only for a saved state;
+            // without one the parity slots move to shared memory (step_mem:
+            // [parity][lane] 16-byte records behind the block's rings)
+            char* const slots = reinterpret_cast<char*>(seg_smem + (size_t)WARPS * kRing * 32) +
+                                (size_t)wid * kSsrSlotBytes + lane * 16;
+            auto slot = [&](int k) -> int4& { return *reinterpret_cast<int4*>(slots + (k << 9)); };
             auto run_spikes = [&](auto frames) {
                 constexpr bool FR = decltype(frames)::value;
+                if constexpr (!FR && SPK_SSR_SLOTS_SMEM) sc.store_slots(slot);
                 auto spikes = [&](int g) {
                     uint32_t w = rg[g & (kRing - 1)][lane];
                     const int base = g * 32;
@@ -222,8 +241,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_segment(SegArgs a) {
                         const int c = __clz(w);
                         w ^= 0x80000000u >> c;
                         int rs, cnt;
-                        const bool e = sc.template step<FR>(base + c, rs, cnt);
-                        emit(e, rs, cnt);
+                        bool e;
+                        if constexpr (!FR && SPK_SSR_SLOTS_SMEM) {
+                            e = sc.step_mem(base + c, slot, rs, cnt);
+                            emit_now(e, rs, cnt);
+                        } else {
+                            e = sc.template step<FR>(base + c, rs, cnt);
+                            emit(e, rs, cnt);
+                        }
                     }
                 };
                 int g = probe;

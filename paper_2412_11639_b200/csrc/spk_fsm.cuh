@@ -361,6 +361,68 @@ struct Scan {
         return emit;
     }
 
+    // SSR: the same step with the two parity slots in memory instead of
+    // registers -- slot(k) is the {last index, gap pair low, gap pair width,
+    // -} record of parity k (K2's spike loop keeps them in shared memory:
+    // one 16-byte load and one 16-byte store replace the 18 FMA-pipe
+    // multiply-adds that select and write back l/g/h by parity; the scan is
+    // issue-bound).  Only the slot of this interval's parity is read and
+    // written, as in step().  The frame fields (fl0, fl1, sf) are not kept:
+    // for loops that neither save the state nor return to the bulk test.
+    // store_slots / load_slots move the register slots in and out.
+    template <class SLOT>
+    SPK_HD bool step_mem(int n, SLOT&& slot, int& out_rs, int& out_cnt) {
+        static_assert(METHOD == kSSR, "parity slots are SSR state");
+        const int t = fsub(n, last);
+        const int d = fsub(t, lo);
+        const bool in = (uint32_t)d <= hw;
+        const bool ext = (!in) & (hw == 0u) & ((uint32_t)fadd(d, 1) <= 2u);
+        const bool fbrk = !(in | ext);
+        int4& sl = slot(t & 1);
+        const int4 s = sl;
+        const int l = s.x, glo = s.y;
+        const uint32_t ghw = (uint32_t)s.z;
+        const bool stale = l < sub0;
+        const int gap = fsub(ii, l);
+        const int gd = fsub(gap, glo);
+        const bool gnone = glo >= kLim;
+        const bool gempty = stale | gnone;
+        const bool gin = (!gempty) & ((uint32_t)gd <= ghw);
+        const bool gext = (!gempty) & (!gin) & (ghw == 0u) & ((uint32_t)fadd(gd, 1) <= 2u);
+        const bool sbrk = (!fbrk) & (!gempty) & (!gin) & (!gext);
+        const bool brk = fbrk | sbrk;
+        const bool emit = (fbrk & (lo < kLim)) | sbrk;
+        const bool fresh = stale | brk;
+        const int keep = gext ? min(glo, gap) : glo;
+        const int nglo = fresh ? kNoPair : (gnone ? gap : keep);
+        // (selects on the predicates themselves: no predicate -> integer moves
+        // on the integer pipe, which bounds this loop)
+        const uint32_t nghw = (fresh | gnone) ? 0u : (gext ? 1u : ghw);
+        sl = make_int4(ii, nglo, (int)nghw, 0);
+        sub0 = brk ? ii : sub0;
+        ii = fadd(ii, 1);
+        out_rs = rs;
+        out_cnt = cnt;
+        const int lext = ext ? min(lo, t) : lo;
+        lo = fbrk ? t : lext;
+        hw = fbrk ? 0u : (ext ? 1u : hw);
+        rs = brk ? last : rs;
+        cnt = brk ? 1 : fadd(cnt, 1);
+        last = n;
+        return emit;
+    }
+    template <class SLOT>
+    SPK_HD void store_slots(SLOT&& slot) const {
+        slot(0) = make_int4(l0, g0, (int)h0, 0);
+        slot(1) = make_int4(l1, g1, (int)h1, 0);
+    }
+    template <class SLOT>
+    SPK_HD void load_slots(SLOT&& slot) {
+        const int4 a = slot(0), b = slot(1);
+        l0 = a.x; g0 = a.y; h0 = (uint32_t)a.z;
+        l1 = b.x; g1 = b.y; h1 = (uint32_t)b.z;
+    }
+
     // open run at end of stream (valid when at least one interval was seen)
     SPK_HD bool tail(int& out_rs, int& out_cnt) const {
         out_rs = rs;

@@ -37,6 +37,7 @@ constexpr int kSegWarpsWide = 11;
 constexpr int kDriftFsr = 48;
 constexpr int kDriftSsr = 160;
 constexpr int kBatch = 8;        // 32-frame groups per prefetch batch
+constexpr int kSsrSlotBytes = 2 * 32 * 16;  // SSR: per warp, [parity][lane] 16-byte slot records (shared memory)
 constexpr int kSsrProbe = 64;    // SSR: words scanned in bulk mode before choosing the mode
 #ifndef SPK_SSR_DENSE
 #define SPK_SSR_DENSE 2
@@ -63,6 +64,7 @@ struct SegArgs {
     spk_run_t* runs;
     uint32_t* counts;
     int32_t* last;
+    int dense_runs = 0;  // host hint for K3: many runs per pixel expected (SSR lists)
     const int32_t* state_in = nullptr;  // time shards: automaton state at frame 0
     int32_t* state_out = nullptr;       //              state after the last frame
     // Several time shards in one launch (blockIdx.y = shard r, fresh state):

@@ -228,6 +228,47 @@ extern "C" long quiet_runs(const uint8_t* bits, long frames, int method, long* s
     return n;
 }
 
+// Scan<kSSR>::step_mem (parity slots in memory, as in K2's SSR spike loop);
+// the first `warm` spikes go through step() so the slots move from registers
+// to memory with some state in them.  FSR: the plain step.
+extern "C" long scanmem_runs(const uint8_t* bits, long frames, int method, long* start, long* end,
+                             long* cnt, long cap) {
+    if (method == 0) return scan_runs(bits, frames, method, start, end, cnt, cap);
+    long n = 0, last = -1, seen = 0;
+    const long warm = frames % 7;
+    spk::Scan<spk::kSSR> sc;
+    sc.init();
+    int4 slots[2];
+    auto slot = [&](int k) -> int4& { return slots[k]; };
+    auto put = [&](bool e, int rs, int c) {
+        if (!e) return;
+        if (n < cap) {
+            start[n] = rs;
+            cnt[n] = c;
+        }
+        ++n;
+    };
+    for (long f = 0; f < frames; ++f) {
+        if (!bits[f]) continue;
+        int rs, c;
+        bool e;
+        if (seen < warm) {
+            e = sc.step((int)f, rs, c);
+        } else {
+            if (seen == warm) sc.store_slots(slot);
+            e = sc.step_mem((int)f, slot, rs, c);
+        }
+        put(e, rs, c);
+        ++seen;
+        last = f;
+    }
+    int rs, c;
+    const bool e = sc.tail(rs, c);
+    put(e, rs, c);
+    for (long k = 0; k < n && k < cap; ++k) end[k] = (k + 1 < n) ? start[k + 1] : last;
+    return n;
+}
+
 // the u8 run-value rule as compiled for the kernels
 extern "C" void host_run_u8(const uint32_t* n, const uint32_t* span, uint32_t* out, long m) {
     for (long i = 0; i < m; ++i) out[i] = spk::run_u8(n[i], span[i]);

@@ -42,6 +42,8 @@ def fsm():
     h.ssr_state_check.argtypes = [C.c_void_p, C.c_long]
     h.ssrword_runs.restype = C.c_long
     h.ssrword_runs.argtypes = h.fsm_runs.argtypes
+    h.scanmem_runs.restype = C.c_long
+    h.scanmem_runs.argtypes = h.fsm_runs.argtypes
 
     def make(fn):
         def run(bits, m):
@@ -53,7 +55,7 @@ def fsm():
         return run
     return {"fsm": make(h.fsm_runs), "scan": make(h.scan_runs), "word": make(h.word_runs),
             "batch": make(h.batch_runs), "quiet": make(h.quiet_runs),
-            "ssrword": make(h.ssrword_runs), "_h": h}
+            "ssrword": make(h.ssrword_runs), "scanmem": make(h.scanmem_runs), "_h": h}
 
 
 def if_stream(rng, t, segs, flips):
@@ -69,7 +71,7 @@ def if_stream(rng, t, segs, flips):
     return b ^ (rng.random(t) < flips).astype(np.uint8)
 
 
-@pytest.mark.parametrize("kind", ["fsm", "scan", "word", "batch", "quiet", "ssrword"])
+@pytest.mark.parametrize("kind", ["fsm", "scan", "word", "batch", "quiet", "ssrword", "scanmem"])
 @pytest.mark.parametrize("family", ["noise", "if", "if_noisy", "if_rare_flips"])
 def test_fsm_matches_oracle(fsm, oracle, family, kind):
     run = fsm[kind]
@@ -86,7 +88,7 @@ def test_fsm_matches_oracle(fsm, oracle, family, kind):
             assert all(np.array_equal(x, y) for x, y in zip(got, want)), (family, m, t)
 
 
-@pytest.mark.parametrize("kind", ["fsm", "scan", "word", "batch", "quiet", "ssrword"])
+@pytest.mark.parametrize("kind", ["fsm", "scan", "word", "batch", "quiet", "ssrword", "scanmem"])
 def test_fsm_golden_rows(fsm, golden_dir, kind):
     z = np.load(golden_dir / "rows.npz")
     for name in sorted({k.split("/")[0] for k in z.files}):
