@@ -373,11 +373,16 @@ struct Scan {
     template <class SLOT>
     SPK_HD bool step_mem(int n, SLOT&& slot, int& out_rs, int& out_cnt) {
         static_assert(METHOD == kSSR, "parity slots are SSR state");
+        // The loop this runs in is bound by the integer pipe (compares,
+        // selects), so the pair tests are folded: a pair of width w accepts
+        // d in {0, w} and, while w = 0, completes on d = +-1 -- together
+        // (unsigned)(d + 1 - w) <= 2 - w, one compare; the additions go to
+        // the FMA pipe.  Same decisions as step() for every 32-bit d.
         const int t = fsub(n, last);
         const int d = fsub(t, lo);
-        const bool in = (uint32_t)d <= hw;
-        const bool ext = (!in) & (hw == 0u) & ((uint32_t)fadd(d, 1) <= 2u);
-        const bool fbrk = !(in | ext);
+        const int c1 = fsub(1, (int)hw);
+        const bool fbrk = (uint32_t)fadd(d, c1) > (uint32_t)fadd(c1, 1);
+        const bool ext = (!fbrk) & ((uint32_t)d > hw);
         int4& sl = slot(t & 1);
         const int4 s = sl;
         const int l = s.x, glo = s.y;
@@ -387,16 +392,17 @@ struct Scan {
         const int gd = fsub(gap, glo);
         const bool gnone = glo >= kLim;
         const bool gempty = stale | gnone;
-        const bool gin = (!gempty) & ((uint32_t)gd <= ghw);
-        const bool gext = (!gempty) & (!gin) & (ghw == 0u) & ((uint32_t)fadd(gd, 1) <= 2u);
-        const bool sbrk = (!fbrk) & (!gempty) & (!gin) & (!gext);
+        const int e1 = fsub(1, (int)ghw);
+        const bool gbad = (uint32_t)fadd(gd, e1) > (uint32_t)fadd(e1, 1);
+        const bool gext = (!gempty) & (!gbad) & ((uint32_t)gd > ghw);
+        const bool sbrk = (!fbrk) & (!gempty) & gbad;
         const bool brk = fbrk | sbrk;
-        const bool emit = (fbrk & (lo < kLim)) | sbrk;
+        // (no interval yet, lo >= kLim, is a first-order break that emits nothing)
+        const bool emit = brk & (lo < kLim);
         const bool fresh = stale | brk;
         const int keep = gext ? min(glo, gap) : glo;
         const int nglo = fresh ? kNoPair : (gnone ? gap : keep);
-        // (selects on the predicates themselves: no predicate -> integer moves
-        // on the integer pipe, which bounds this loop)
+        // (selects on the predicates themselves: no predicate -> integer moves)
         const uint32_t nghw = (fresh | gnone) ? 0u : (gext ? 1u : ghw);
         sl = make_int4(ii, nglo, (int)nghw, 0);
         sub0 = brk ? ii : sub0;
