@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_segment(SegArgs a) {
         int wi = -1;  // word of this lane (its ring slot may be reused)
         uint32_t So = 0u, S = 0u;
         int prevlast = kNoSpike;
-        int events = 0;
+        int events = 0, nspk = 0;  // this lane's exact steps / spikes so far (the mode choice below)
         auto bulk = [&](int limit) {
             for (;;) {
                 const bool more = wi + 1 < limit;
@@ -199,6 +199,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_segment(SegArgs a) {
                         ++wi;
                         So = S = rg[wi & (kRing - 1)][lane];
                         prevlast = sc.last;
+                        nspk += __popc(So);
                     }
                     if (S) {
                         const int base = wi * 32;
@@ -221,8 +222,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_segment(SegArgs a) {
         };
         const int probe = min(ngroups, kSsrProbe);
         bulk(probe);
-        const int ev = __reduce_add_sync(kFull, (unsigned)events);
-        if (ev <= kSsrDense * 32 * probe) {
+        // Mode for the rest of the stream, from the probe's busiest lanes:
+        // bulk mode pays a pass (~kSsrBulkCost instructions) per word and per
+        // event of its busiest lane, the spike loop a step (~kSsrStepCost)
+        // per spike of the busiest lane plus a per-word overhead.  Bright
+        // pixels with few events stay in bulk mode, dim or eventful ones
+        // take the spike loop.
+        const int emax = (int)__reduce_max_sync(kFull, (unsigned)events);
+        const int smax = (int)__reduce_max_sync(kFull, (unsigned)nspk);
+        if (kSsrBulkCost * (probe + emax) <= kSsrStepCost * smax + kSsrWordCost * probe) {
             bulk(ngroups);
         } else {  // lanes all stand at word `probe`
             // the frame fields of the state matter only for a saved state;

@@ -39,10 +39,12 @@ constexpr int kDriftSsr = 160;
 constexpr int kBatch = 8;        // 32-frame groups per prefetch batch
 constexpr int kSsrSlotBytes = 2 * 32 * 16;  // SSR: per warp, [parity][lane] 16-byte slot records (shared memory)
 constexpr int kSsrProbe = 64;    // SSR: words scanned in bulk mode before choosing the mode
-#ifndef SPK_SSR_DENSE
-#define SPK_SSR_DENSE 2
+#ifndef SPK_SSR_CB
+#define SPK_SSR_CB 250
 #endif
-constexpr int kSsrDense = SPK_SSR_DENSE;  // SSR: events per lane-word above which spike mode wins
+constexpr int kSsrBulkCost = SPK_SSR_CB;  // SSR mode choice: instructions per bulk pass (word or event) ...
+constexpr int kSsrStepCost = 63;          // ... per spike-loop step ...
+constexpr int kSsrWordCost = 15;          // ... and per spike-loop word
 // transposed words buffered per lane (bounds lane drift); 32 keeps the rings
 // at 32 KB per block, which leaves L1 room for the plane sectors the block's
 // warps share (64: C3 K2 4.01 vs 3.82 ms)
