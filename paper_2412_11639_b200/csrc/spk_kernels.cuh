@@ -35,7 +35,10 @@ constexpr int kSegWarpsWide = 11;
 // method (measured: FSR 48 vs 96 -- C5 K2 -3%, C3 -2%; SSR 160 vs 96 --
 // C3 SSR K2 -1%)
 constexpr int kDriftFsr = 48;
-constexpr int kDriftSsr = 160;
+#ifndef SPK_DRIFT_SSR
+#define SPK_DRIFT_SSR 160
+#endif
+constexpr int kDriftSsr = SPK_DRIFT_SSR;
 constexpr int kBatch = 8;        // 32-frame groups per prefetch batch
 constexpr int kSsrSlotBytes = 2 * 32 * 16;  // SSR: per warp, [parity][lane] 16-byte slot records (shared memory)
 constexpr int kSsrProbe = 64;    // SSR: words scanned in bulk mode before choosing the mode
