@@ -252,17 +252,22 @@ __global__ void __launch_bounds__(WARPS * 32) k_segment(SegArgs a) {
                 if constexpr (!FR && SPK_SSR_SLOTS_SMEM) sc.store_slots(slot);
                 auto spikes = [&](int g) {
                     uint32_t w = rg[g & (kRing - 1)][lane];
-                    const int base = g * 32;
+                    // the word is shifted past each spike (one funnel shift on
+                    // the integer pipe; the frame bookkeeping on the FMA pipe)
+                    int pos = g * 32;  // frame of bit 31 of w
                     while (w) {
                         const int c = __clz(w);
-                        w ^= 0x80000000u >> c;
+                        const int n = fadd(pos, c);
+                        const int c1 = fadd(c, 1);
+                        w = bit_shl_clamp(w, (uint32_t)c1);
+                        pos = fadd(pos, c1);
                         int rs, cnt;
                         bool e;
                         if constexpr (!FR && SPK_SSR_SLOTS_SMEM) {
-                            e = sc.step_mem(base + c, slot, rs, cnt);
+                            e = sc.step_mem(n, slot, rs, cnt);
                             emit_now(e, rs, cnt);
                         } else {
-                            e = sc.template step<FR>(base + c, rs, cnt);
+                            e = sc.template step<FR>(n, rs, cnt);
                             emit(e, rs, cnt);
                         }
                     }
