@@ -22,7 +22,7 @@
 #include <type_traits>
 
 #ifndef SPK_SSR_REPS
-#define SPK_SSR_REPS 3  // SSR bulk mode: words (or events) per pass of its loop head (3: C3 SSR -1% vs 2)
+#define SPK_SSR_REPS 2  // SSR bulk mode: words (or events) per pass of its loop head (with the smaller spike loop: C3 SSR K2 12.12 ms at 2, 12.28 at 3, 12.45 at 1, 13.0 at 4)
 #endif
 
 #ifndef SPK_SSR_SPIKE_UNROLL
