@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kFinWarps * 32, 2) k_fin_bins(FinArgs a) {
     // meet in global memory, zeroed beforehand)
     const int share = GP / (int)gridDim.z;
     const int pl0 = (int)blockIdx.z * share, pl1 = pl0 + share;
-    for (int i = threadIdx.x; i < kFinWindow * kBins; i += blockDim.x) hist[i] = 0;
+    for (int i = threadIdx.x; i < (cw1 - cw0) * kBins; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     auto bin_start = [&](uint32_t sv) {
         const int st = (int)sv;
@@ -74,12 +74,35 @@ __global__ void __launch_bounds__(kFinWarps * 32, 2) k_fin_bins(FinArgs a) {
         if (sv != 0xffffffffu && c >= cw0 && c < cw1)
             atomicAdd(&hist[(c - cw0) * kBins + ((st & (kChunk - 1)) / kSub)], 1u);
     };
-    for (int pl = pl0 + warp; pl < pl1; pl += kFinWarps) {
-        const int64_t p = (int64_t)g * GP + pl;
-        if (p >= a.npix) break;
-        const spk_run_t* rp = a.runs + p * a.cap;
-        const int n = (int)min(a.counts[p], (uint32_t)a.cap);
-        if constexpr (!SPLIT) {  // one contiguous list: 128 runs per pass
+    if constexpr (!SPLIT) {
+        // One contiguous list per pixel.  The warp's pixels are pl0 + warp +
+        // j * kFinWarps: lane j loads the count of pixel j (one round trip
+        // for all of them instead of one per pixel), counts a short list
+        // (<= kShortList runs: static pixels hold one or two) by itself, and
+        // the longer lists are read by the whole warp, 128 runs per pass
+        // (lane k <- runs b + 32u + k).  K2b on a static 400x250 scene was
+        // 21 us of dependent count -> runs round trips.
+        static_assert(GP <= 32 * kFinWarps, "a warp's pixels fit one lane each");
+        constexpr int kShortList = 4;
+        const int npx = max(0, (share - warp + kFinWarps - 1) / kFinWarps);
+        int myn = 0;
+        const int64_t pj = (int64_t)g * GP + pl0 + warp + (int64_t)lane * kFinWarps;
+        if (lane < npx && pj < a.npix) myn = (int)min(a.counts[pj], (uint32_t)a.cap);
+        if (myn > 0 && myn <= kShortList) {
+            const spk_run_t* rp = a.runs + pj * a.cap;
+            uint32_t sv[kShortList];
+#pragma unroll
+            for (int k = 0; k < kShortList; ++k)
+                sv[k] = k < myn ? (uint32_t)max((int)rp[k].start, 0) : 0xffffffffu;
+#pragma unroll
+            for (int k = 0; k < kShortList; ++k) bin_start(sv[k]);
+        }
+        uint32_t todo = __ballot_sync(kFull, myn > kShortList);
+        while (todo) {  // warp-uniform
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int n = __shfl_sync(kFull, myn, j);
+            const spk_run_t* rp = a.runs + ((int64_t)g * GP + pl0 + warp + (int64_t)j * kFinWarps) * a.cap;
             for (int b = 0; b < n; b += 128) {
                 uint32_t sv[4];
 #pragma unroll
@@ -91,8 +114,14 @@ __global__ void __launch_bounds__(kFinWarps * 32, 2) k_fin_bins(FinArgs a) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) bin_start(sv[u]);
             }
-            continue;
-        } else {
+        }
+    } else {
+    for (int pl = pl0 + warp; pl < pl1; pl += kFinWarps) {
+        const int64_t p = (int64_t)g * GP + pl;
+        if (p >= a.npix) break;
+        const spk_run_t* rp = a.runs + p * a.cap;
+        const int n = (int)min(a.counts[p], (uint32_t)a.cap);
+        {
         // in-grid time split: the row's segments, 32-slot blocks of them four
         // per pass; lane r holds segment r (begin, end, first block index)
         const uint32_t* sg = a.seg + p * a.nseg * 2;
@@ -126,6 +155,7 @@ __global__ void __launch_bounds__(kFinWarps * 32, 2) k_fin_bins(FinArgs a) {
             for (int u = 0; u < 4; ++u) bin_start(sv[u]);
         }
         }
+    }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < (cw1 - cw0) * kBins; i += blockDim.x) {
