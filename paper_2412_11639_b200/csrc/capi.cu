@@ -242,6 +242,7 @@ struct ExpandWork {
     Scratch tblv, bins, offs, cursor, stream;
     int ngroups = 0;
     int64_t nbins = 0;
+    bool exact_stream = false;  // the change stream is allocated after the scan, at its exact length
     explicit ExpandWork(cudaStream_t s) : tblv(s), bins(s), offs(s), cursor(s), stream(s) {}
 };
 
@@ -254,7 +255,18 @@ int prepare_expand(SegArgs& sa, ExpandWork<OUT>& w, cudaStream_t s) {
     SPK_CK(w.bins.alloc((size_t)w.nbins * sizeof(uint32_t)));
     SPK_CK(w.offs.alloc((size_t)w.nbins * sizeof(uint32_t)));
     SPK_CK(w.cursor.alloc((size_t)w.nbins * sizeof(uint32_t)));
-    SPK_CK(w.stream.alloc((size_t)sa.npix * sa.cap * sizeof(Change<OUT>)));
+    // The change stream holds one entry per stored run: at most npix * cap,
+    // usually far fewer (a 1M-frame static stream: 12.5 GB worst case, ~0.2 GB
+    // of runs).  Large worst cases are allocated after the scan at the exact
+    // length -- one 8-byte read-back and a stream synchronisation, ~20 us on
+    // steps of several ms; small ones (and calls under stream capture, which
+    // may not synchronise) take the bound.
+    static const int64_t exact_from = test_limit("SPK_TEST_EXACT_STREAM", (int64_t)1 << 30);
+    cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
+    SPK_CK(cudaStreamIsCapturing(s, &cap_status));
+    const size_t worst = (size_t)sa.npix * sa.cap * sizeof(Change<OUT>);
+    w.exact_stream = (int64_t)worst >= exact_from && cap_status == cudaStreamCaptureStatusNone;
+    if (!w.exact_stream) SPK_CK(w.stream.alloc(worst));
     // chunks before a pixel's first run keep value 0
     SPK_CK(cudaMemsetAsync(w.tblv.p, 0, (size_t)sa.nchunks * sa.npix * sizeof(OUT), s));
     return SPK_OK;
@@ -296,6 +308,17 @@ int launch_expand(const SegArgs& sa, ExpandWork<OUT>& w, OUT* out, size_t out_pi
                          static_cast<uint32_t*>(w.cursor.p));
     if (rc) return rc;
     f.cursor = static_cast<uint32_t*>(w.cursor.p);
+    if (w.exact_stream) {  // entries = last offset + last bin
+        static thread_local uint32_t* h_tot = nullptr;
+        if (!h_tot) SPK_CK(cudaMallocHost(&h_tot, 2 * sizeof(uint32_t)));
+        SPK_CK(cudaMemcpyAsync(h_tot, f.offs + (w.nbins - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        SPK_CK(cudaMemcpyAsync(h_tot + 1, f.bins + (w.nbins - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        SPK_CK(cudaStreamSynchronize(s));
+        const int64_t total = (int64_t)h_tot[0] + h_tot[1];
+        SPK_CK(w.stream.alloc((size_t)std::max<int64_t>(total, 1) * sizeof(Change<OUT>)));
+        f.stream = w.stream.p;
+        f.stream_len = total;
+    }
     // threads stride over a pixel's kFinSeg-run blocks (grid.y <= 64: a
     // 1M-frame list of one run per pixel is not 500 block rows of exits)
     f.fin_seg = fin_seg_for(sa.npix);

@@ -53,3 +53,12 @@ def test_expand_in_pixel_parts():
 def test_fin_scatter_segment_slabs():
     # cap 3000 -> 47 run blocks of 64; grid.y limited to 5 -> each thread strides over ~10
     _run({"SPK_TEST_GRID_Y": "5"}, 3000)
+
+
+@pytest.mark.gpu
+def test_exact_length_change_stream():
+    # the change stream allocated after the scan at its exact length (the path
+    # of >= 1 GiB worst cases: 1000x1000 sensors, 1M-frame streams), forced on a
+    # small volume; also with pixel parts (each part reads back its own total)
+    _run({"SPK_TEST_EXACT_STREAM": "1"}, 1500)
+    _run({"SPK_TEST_EXACT_STREAM": "1", "SPK_TEST_PART_ENTRIES": "1000000"}, 700)
