@@ -187,7 +187,10 @@ constexpr int kPieces = kBins / kPieceSubs;  // K3 tiles per (group, chunk)
 #endif
 constexpr int kPieceSparse = SPK_PIECE_SPARSE;  // changes per pixel per chunk up to which
                                              // K3 tiles are 64 frames high (else 128)
-constexpr int kPieceDensity = 12;            // ... up to which 128 frames high (else 256)
+#ifndef SPK_PIECE_DENSITY
+#define SPK_PIECE_DENSITY 12
+#endif
+constexpr int kPieceDensity = SPK_PIECE_DENSITY;            // ... up to which 128 frames high (else 256)
 constexpr int kPieceDense = 48;              // ... above which K3 writes the chunk whole
 #ifndef SPK_PIECE_MAXG
 #define SPK_PIECE_MAXG 512
