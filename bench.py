@@ -47,10 +47,11 @@ def peaks():
 
 
 def build_sha16() -> str:
-    """SHA-256 (16 hex) of the sm_100a library this run loads."""
-    import hashlib
-    lib = ROOT / "paper_2412_11639_b200" / "libspikecam_b200.so"
-    return hashlib.sha256(lib.read_bytes()).hexdigest()[:16] if lib.exists() else "missing"
+    """Hash (16 hex) of the sources and flags the loaded sm_100a library was
+    built from (paper_2412_11639_b200.build.source_sha16: nvcc's output is not
+    byte-reproducible, so a build is identified by its sources)."""
+    from paper_2412_11639_b200.build import source_sha16
+    return source_sha16()
 
 
 def step_profile(lib_sha: str):

@@ -39,6 +39,24 @@ def sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu"))
 
 
+def source_sha16() -> str:
+    """SHA-256 (16 hex) of what libspikecam_b200.so is built from: the kernel
+    sources, the C-ABI header and the nvcc flags.  nvcc's output is not
+    byte-reproducible, so profiles are tied to a build by this hash
+    (bench.py, profiles/ncu_step_profile.py).  build_library() rebuilds the
+    library whenever a source is newer, so the library on disk is the build
+    of these sources."""
+    import hashlib
+    deps = sources() + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "spikecam_b200.h"]
+    if not LIB.exists():
+        return "missing"
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for d in deps:
+        h.update(d.name.encode())
+        h.update(d.read_bytes())
+    return h.hexdigest()[:16]
+
+
 def _stale(target: Path, deps: list[Path]) -> bool:
     if not target.exists():
         return True

@@ -38,7 +38,8 @@ def run(method: str) -> None:
     for _ in range(2):
         spk.reconstruct(vol, method, out=out)
     torch.cuda.synchronize()
-    print("ok", method, hashlib.sha256(LIB.read_bytes()).hexdigest()[:16])
+    from paper_2412_11639_b200.build import source_sha16
+    print("ok", method, source_sha16())
 
 
 def kernel_rows(rep: str):
@@ -79,7 +80,9 @@ def kernel_rows(rep: str):
 
 
 def summarize(reps, out=None):
-    d = {"build_sha16": hashlib.sha256(LIB.read_bytes()).hexdigest()[:16],
+    sys.path.insert(0, str(ROOT))
+    from paper_2412_11639_b200.build import source_sha16
+    d = {"build_sha16": source_sha16(),
          "source": "ncu --set full --clock-control none, one warm configs[1] step per method "
                    "(profiles/ncu_step_profile.py)"}
     for rep in reps:
