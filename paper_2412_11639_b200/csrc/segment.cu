@@ -228,7 +228,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_segment(SegArgs a) {
                 }
             }
         };
-        const int probe = min(ngroups, kSsrProbe);
+        // (short streams: an eighth of the stream, at least 16 words -- a 64-word
+        // probe is half of a 4,000-frame stream spent in what may be the slower mode)
+#ifndef SPK_SSR_PROBE_DIV
+#define SPK_SSR_PROBE_DIV 8
+#endif
+        const int probe = min(ngroups, min(kSsrProbe, max(16, ngroups / SPK_SSR_PROBE_DIV)));
         bulk(probe);
         // Mode for the rest of the stream, from the probe's busiest lanes:
         // bulk mode pays a pass (~kSsrBulkCost instructions) per word and per
