@@ -143,15 +143,14 @@ struct Scratch {
 };
 
 
-// warps per K2 block: kSegWarpsWide when the sensor fits one wave and those blocks
+// warps per K2 block: kSegWarpsWide when FSR fits one wave and those blocks
 // leave fewer warps on the busiest SM (W * ceil(blocks / SMs)), else kSegWarps
 int seg_warps_for(int method, int64_t nwords, unsigned shards) {
 #ifdef SPK_SEG_WARPS_FIXED
     (void)method; (void)nwords; (void)shards;
     return kSegWarps;
 #else
-    (void)method;  // (SSR gained the wide blocks with its smaller spike loop: C1 SSR K2 0.646 -> 0.622 ms)
-    if (shards != 1) return kSegWarps;
+    if (method != SPK_FSR || shards != 1) return kSegWarps;
     static int sms = [] {
         int dev = 0, n = 148;
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -180,8 +179,7 @@ int launch_segment(int method, const SegArgs& a, cudaStream_t s) {
     const int warps = a.flags != nullptr ? kSegWarps : seg_warps_for(method, nwords, shards);
     int rc = method == SPK_FSR ? (warps == kSegWarpsWide ? go(k_segment<kFSR, kSegWarpsWide>, warps)
                                                          : go(k_segment<kFSR, kSegWarps>, warps))
-                               : (warps == kSegWarpsWide ? go(k_segment<kSSR, kSegWarpsWide>, warps)
-                                                         : go(k_segment<kSSR, kSegWarps>, warps));
+                               : go(k_segment<kSSR, kSegWarps>, kSegWarps);
     if (rc) return rc;
     SPK_LAUNCHED("k_segment");
     return SPK_OK;

@@ -362,7 +362,6 @@ __global__ void __launch_bounds__(WARPS * 32) k_segment(SegArgs a) {
 template __global__ void k_segment<kFSR, kSegWarps>(SegArgs);
 template __global__ void k_segment<kSSR, kSegWarps>(SegArgs);
 template __global__ void k_segment<kFSR, kSegWarpsWide>(SegArgs);
-template __global__ void k_segment<kSSR, kSegWarpsWide>(SegArgs);
 
 // ---------------------------------------------------------------- fixup ----
 // Pixels whose run list overflowed `cap`: rescan the pixel and write its

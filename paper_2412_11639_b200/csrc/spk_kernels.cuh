@@ -26,11 +26,10 @@ using spk_stab_t = ::spk_stab;
 #endif
 constexpr int kSegThreads = SPK_SEG_THREADS;
 constexpr int kSegWarps = kSegThreads / 32;
-// Sensors that fit one wave: 11-warp blocks, two per SM.  400x250 is 3,125
-// warps on 148 SMs: 8-warp blocks put 24 warps on 95 SMs and 16 on the rest,
-// 11-warp blocks at most 22 on every SM (C2 FSR K2 0.83 -> 0.80 ms, C1 SSR K2
-// 0.646 -> 0.622 ms; many-wave sensors are slower with them: the blocks
-// straddle 32-byte sectors).
+// FSR on sensors that fit one wave: 11-warp blocks, two per SM.  400x250 is
+// 3,125 warps on 148 SMs: 8-warp blocks put 24 warps on 95 SMs and 16 on the
+// rest, 11-warp blocks at most 22 on every SM (C2 K2 0.83 -> 0.80 ms; SSR and
+// many-wave sensors are slower with them: the blocks straddle 32-byte sectors).
 constexpr int kSegWarpsWide = 11;
 // max groups a warp may produce ahead of its block's slowest warp, per
 // method (measured: FSR 48 vs 96 -- C5 K2 -3%, C3 -2%; SSR 160 vs 96 --
