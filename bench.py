@@ -383,8 +383,8 @@ def main():
         (CUDA events on the launch stream), its own algorithmic bytes (K2
         reads 0.125 B/px-frame, the finalize none, K3 writes 1 B/px-frame) over
         its time, and what binds it -- from the ncu --set full capture of this
-        very build (profiles/ncu_step_<method>.json, matched by the library's
-        SHA-256; null when the capture is of another build)."""
+        very build (profiles/ncu_step.json, matched by the hash of the library's
+        sources and flags; null when the capture is of another build)."""
         seg, fin, exp, fix = ph
         step_gbs = pxf * BYTES_PER_PXF / (ms_step * 1e-3) / 1e9
         kp = (prof or {}).get(method, {})
@@ -400,7 +400,8 @@ def main():
                    kern("finalize", fin, 0.0, "latency (scattered 4-B stores)"),
                    kern("k_expand", exp, pxf * 1.0, "HBM write"),
                    kern("k_fixup", fix, 0.0, "-")]
-        traffic = sum(v.get("dram_bytes", 0.0) for v in kp.values()) if kp else None
+        # ("finalize" is the aggregate of K2b + scans + K2c, already counted by name)
+        traffic = sum(v.get("dram_bytes", 0.0) for k, v in kp.items() if k != "finalize") if kp else None
         return {"bound": "hbm", "scope": "whole step (K2 + finalize + K3 + fixup)",
                 "achieved": step_gbs, "peak": peak, "unit": "GB/s", "frac": step_gbs / peak,
                 "traffic": traffic, "algorithmic_bytes": pxf * BYTES_PER_PXF,
