@@ -32,9 +32,10 @@ constexpr int kSegWarps = kSegThreads / 32;
 // many-wave sensors are slower with them: the blocks straddle 32-byte sectors).
 constexpr int kSegWarpsWide = 11;
 // max groups a warp may produce ahead of its block's slowest warp, per
-// method (measured: FSR 48 vs 96 -- C5 K2 -3%, C3 -2%; SSR 160 vs 96 --
-// C3 SSR K2 -1%)
-constexpr int kDriftFsr = 48;
+// method (measured: FSR 48 vs 96 -- C5 K2 -3%, C3 -2%; 40, the smallest
+// bound a warp cannot wait on itself with, vs 48 -- range-200k K2 1.82 ->
+// 1.76 ms, C1 0.202 -> 0.200; SSR 160 vs 96 -- C3 SSR K2 -1%)
+constexpr int kDriftFsr = 40;
 #ifndef SPK_DRIFT_SSR
 #define SPK_DRIFT_SSR 160
 #endif
